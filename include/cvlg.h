@@ -1,0 +1,155 @@
+/* cvlg — C ABI of the B200 (sm_100a) connected-vehicle ETL pipeline.
+ *
+ * Drop-in boundary for the reference pipeline API
+ *   std::vector<BatchFrame> cvl::run_pipeline(const SourceManifest&, const GridSpec&,
+ *       const FilterRules&, uint32_t n_partitions, uint32_t n_threads, PipelineStats*)
+ *   (reference: proj/include/cvl/aggregate.hpp:125-127, impl proj/src/aggregate.cpp:401-452)
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary. A C++ shim with the
+ * reference's exact signature lives in include/cvlg.hpp; the bindings a reference maintainer would
+ * add are shown in INTEGRATION.md.
+ *
+ * Output lattice (caller-owned, dense, little-endian u32 words):
+ *   planes    [T][8][R][C]: channels 0..3 = mean speed N,E,S,W as f32 bit patterns,
+ *                           channels 4..7 = distinct-journey volume N,E,S,W
+ *             (= BatchFrame::speed / ::volume, aggregate.hpp:46-57; this is also the block
+ *              payload of the .cvl1 container, lattice_store.hpp:14-19)
+ *   raw_count [T][4][R][C]: raw record counts per direction (BatchFrame::raw_count)
+ * Planes are row-major R x C with row 0 at lat_min. T = 1440/min_step, R/C from extent_bins.
+ *
+ * Errors: every entry point returns 0 on success, otherwise 1 + the ordinal of the reference's
+ * cvl::Err (proj/include/cvl/error.hpp:8-26), or one of the CVLG_E_* codes >= 100 for conditions
+ * the reference has no code for. cvlg_last_error() returns the message of the calling thread's
+ * last failure. Data problems are never errors: they are counted in cvlg_stats, exactly like the
+ * reference's PipelineStats (aggregate.hpp:112-121).
+ */
+#ifndef CVLG_H_
+#define CVLG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* cvl::Err + 1 (error.hpp:8-26) */
+enum cvlg_status {
+    CVLG_OK = 0,
+    CVLG_E_MISSING_ROOT = 1,
+    CVLG_E_BAD_CONFIG = 2,
+    CVLG_E_BAD_GRID = 3,
+    CVLG_E_ZERO_PARTITIONS = 4,
+    CVLG_E_OUT_OF_BOUNDS = 5,
+    CVLG_E_COMPONENT_OUT_OF_RANGE = 6,
+    CVLG_E_INDEX_OVERFLOW = 7,
+    CVLG_E_GRID_MISMATCH = 8,
+    CVLG_E_DIMS_MISMATCH = 9,
+    CVLG_E_NON_FINITE_VALUE = 10,
+    CVLG_E_IO = 11,
+    CVLG_E_BAD_MAGIC = 12,
+    CVLG_E_VERSION_UNSUPPORTED = 13,
+    CVLG_E_TRUNCATED_FILE = 14,
+    CVLG_E_BAD_CHANNEL = 15,
+    CVLG_E_TASK_FAILED = 16,
+    CVLG_E_DIVIDE_BY_ZERO = 17,
+    /* conditions without a reference equivalent */
+    CVLG_E_CUDA = 100,        /* CUDA runtime failure (no device, OOM, launch failure) */
+    CVLG_E_INVALID_ARG = 101, /* null pointer / inconsistent sizes */
+    CVLG_E_UNSUPPORTED = 102, /* e.g. > 4 direction bins (reference: UB), > 2^32-5 cells */
+    CVLG_E_INTERNAL = 103     /* a capacity invariant was violated (bug) */
+};
+
+/* GridSpec, field for field (proj/include/cvl/grid.hpp:21-41). Defaults: 36, 40.6, -95.8,
+ * -89.1, 0.1, 0.1, 5, 90, 0.0 (cvlg_default_grid). */
+typedef struct cvlg_grid_spec {
+    double lat_min, lat_max, lon_min, lon_max, lat_step, lon_step;
+    uint32_t min_step, dxn_step;
+    double dxn_offset;
+} cvlg_grid_spec;
+
+/* FilterRules (proj/include/cvl/aggregate.hpp:16-20). Defaults: 1, 1, 250.0. */
+typedef struct cvlg_filter_rules {
+    int32_t require_in_grid;
+    int32_t drop_missing;
+    double speed_ceiling;
+} cvlg_filter_rules;
+
+/* PipelineStats (aggregate.hpp:112-121) with the string-keyed maps flattened:
+ *   rejected[]: BadTimestamp, BadNumeric, MissingField, RangeViolation, BadHeader
+ *   filtered[]: OutOfGrid, SpeedCeiling, MissingField
+ *   stage_seconds[]: decode, dictionary+order, fold, finalize (device time, CUDA events) */
+typedef struct cvlg_stats {
+    uint64_t rows_read, parsed, duplicates_dropped, conflicting_duplicates, accepted;
+    uint64_t rejected[5];
+    uint64_t filtered[3];
+    double stage_seconds[4];
+} cvlg_stats;
+
+typedef struct cvlg_context cvlg_context;
+
+void cvlg_default_grid(cvlg_grid_spec* spec);
+void cvlg_default_rules(cvlg_filter_rules* rules);
+
+/* Validates like GridSpec::validate (grid.cpp:47-57) and returns the lattice dimensions
+ * T = batches, D = directions, R = rows, C = cols (grid.cpp:18-22, grid.hpp:33-36). */
+int cvlg_grid_dims(const cvlg_grid_spec* spec, uint32_t* T, uint32_t* D, uint32_t* R, uint32_t* C);
+
+/* One context per (host thread, device). Holds streams and grow-only HBM/pinned scratch so
+ * repeated calls do not allocate. device < 0 selects the current device. NULL on failure. */
+cvlg_context* cvlg_context_create(int device);
+void cvlg_context_destroy(cvlg_context* ctx);
+
+/* Replaces cvl::run_pipeline (aggregate.hpp:125-127). Shards are read from disk (n_threads
+ * reader threads, 0 = hardware concurrency) into pinned memory, ranked by lexicographic path
+ * (aggregate.cpp:389-397), streamed to HBM and processed on the GPU. n_partitions is validated
+ * (0 -> CVLG_E_ZERO_PARTITIONS) and otherwise cannot change the output: the result is
+ * byte-identical for every partition count, like the reference's. planes / raw_count may be
+ * NULL. ctx may be NULL (a thread-local default context is used). */
+int cvlg_run_pipeline(cvlg_context* ctx, const char* const* shard_paths, size_t n_shards,
+                      const cvlg_grid_spec* spec, const cvlg_filter_rules* rules,
+                      uint32_t n_partitions, uint32_t n_threads, uint32_t* planes,
+                      uint32_t* raw_count, cvlg_stats* stats);
+
+/* Same pipeline over shard bytes already in host memory (pinned or pageable), given in rank
+ * order (index i = provenance rank i). Host->device copies are chunked, line-aligned and
+ * overlapped with decode. */
+int cvlg_run_pipeline_host(cvlg_context* ctx, const uint8_t* const* shard_bufs,
+                           const uint64_t* shard_lens, size_t n_shards,
+                           const cvlg_grid_spec* spec, const cvlg_filter_rules* rules,
+                           uint32_t n_partitions, uint32_t* planes, uint32_t* raw_count,
+                           cvlg_stats* stats);
+
+/* Device-resident pipeline: d_csv holds the shards concatenated in rank order (HBM, 16-byte
+ * alignment recommended), shard i occupying [shard_offsets[i], shard_offsets[i+1]) with
+ * shard_offsets (host array, n_shards + 1 entries) starting at 0. d_planes / d_raw_count are
+ * device buffers (d_raw_count may be NULL). Runs on `stream` (cudaStream_t, NULL = the
+ * context's stream) and returns after the results are complete. */
+int cvlg_run_pipeline_device(cvlg_context* ctx, const uint8_t* d_csv, const uint64_t* shard_offsets,
+                             size_t n_shards, const cvlg_grid_spec* spec,
+                             const cvlg_filter_rules* rules, uint32_t* d_planes,
+                             uint32_t* d_raw_count, cvlg_stats* stats, void* stream);
+
+/* .cvl1 container writer (lattice_store.cpp:78-134): 58-byte header then T blocks of
+ * (u32 t, planes[t]). Byte-identical to the reference for the same frames. */
+int cvlg_write_container(const uint32_t* planes, const cvlg_grid_spec* spec, int32_t day,
+                         const char* path, uint64_t* bytes_written);
+
+/* Per-stage device milliseconds of the context's last run: decode kernel, dictionary+order,
+ * fold, finalize, and (index 4) the decode kernel alone. n <= 5. */
+int cvlg_last_stage_ms(cvlg_context* ctx, float* ms, int n);
+
+/* Pins / unpins caller memory for faster H2D (cudaHostRegister). */
+int cvlg_pin_host(void* ptr, size_t bytes);
+int cvlg_unpin_host(void* ptr);
+
+/* Number of CUDA kernels this library has launched in this process. */
+uint64_t cvlg_launch_count(void);
+
+/* Copies the calling thread's last error message (NUL-terminated, truncated to len). */
+int cvlg_last_error(char* buf, size_t len);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CVLG_H_ */

@@ -1,0 +1,101 @@
+// Filter + spatio-temporal binning, restated from the reference:
+//   snap_to_integer   proj/src/grid.cpp:10-14
+//   extent_bins       proj/src/grid.cpp:18-22   (host side: grid dims)
+//   linear_bin        proj/src/grid.cpp:26-36
+//   time_bin          proj/src/grid.cpp:69-71 (+ Timestamp::minute_of_day datetime.cpp:97-107)
+//   dxn_bin           proj/src/grid.cpp:73-81
+//   global_index      proj/src/grid.cpp:83-90
+//   filter_reason     proj/src/aggregate.cpp:48-56
+// All arithmetic is IEEE binary64 with explicit round-to-nearest intrinsics on the device so
+// no FMA contraction can change a bin edge.
+#pragma once
+#include "parse.cuh"
+
+namespace cvlg {
+
+// Per-record cell code. Values >= kCodeFirstSpecial are not cells.
+enum : uint32_t {
+    kCodeOutOfGrid = 0xFFFFFFFFu,     // filtered: OutOfGrid
+    kCodeSpeedCeiling = 0xFFFFFFFEu,  // filtered: SpeedCeiling
+    kCodeMissingField = 0xFFFFFFFDu,  // filtered: MissingField (empty id; unreachable after parse)
+    kCodeUnbinnable = 0xFFFFFFFCu,    // require_in_grid=false and off-grid: OutOfBounds if kept
+    kCodeFirstSpecial = 0xFFFFFFFCu,
+};
+
+struct GridParams {
+    double lat_min, lat_max, lon_min, lon_max, lat_step, lon_step, dxn_offset, dxn_step_d;
+    double speed_ceiling;
+    uint32_t min_step, dxn_step, R, C, D, T;
+    int32_t require_in_grid, drop_missing;
+};
+
+CVLG_HD double d_abs(double x) { return bits_dbl(dbl_bits(x) & 0x7FFFFFFFFFFFFFFFull); }
+
+CVLG_HD double d_rint(double x) {
+#if defined(__CUDA_ARCH__)
+    return rint(x);
+#else
+    return nearbyint(x);
+#endif
+}
+
+CVLG_HD double snap_to_integer(double q) {
+    const double r = d_rint(q);
+    const double ar = d_abs(r);
+    const double m = ar > 1.0 ? ar : 1.0;  // fmax(1, |r|); r is never NaN here
+    if (d_abs(d_sub(q, r)) <= d_mul(1e-9, m)) return r;
+    return q;
+}
+
+CVLG_HD uint32_t extent_bins(double lo, double hi, double step) {
+    const double q = snap_to_integer(d_div(d_sub(hi, lo), step));
+    const double n = ceil(q);
+    return n < 1.0 ? 1u : static_cast<uint32_t>(n);
+}
+
+// precondition: lo <= x <= hi (checked by the caller)
+CVLG_HD uint32_t linear_bin(double x, double lo, double step, uint32_t n) {
+    const double q = snap_to_integer(d_div(d_sub(x, lo), step));
+    double b = floor(q);
+    if (b < 0.0) b = 0.0;
+    const double last = static_cast<double>(n - 1);
+    if (b > last) b = last;
+    return static_cast<uint32_t>(b);
+}
+
+CVLG_HD uint32_t time_bin(int64_t epoch, uint32_t min_step) {
+    int64_t day = epoch / 86400;
+    if (epoch % 86400 < 0) --day;
+    const int64_t sod = epoch - day * 86400;
+    return static_cast<uint32_t>(sod / 60) / min_step;
+}
+
+CVLG_HD double d_fmod360(double h) {
+    if (h >= 0.0 && h < 360.0) return h;  // fmod(h, 360) == h exactly in this range
+    return fmod(h, 360.0);
+}
+
+CVLG_HD uint32_t dxn_bin(double heading, const GridParams& g) {
+    double h = d_add(heading, g.dxn_offset);
+    h = d_fmod360(h);
+    if (h < 0.0) h = d_add(h, 360.0);
+    const double q = snap_to_integer(d_div(h, g.dxn_step_d));
+    const uint32_t d = static_cast<uint32_t>(floor(q));
+    return d % g.D;
+}
+
+// filter_reason + binning for one accepted record -> cell code.
+CVLG_HD uint32_t cell_code(int64_t epoch, double lat, double lon, double speed, double heading,
+                           const GridParams& g) {
+    const bool in_grid = lat >= g.lat_min && lat <= g.lat_max && lon >= g.lon_min && lon <= g.lon_max;
+    if (g.require_in_grid && !in_grid) return kCodeOutOfGrid;
+    if (speed > g.speed_ceiling) return kCodeSpeedCeiling;
+    if (!in_grid) return kCodeUnbinnable;
+    const uint32_t t = time_bin(epoch, g.min_step);
+    const uint32_t d = dxn_bin(heading, g);
+    const uint32_t r = linear_bin(lat, g.lat_min, g.lat_step, g.R);
+    const uint32_t c = linear_bin(lon, g.lon_min, g.lon_step, g.C);
+    return ((t * g.D + d) * g.R + r) * g.C + c;
+}
+
+}  // namespace cvlg

@@ -1,0 +1,75 @@
+// Kernel interfaces of the sm_100a CV-ETL path (see DESIGN.md for the data layout).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "grid.cuh"
+#include "parse.cuh"
+
+namespace cvlg {
+
+// ---- decode (K0 header map, K1 tile decode) -------------------------------------------------
+constexpr int kTile = 16384;  // CSV bytes per decode tile
+constexpr int kHalo = 1024;   // bytes staged past the tile end (lines finishing in the next tile)
+constexpr int kPre = 16;      // bytes staged before the tile (previous-byte '\n' test)
+constexpr int kDecodeThreads = 256;
+// An accepted line holds >= 6 non-empty fields (id, 19-byte timestamp, 4 numbers), 5 commas and
+// a terminator: >= 30 bytes. So a tile starts at most kTile/30 + 1 accepted records.
+constexpr int kMaxAccPerTile = kTile / 30 + 2;
+constexpr int kLineCap = 1024;  // line starts handled per pass over a tile
+
+// Stats counters in device memory (u64 each).
+enum : int {
+    kStRowsRead = 0,
+    kStRejBase = 1,  // + (reason-1): BadTimestamp, BadNumeric, MissingField, RangeViolation
+    kStBadHeader = 5,
+    kStParsed = 6,
+    kStDups = 7,
+    kStConflicts = 8,
+    kStAccepted = 9,
+    kStFiltOutOfGrid = 10,
+    kStFiltSpeed = 11,
+    kStFiltMissing = 12,
+    kStGTransitions = 13,  // (run, cell) changes seen in decode: bound on (cell, journey) pairs
+    kStUnbinnable = 14,    // kept records that would throw OutOfBounds
+    kStOverflow = 15,      // capacity overflow (hash tables / slot arrays)
+    kStCount = 16,
+};
+
+struct DecodeOut {
+    int64_t* ts;      // [slot] epoch seconds
+    double* speed;    // [slot]
+    uint32_t* code;   // [slot] cell code (g or kCode*)
+    uint64_t* loff;   // [slot] absolute line offset in the CSV buffer
+    uint32_t* hslot;  // [head] first slot of the run
+    uint64_t* hk0;    // [head] inline journey key, bytes 0..7 big-endian
+    uint64_t* hk1;    // [head] bytes 8..14 big-endian << 8 | (len <= 15 ? len : 0xFF)
+    uint64_t* hidref; // [head] (absolute id offset << 24) | min(len, 2^24-1)
+    uint64_t* hhash;  // [head] FNV-1a 64 of the id (ingest.cpp:287-291)
+    uint64_t slot_cap, head_cap;
+};
+
+struct DecodeParams {
+    const uint8_t* csv;
+    uint64_t avail_end;  // bytes [0, avail_end) resident in HBM
+    uint64_t total_end;  // total CSV bytes
+    const uint64_t* shard_off;  // [n_shards + 1]
+    const ColumnMap* cmap;      // [n_shards]
+    const uint8_t* shard_good;  // [n_shards]
+    uint32_t n_shards;
+    uint32_t tile_end;
+    uint32_t* tile_counter;
+    LookbackState lb;
+    GridParams grid;
+    DecodeOut out;
+    uint64_t* stats;
+    long long* ts_minmax;  // [0] = min, [1] = max over accepted records
+    int aligned16;
+};
+
+void launch_parse_headers(const uint8_t* csv, const uint64_t* shard_off, uint32_t n_shards,
+                          ColumnMap* cmap, uint8_t* good, uint64_t* stats, cudaStream_t s);
+void launch_decode(const DecodeParams& p, uint32_t n_ctas, cudaStream_t s);
+
+}  // namespace cvlg

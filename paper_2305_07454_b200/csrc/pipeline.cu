@@ -1,0 +1,920 @@
+// Host orchestration of the sm_100a pipeline and the C ABI (include/cvlg.h).
+//
+//   K0 header map  ->  K1 tile decode (+ filter + bin, look-back compaction)
+//   -> journey dictionary (128-bit CAS hash table) -> lexicographic rank (LSD string sort)
+//   -> canonical order: run-merge fast path (sort run heads only) or full (rank, ts) radix sort
+//   -> per-journey fold into the (cell, journey) table (dedup + conflict check on the slow path)
+//   -> (cell, journey) sort -> canonical per-cell fold -> dense [T][8][R][C] lattice.
+// Mirrors cvl::run_pipeline (proj/src/aggregate.cpp:401-452); see DESIGN.md for the mapping.
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <cmath>
+#include <fstream>
+#include <functional>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/cvlg.h"
+#include "agg_api.cuh"
+#include "kernels.cuh"
+#include "sort_api.cuh"
+
+namespace cvlg {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+namespace {
+
+thread_local std::string t_last_error;
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(CVLG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t bytes) {
+        if (bytes <= cap && p) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(bytes, 256);
+        CK(cudaMalloc(&p, want));
+        cap = want;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct HostPinned {
+    void* p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t bytes) {
+        if (bytes <= cap && p) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(bytes, 4096);
+        CK(cudaHostAlloc(&p, want, cudaHostAllocDefault));
+        cap = want;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+int bits_for(uint64_t v) {  // bits needed to represent values 0..v
+    int b = 0;
+    while (b < 64 && (v >> b)) ++b;
+    return b;
+}
+
+uint64_t pow2_at_least(uint64_t v) {
+    uint64_t p = 1024;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+struct Dims {
+    uint32_t T, D, R, C;
+    uint64_t RC, cells;
+};
+
+Dims validate_grid(const cvlg_grid_spec* s) {
+    if (!s) fail(CVLG_E_INVALID_ARG, "grid spec is NULL");
+    // GridSpec::validate (grid.cpp:47-57), same order and messages
+    if (!(s->lat_min < s->lat_max)) fail(CVLG_E_BAD_GRID, "BadGrid: lat_min must be < lat_max");
+    if (!(s->lon_min < s->lon_max)) fail(CVLG_E_BAD_GRID, "BadGrid: lon_min must be < lon_max");
+    if (!(s->lat_step > 1e-9) || !(s->lon_step > 1e-9))
+        fail(CVLG_E_BAD_GRID, "BadGrid: lat_step/lon_step must be > 1e-9");
+    if (s->min_step == 0 || 1440 % s->min_step != 0)
+        fail(CVLG_E_BAD_GRID, "BadGrid: min_step must divide 1440");
+    if (s->dxn_step == 0 || 360 % s->dxn_step != 0)
+        fail(CVLG_E_BAD_GRID, "BadGrid: dxn_step must divide 360");
+    if (!std::isfinite(s->dxn_offset)) fail(CVLG_E_BAD_GRID, "BadGrid: dxn_offset must be finite");
+    Dims d;
+    d.T = 1440 / s->min_step;
+    d.D = 360 / s->dxn_step;
+    d.R = extent_bins(s->lat_min, s->lat_max, s->lat_step);
+    d.C = extent_bins(s->lon_min, s->lon_max, s->lon_step);
+    d.RC = static_cast<uint64_t>(d.R) * d.C;
+    d.cells = static_cast<uint64_t>(d.T) * d.D * d.RC;
+    if (d.D > 4)
+        fail(CVLG_E_UNSUPPORTED,
+             "dxn_step < 90: BatchFrame holds 4 direction planes (aggregate.hpp:52-54); the "
+             "reference indexes past them (undefined behaviour)");
+    if (d.cells >= kCodeFirstSpecial)
+        fail(CVLG_E_UNSUPPORTED, "grid has >= 2^32-4 cells; the device cell code is 32-bit");
+    return d;
+}
+
+GridParams make_params(const cvlg_grid_spec* s, const cvlg_filter_rules* r, const Dims& d) {
+    GridParams g;
+    g.lat_min = s->lat_min;
+    g.lat_max = s->lat_max;
+    g.lon_min = s->lon_min;
+    g.lon_max = s->lon_max;
+    g.lat_step = s->lat_step;
+    g.lon_step = s->lon_step;
+    g.dxn_offset = s->dxn_offset;
+    g.dxn_step_d = static_cast<double>(s->dxn_step);
+    g.min_step = s->min_step;
+    g.dxn_step = s->dxn_step;
+    g.R = d.R;
+    g.C = d.C;
+    g.D = d.D;
+    g.T = d.T;
+    cvlg_filter_rules def;
+    cvlg_default_rules(&def);
+    const cvlg_filter_rules* rr = r ? r : &def;
+    g.require_in_grid = rr->require_in_grid;
+    g.drop_missing = rr->drop_missing;
+    g.speed_ceiling = rr->speed_ceiling;
+    return g;
+}
+
+__global__ void iota_kernel(uint32_t* v, uint64_t n) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) v[i] = static_cast<uint32_t>(i);
+}
+
+__global__ void set_u32_kernel(uint32_t* p, uint32_t v) { *p = v; }
+
+__global__ void init_run_kernel(uint64_t* stats, long long* tsmm) {
+    const int i = threadIdx.x;
+    if (i < kStCount) stats[i] = 0;
+    if (i == 0) {
+        tsmm[0] = LLONG_MAX;
+        tsmm[1] = LLONG_MIN;
+    }
+}
+
+unsigned blocks_for(uint64_t n, int bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
+
+}  // namespace
+
+// A chunk of CSV bytes that became resident: decode every tile whose lines are complete.
+struct ChunkMark {
+    uint64_t avail_end;  // bytes [0, avail_end) resident
+    uint64_t safe_end;   // every line starting before safe_end ends before it
+    cudaEvent_t ready;   // recorded on the copy stream (nullptr: already resident)
+};
+
+}  // namespace cvlg
+
+using namespace cvlg;
+
+struct cvlg_context {
+    int device = 0;
+    cudaStream_t stream = nullptr, copy_stream = nullptr;
+    bool own_stream = true;
+    DevBuf csv, shard_off, cmap, good, lb_flag, lb_val, counter, stats, tsmm;
+    DevBuf ts, speed, code, loff, hslot, hk0, hk1, hidref, hhash;
+    DevBuf dict, hdict, flags, pos, uslot, rank_of_slot, hrank, scal;
+    DevBuf keys, vals, keys_alt, vals_alt, sort_tmp, scan_tmp, srank, jstart;
+    DevBuf pair_key, pair_sum, pair_cnt;
+    DevBuf planes, raw;
+    HostPinned h_small, h_csv;
+    std::vector<cudaEvent_t> chunk_events;
+    cudaEvent_t ev[6] = {};
+    cudaEvent_t ev_dec0 = nullptr, ev_dec1 = nullptr;
+    float stage_ms[5] = {0, 0, 0, 0, 0};
+};
+
+namespace {
+
+cvlg_context* default_context() {
+    thread_local cvlg_context* ctx = nullptr;
+    if (!ctx) ctx = cvlg_context_create(-1);
+    return ctx;
+}
+
+uint64_t* h_small64(cvlg_context* c) { return static_cast<uint64_t*>(c->h_small.p); }
+
+void sync(cvlg_context* c) { CK(cudaStreamSynchronize(c->stream)); }
+
+// The pipeline proper over CSV bytes in HBM. `marks` drive incremental decode while the bytes
+// stream in; the last mark must cover everything.
+void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>& shard_off,
+              const ColumnMap* h_cmap, const uint8_t* h_good, uint64_t bad_headers,
+              const cvlg_grid_spec* spec, const cvlg_filter_rules* rules, uint32_t* d_planes,
+              uint32_t* d_raw, cvlg_stats* out_stats, const std::vector<ChunkMark>& marks) {
+    const Dims dims = validate_grid(spec);
+    const GridParams gp = make_params(spec, rules, dims);
+    cudaStream_t s = c->stream;
+    const uint32_t n_shards = static_cast<uint32_t>(shard_off.size() - 1);
+    const uint64_t total = shard_off.back();
+    const uint64_t n_tiles = (total + kTile - 1) / kTile;
+    if (n_tiles >= (1ull << 32)) fail(CVLG_E_UNSUPPORTED, "input larger than 64 TiB");
+
+    c->h_small.ensure(4096);
+    uint64_t* hs = h_small64(c);
+
+    CK(cudaEventRecord(c->ev[0], s));
+    // ---- setup -----------------------------------------------------------------------------
+    c->stats.ensure(kStCount * 8);
+    c->tsmm.ensure(16);
+    init_run_kernel<<<1, 32, 0, s>>>(c->stats.as<uint64_t>(), c->tsmm.as<long long>());
+    count_launch();
+    c->shard_off.ensure((n_shards + 1) * 8);
+    CK(cudaMemcpyAsync(c->shard_off.p, shard_off.data(), (n_shards + 1) * 8, cudaMemcpyHostToDevice, s));
+    c->cmap.ensure(std::max<uint32_t>(n_shards, 1) * sizeof(ColumnMap));
+    c->good.ensure(std::max<uint32_t>(n_shards, 1));
+    if (h_cmap) {
+        CK(cudaMemcpyAsync(c->cmap.p, h_cmap, n_shards * sizeof(ColumnMap), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(c->good.p, h_good, n_shards, cudaMemcpyHostToDevice, s));
+        if (bad_headers) {
+            hs[0] = bad_headers;
+            CK(cudaMemcpyAsync(c->stats.as<uint64_t>() + kStBadHeader, hs, 8, cudaMemcpyHostToDevice, s));
+        }
+    } else {
+        launch_parse_headers(d_csv, c->shard_off.as<uint64_t>(), n_shards, c->cmap.as<ColumnMap>(),
+                             c->good.as<uint8_t>(), c->stats.as<uint64_t>(), s);
+        count_launch();
+    }
+    const uint64_t slot_cap = total / 30 + n_shards + 2;
+    c->ts.ensure(slot_cap * 8);
+    c->speed.ensure(slot_cap * 8);
+    c->code.ensure(slot_cap * 4);
+    c->loff.ensure(slot_cap * 8);
+    c->hslot.ensure(slot_cap * 4);
+    c->hk0.ensure(slot_cap * 8);
+    c->hk1.ensure(slot_cap * 8);
+    c->hidref.ensure(slot_cap * 8);
+    c->hhash.ensure(slot_cap * 8);
+    c->lb_flag.ensure(std::max<uint64_t>(n_tiles, 1) * 4);
+    c->lb_val.ensure(std::max<uint64_t>(n_tiles, 1) * 32);
+    c->counter.ensure(4);
+    CK(cudaMemsetAsync(c->lb_flag.p, 0, std::max<uint64_t>(n_tiles, 1) * 4, s));
+    CK(cudaMemsetAsync(c->counter.p, 0, 4, s));
+
+    // ---- K1 decode ---------------------------------------------------------------------------
+    DecodeParams P;
+    P.csv = d_csv;
+    P.total_end = total;
+    P.shard_off = c->shard_off.as<uint64_t>();
+    P.cmap = c->cmap.as<ColumnMap>();
+    P.shard_good = c->good.as<uint8_t>();
+    P.n_shards = n_shards;
+    P.tile_counter = c->counter.as<uint32_t>();
+    P.lb.flag = c->lb_flag.as<uint32_t>();
+    P.lb.agg = c->lb_val.as<uint64_t>();
+    P.lb.inc = c->lb_val.as<uint64_t>() + 2 * std::max<uint64_t>(n_tiles, 1);
+    P.grid = gp;
+    P.out.ts = c->ts.as<int64_t>();
+    P.out.speed = c->speed.as<double>();
+    P.out.code = c->code.as<uint32_t>();
+    P.out.loff = c->loff.as<uint64_t>();
+    P.out.hslot = c->hslot.as<uint32_t>();
+    P.out.hk0 = c->hk0.as<uint64_t>();
+    P.out.hk1 = c->hk1.as<uint64_t>();
+    P.out.hidref = c->hidref.as<uint64_t>();
+    P.out.hhash = c->hhash.as<uint64_t>();
+    P.out.slot_cap = slot_cap;
+    P.out.head_cap = slot_cap;
+    P.stats = c->stats.as<uint64_t>();
+    P.ts_minmax = c->tsmm.as<long long>();
+    P.aligned16 = (reinterpret_cast<uintptr_t>(d_csv) % 16) == 0;
+    CK(cudaEventRecord(c->ev_dec0, s));
+    uint64_t tiles_done = 0;
+    for (size_t m = 0; m < marks.size(); ++m) {
+        const bool last = m + 1 == marks.size();
+        const uint64_t t_hi = last ? n_tiles : std::min<uint64_t>(marks[m].safe_end / kTile, n_tiles);
+        if (marks[m].ready) CK(cudaStreamWaitEvent(s, marks[m].ready, 0));
+        if (t_hi > tiles_done) {
+            P.avail_end = marks[m].avail_end;
+            P.tile_end = static_cast<uint32_t>(t_hi);
+            launch_decode(P, static_cast<uint32_t>(t_hi - tiles_done), s);
+            count_launch();
+            tiles_done = t_hi;
+        }
+    }
+    CK(cudaEventRecord(c->ev_dec1, s));
+    CK(cudaGetLastError());
+
+    // ---- read back sizes ---------------------------------------------------------------------
+    CK(cudaMemcpyAsync(hs, c->stats.p, kStCount * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hs + kStCount, c->tsmm.p, 16, cudaMemcpyDeviceToHost, s));
+    if (n_tiles)
+        CK(cudaMemcpyAsync(hs + kStCount + 2, P.lb.inc + 2 * (n_tiles - 1), 16, cudaMemcpyDeviceToHost, s));
+    sync(c);
+    CK(cudaEventRecord(c->ev[1], s));
+    if (hs[kStOverflow]) fail(CVLG_E_INTERNAL, "decode capacity invariant violated");
+    const uint64_t N = n_tiles ? hs[kStCount + 2] : 0;
+    const uint64_t H = n_tiles ? hs[kStCount + 3] : 0;
+    const int64_t ts_min = static_cast<int64_t>(hs[kStCount]);
+    const int64_t ts_max = static_cast<int64_t>(hs[kStCount + 1]);
+    const uint64_t transitions = hs[kStGTransitions];
+    if (N != hs[kStParsed]) fail(CVLG_E_INTERNAL, "decode count mismatch");
+    if (N >= (1ull << 32) - 1) fail(CVLG_E_UNSUPPORTED, ">= 2^32-1 records on one device");
+
+    const uint64_t lattice_words = static_cast<uint64_t>(dims.T) * 8 * dims.RC;
+    const uint64_t raw_words = static_cast<uint64_t>(dims.T) * 4 * dims.RC;
+    CK(cudaMemsetAsync(d_planes, 0, lattice_words * 4, s));
+    if (d_raw) CK(cudaMemsetAsync(d_raw, 0, raw_words * 4, s));
+
+    bool slow = false;
+    uint64_t J = 0;
+    if (N > 0) {
+        // ---- journey dictionary ----------------------------------------------------------------
+        const uint64_t dcap = pow2_at_least(2 * H);
+        c->dict.ensure(dcap * 16);
+        c->hdict.ensure(H * 4);
+        c->scal.ensure(64);
+        CK(cudaMemsetAsync(c->dict.p, 0xFF, dcap * 16, s));
+        CK(cudaMemsetAsync(c->scal.p, 0, 64, s));
+        unsigned long long* d_maxlen = c->scal.as<unsigned long long>();
+        launch_dict_insert(P.out, H, d_csv, c->dict.as<unsigned long long>(), dcap - 1,
+                           c->hdict.as<uint32_t>(), c->stats.as<uint64_t>(), d_maxlen, s);
+        c->flags.ensure(std::max<uint64_t>(dcap, N + 1) * 4 + 16);
+        c->pos.ensure(std::max<uint64_t>(dcap, N + 1) * 4 + 16);
+        c->scan_tmp.ensure(scan_temp_words(std::max<uint64_t>(dcap, N + 1)) * 4 + 64);
+        launch_dict_flags(c->dict.as<unsigned long long>(), dcap, c->flags.as<uint32_t>(), s);
+        uint32_t* d_total = c->scal.as<uint32_t>() + 4;
+        exclusive_scan_u32(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), dcap, d_total,
+                           c->scan_tmp.as<uint32_t>(), s);
+        CK(cudaMemcpyAsync(hs, c->scal.p, 32, cudaMemcpyDeviceToHost, s));
+        sync(c);
+        const uint64_t max_len = hs[0];
+        J = static_cast<uint32_t*>(static_cast<void*>(hs))[4];
+        c->uslot.ensure(J * 4);
+        launch_dict_compact(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), dcap,
+                            c->uslot.as<uint32_t>(), s);
+
+        // ---- lexicographic rank: LSD over (length, then 8-byte chunks last..first) ----------------
+        const uint64_t sort_n = std::max<uint64_t>({J, H, N});
+        c->keys.ensure(sort_n * 8);
+        c->keys_alt.ensure(sort_n * 8);
+        c->vals.ensure(sort_n * 4);
+        c->vals_alt.ensure(sort_n * 4);
+        c->sort_tmp.ensure(radix_temp_bytes(sort_n));
+        unsigned long long* d_orand = c->scal.as<unsigned long long>() + 4;
+        unsigned long long* h_orand = reinterpret_cast<unsigned long long*>(hs + 8);
+        iota_kernel<<<blocks_for(J, 256), 256, 0, s>>>(c->vals.as<uint32_t>(), J);
+        count_launch();
+        const int n_chunks = static_cast<int>((max_len + 7) / 8);
+        for (int ch = -1; ch < n_chunks; ++ch) {
+            const int cc = ch < 0 ? -1 : n_chunks - 1 - ch;
+            launch_dict_chunk(c->dict.as<unsigned long long>(), c->uslot.as<uint32_t>(),
+                              c->vals.as<uint32_t>(), J, cc, d_csv, c->keys.as<uint64_t>(), s);
+            // keys are gathered in current perm order; sort (keys, perm) stably
+            radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(),
+                             c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), J, 0, 64,
+                             c->sort_tmp.p, s, d_orand, h_orand);
+        }
+        // vals now holds unique indices in lexicographic order
+        c->rank_of_slot.ensure(dcap * 4);
+        launch_dict_rank(c->uslot.as<uint32_t>(), c->vals.as<uint32_t>(), J,
+                         c->rank_of_slot.as<uint32_t>(), s);
+        c->hrank.ensure(H * 4);
+        launch_head_rank(c->hdict.as<uint32_t>(), c->rank_of_slot.as<uint32_t>(), H,
+                         c->hrank.as<uint32_t>(), s);
+
+        // ---- canonical order -----------------------------------------------------------------
+        const int tsbits = bits_for(static_cast<uint64_t>(ts_max - ts_min));
+        const int rbits = bits_for(J - 1);
+        const int mode = (tsbits + rbits <= 64) ? 0 : 1;
+        c->jstart.ensure((J + 1) * 4);
+        c->srank.ensure(sort_n * 4);
+        uint32_t* d_invalid = c->scal.as<uint32_t>() + 12;
+        CK(cudaMemsetAsync(d_invalid, 0, 4, s));
+        launch_head_keys(c->hrank.as<uint32_t>(), c->hslot.as<uint32_t>(), c->ts.as<int64_t>(), H,
+                         ts_min, tsbits, mode, c->keys.as<uint64_t>(), c->vals.as<uint32_t>(), s);
+        radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(), c->keys_alt.as<uint64_t>(),
+                         c->vals_alt.as<uint32_t>(), H, 0, mode == 0 ? tsbits + rbits : tsbits,
+                         c->sort_tmp.p, s, d_orand, h_orand);
+        if (mode == 1) {
+            launch_gather_rank_keys(c->hrank.as<uint32_t>(), c->vals.as<uint32_t>(), H,
+                                    c->keys.as<uint64_t>(), s);
+            radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(),
+                             c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), H, 0, rbits,
+                             c->sort_tmp.p, s, d_orand, h_orand);
+        }
+        launch_head_order_check(c->vals.as<uint32_t>(), c->hrank.as<uint32_t>(),
+                                c->hslot.as<uint32_t>(), c->ts.as<int64_t>(), H, N,
+                                c->jstart.as<uint32_t>(), d_invalid, s);
+        CK(cudaMemcpyAsync(hs, d_invalid, 4, cudaMemcpyDeviceToHost, s));
+        sync(c);
+        slow = static_cast<uint32_t*>(static_cast<void*>(hs))[0] != 0;
+        uint32_t* jstart = c->jstart.as<uint32_t>();
+        if (!slow) {
+            set_u32_kernel<<<1, 1, 0, s>>>(jstart + J, static_cast<uint32_t>(H));
+            count_launch();
+        } else {
+            // full (rank, ts) sort of every record; provenance order breaks ties (stable)
+            launch_slot_keys(c->hslot.as<uint32_t>(), c->hrank.as<uint32_t>(), H,
+                             c->ts.as<int64_t>(), N, ts_min, tsbits, mode, c->keys.as<uint64_t>(),
+                             c->vals.as<uint32_t>(), c->srank.as<uint32_t>(), s);
+            radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(),
+                             c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), N, 0,
+                             mode == 0 ? tsbits + rbits : tsbits, c->sort_tmp.p, s, d_orand,
+                             h_orand);
+            if (mode == 1) {
+                launch_gather_rank_keys(c->srank.as<uint32_t>(), c->vals.as<uint32_t>(), N,
+                                        c->keys.as<uint64_t>(), s);
+                radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(),
+                                 c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), N, 0,
+                                 rbits, c->sort_tmp.p, s, d_orand, h_orand);
+            }
+            launch_slot_jstart(c->vals.as<uint32_t>(), c->srank.as<uint32_t>(), N, jstart, s);
+            set_u32_kernel<<<1, 1, 0, s>>>(jstart + J, static_cast<uint32_t>(N));
+            count_launch();
+        }
+        CK(cudaEventRecord(c->ev[2], s));
+
+        // ---- per-journey fold ------------------------------------------------------------------
+        const uint64_t pair_bound = slow ? N : std::min<uint64_t>(N, H + transitions);
+        const uint64_t pcap = pow2_at_least(2 * pair_bound);
+        c->pair_key.ensure(pcap * 8);
+        c->pair_sum.ensure(pcap * 8);
+        c->pair_cnt.ensure(pcap * 4);
+        CK(cudaMemsetAsync(c->pair_key.p, 0xFF, pcap * 8, s));
+        FoldParams F;
+        F.n_journeys = J;
+        F.jstart = jstart;
+        F.perm = c->vals.as<uint32_t>();
+        F.hslot = c->hslot.as<uint32_t>();
+        F.n_heads = H;
+        F.n_slots = N;
+        F.ts = c->ts.as<int64_t>();
+        F.speed = c->speed.as<double>();
+        F.code = c->code.as<uint32_t>();
+        F.loff = c->loff.as<uint64_t>();
+        F.pair_key = c->pair_key.as<uint64_t>();
+        F.pair_sum = c->pair_sum.as<double>();
+        F.pair_cnt = c->pair_cnt.as<uint32_t>();
+        F.pair_mask = pcap - 1;
+        F.csv = d_csv;
+        F.shard_off = c->shard_off.as<uint64_t>();
+        F.cmap = c->cmap.as<ColumnMap>();
+        F.n_shards = n_shards;
+        F.stats = c->stats.as<uint64_t>();
+        launch_fold(F, slow, s);
+        CK(cudaEventRecord(c->ev[3], s));
+
+        // ---- (cell, journey) pairs -> canonical per-cell fold ----------------------------------
+        c->flags.ensure(pcap * 4 + 16);
+        c->pos.ensure(pcap * 4 + 16);
+        c->scan_tmp.ensure(scan_temp_words(pcap) * 4 + 64);
+        launch_pair_flags(c->pair_key.as<uint64_t>(), pcap, c->flags.as<uint32_t>(), s);
+        exclusive_scan_u32(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), pcap, d_total,
+                           c->scan_tmp.as<uint32_t>(), s);
+        CK(cudaMemcpyAsync(hs, d_total, 4, cudaMemcpyDeviceToHost, s));
+        sync(c);
+        const uint64_t n_pairs = static_cast<uint32_t*>(static_cast<void*>(hs))[0];
+        c->keys.ensure(std::max<uint64_t>(n_pairs, sort_n) * 8);
+        c->keys_alt.ensure(std::max<uint64_t>(n_pairs, sort_n) * 8);
+        c->vals.ensure(std::max<uint64_t>(n_pairs, sort_n) * 4);
+        c->vals_alt.ensure(std::max<uint64_t>(n_pairs, sort_n) * 4);
+        c->sort_tmp.ensure(radix_temp_bytes(std::max<uint64_t>(n_pairs, sort_n)));
+        launch_pair_compact(c->pair_key.as<uint64_t>(), c->flags.as<uint32_t>(),
+                            c->pos.as<uint32_t>(), pcap, rbits, c->keys.as<uint64_t>(),
+                            c->vals.as<uint32_t>(), s);
+        const int gbits = bits_for(dims.cells - 1);
+        radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(), c->keys_alt.as<uint64_t>(),
+                         c->vals_alt.as<uint32_t>(), n_pairs, 0, gbits + rbits, c->sort_tmp.p, s,
+                         d_orand, h_orand);
+        launch_finalize(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(), n_pairs, rbits,
+                        c->pair_sum.as<double>(), c->pair_cnt.as<uint32_t>(), dims.D, dims.RC,
+                        d_planes, d_raw, s);
+    } else {
+        CK(cudaEventRecord(c->ev[2], s));
+        CK(cudaEventRecord(c->ev[3], s));
+    }
+    CK(cudaEventRecord(c->ev[4], s));
+    CK(cudaMemcpyAsync(hs, c->stats.p, kStCount * 8, cudaMemcpyDeviceToHost, s));
+    sync(c);
+    CK(cudaGetLastError());
+    if (hs[kStOverflow]) fail(CVLG_E_INTERNAL, "aggregation capacity invariant violated");
+    float ms[4] = {0, 0, 0, 0};
+    cudaEventElapsedTime(&ms[0], c->ev[0], c->ev[1]);
+    cudaEventElapsedTime(&ms[1], c->ev[1], c->ev[2]);
+    cudaEventElapsedTime(&ms[2], c->ev[2], c->ev[3]);
+    cudaEventElapsedTime(&ms[3], c->ev[3], c->ev[4]);
+    for (int i = 0; i < 4; ++i) c->stage_ms[i] = ms[i];
+    cudaEventElapsedTime(&c->stage_ms[4], c->ev_dec0, c->ev_dec1);
+    if (out_stats) {
+        cvlg_stats& st = *out_stats;
+        std::memset(&st, 0, sizeof(st));
+        st.rows_read = hs[kStRowsRead];
+        st.parsed = hs[kStParsed];
+        st.duplicates_dropped = hs[kStDups];
+        st.conflicting_duplicates = hs[kStConflicts];
+        st.accepted = hs[kStAccepted];
+        for (int i = 0; i < 4; ++i) st.rejected[i] = hs[kStRejBase + i];
+        st.rejected[4] = hs[kStBadHeader];
+        st.filtered[0] = hs[kStFiltOutOfGrid];
+        st.filtered[1] = hs[kStFiltSpeed];
+        st.filtered[2] = hs[kStFiltMissing];
+        for (int i = 0; i < 4; ++i) st.stage_seconds[i] = ms[i] / 1000.0;
+    }
+    if (hs[kStUnbinnable])
+        fail(CVLG_E_OUT_OF_BOUNDS,
+             "OutOfBounds: a kept record lies outside the grid (require_in_grid = false)");
+}
+
+// Host-side header map for shards whose bytes are in host memory.
+void host_headers(const uint8_t* const* bufs, const uint64_t* lens, size_t n,
+                  std::vector<ColumnMap>& cmap, std::vector<uint8_t>& good, uint64_t& bad) {
+    cmap.resize(n);
+    good.resize(n);
+    bad = 0;
+    for (size_t s = 0; s < n; ++s) {
+        ColumnMap m;
+        std::memset(&m, 0xFF, sizeof(m));
+        m.n_columns = 0;
+        if (lens[s] == 0) {
+            good[s] = 0;
+            cmap[s] = m;
+            continue;
+        }
+        const uint8_t* b = bufs[s];
+        const void* nlp = std::memchr(b, '\n', lens[s]);
+        uint64_t len = nlp ? static_cast<uint64_t>(static_cast<const uint8_t*>(nlp) - b) : lens[s];
+        if (len > 0 && b[len - 1] == '\r') --len;
+        const bool ok = parse_header(b, static_cast<int64_t>(len), m);
+        good[s] = ok ? 1 : 0;
+        cmap[s] = m;
+        if (!ok) ++bad;
+    }
+}
+
+void run_host(cvlg_context* c, const uint8_t* const* bufs, const uint64_t* lens, size_t n,
+              const cvlg_grid_spec* spec, const cvlg_filter_rules* rules, uint32_t* planes,
+              uint32_t* raw, cvlg_stats* stats) {
+    const Dims dims = validate_grid(spec);
+    std::vector<uint64_t> off(n + 1, 0);
+    for (size_t i = 0; i < n; ++i) off[i + 1] = off[i] + lens[i];
+    const uint64_t total = off[n];
+    std::vector<ColumnMap> cmap;
+    std::vector<uint8_t> good;
+    uint64_t bad = 0;
+    host_headers(bufs, lens, n, cmap, good, bad);
+    c->csv.ensure(total + 16);
+    uint8_t* d_csv = c->csv.as<uint8_t>();
+    // chunked, line-aligned H2D on the copy stream, decode overlapped on the compute stream
+    constexpr uint64_t kChunk = 64ull << 20;
+    std::vector<ChunkMark> marks;
+    size_t ev_i = 0;
+    auto next_event = [&]() {
+        if (ev_i >= c->chunk_events.size()) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->chunk_events.push_back(e);
+        }
+        return c->chunk_events[ev_i++];
+    };
+    // the copy stream must not start before the previous run finished with the buffer
+    cudaEvent_t start_ev = next_event();
+    CK(cudaEventRecord(start_ev, c->stream));
+    CK(cudaStreamWaitEvent(c->copy_stream, start_ev, 0));
+    uint64_t safe = 0;
+    for (size_t sidx = 0; sidx < n; ++sidx) {
+        const uint64_t len = lens[sidx];
+        for (uint64_t a = 0; a < len; a += kChunk) {
+            const uint64_t b = std::min(len, a + kChunk);
+            CK(cudaMemcpyAsync(d_csv + off[sidx] + a, bufs[sidx] + a, b - a, cudaMemcpyHostToDevice,
+                               c->copy_stream));
+            cudaEvent_t e = next_event();
+            CK(cudaEventRecord(e, c->copy_stream));
+            if (b == len) {
+                safe = off[sidx + 1];
+            } else {
+                // last '\n' in the piece
+                const uint8_t* p = bufs[sidx] + a;
+                uint64_t k = b - a;
+                while (k > 0 && p[k - 1] != '\n') --k;
+                if (k > 0) safe = off[sidx] + a + k;
+            }
+            marks.push_back(ChunkMark{off[sidx] + b, safe, e});
+        }
+    }
+    if (marks.empty()) marks.push_back(ChunkMark{total, total, nullptr});
+    uint32_t* d_planes;
+    uint32_t* d_raw = nullptr;
+    const uint64_t lattice_words = static_cast<uint64_t>(dims.T) * 8 * dims.RC;
+    const uint64_t raw_words = static_cast<uint64_t>(dims.T) * 4 * dims.RC;
+    c->planes.ensure(lattice_words * 4);
+    d_planes = c->planes.as<uint32_t>();
+    if (raw) {
+        c->raw.ensure(raw_words * 4);
+        d_raw = c->raw.as<uint32_t>();
+    }
+    run_core(c, d_csv, off, cmap.data(), good.data(), bad, spec, rules, d_planes, d_raw, stats,
+             marks);
+    if (planes)
+        CK(cudaMemcpyAsync(planes, d_planes, lattice_words * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (raw) CK(cudaMemcpyAsync(raw, d_raw, raw_words * 4, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+}
+
+int guard(const std::function<void()>& fn) {
+    try {
+        fn();
+        return CVLG_OK;
+    } catch (const Error& e) {
+        t_last_error = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        t_last_error = "host allocation failed";
+        return CVLG_E_CUDA;
+    } catch (const std::exception& e) {
+        t_last_error = e.what();
+        return CVLG_E_INTERNAL;
+    }
+}
+
+}  // namespace
+
+// ==================================== C ABI =====================================================
+extern "C" {
+
+void cvlg_default_grid(cvlg_grid_spec* s) {
+    if (!s) return;
+    s->lat_min = 36.0;
+    s->lat_max = 40.6;
+    s->lon_min = -95.8;
+    s->lon_max = -89.1;
+    s->lat_step = 0.1;
+    s->lon_step = 0.1;
+    s->min_step = 5;
+    s->dxn_step = 90;
+    s->dxn_offset = 0.0;
+}
+
+void cvlg_default_rules(cvlg_filter_rules* r) {
+    if (!r) return;
+    r->require_in_grid = 1;
+    r->drop_missing = 1;
+    r->speed_ceiling = 250.0;
+}
+
+int cvlg_grid_dims(const cvlg_grid_spec* spec, uint32_t* T, uint32_t* D, uint32_t* R, uint32_t* C) {
+    return guard([&] {
+        const Dims d = validate_grid(spec);
+        if (T) *T = d.T;
+        if (D) *D = d.D;
+        if (R) *R = d.R;
+        if (C) *C = d.C;
+    });
+}
+
+cvlg_context* cvlg_context_create(int device) {
+    cvlg_context* c = nullptr;
+    const int rc = guard([&] {
+        int dev = device;
+        if (dev < 0) CK(cudaGetDevice(&dev));
+        CK(cudaSetDevice(dev));
+        c = new cvlg_context();
+        c->device = dev;
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        for (auto& e : c->ev) CK(cudaEventCreate(&e));
+        CK(cudaEventCreate(&c->ev_dec0));
+        CK(cudaEventCreate(&c->ev_dec1));
+    });
+    if (rc != CVLG_OK) {
+        delete c;
+        return nullptr;
+    }
+    return c;
+}
+
+void cvlg_context_destroy(cvlg_context* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    cudaStreamSynchronize(c->copy_stream);
+    DevBuf* bufs[] = {&c->csv,    &c->shard_off, &c->cmap,     &c->good,     &c->lb_flag,
+                      &c->lb_val, &c->counter,   &c->stats,    &c->tsmm,     &c->ts,
+                      &c->speed,  &c->code,      &c->loff,     &c->hslot,    &c->hk0,
+                      &c->hk1,    &c->hidref,    &c->hhash,    &c->dict,     &c->hdict,
+                      &c->flags,  &c->pos,       &c->uslot,    &c->rank_of_slot, &c->hrank,
+                      &c->scal,   &c->keys,      &c->vals,     &c->keys_alt, &c->vals_alt,
+                      &c->sort_tmp, &c->scan_tmp, &c->srank,   &c->jstart,   &c->pair_key,
+                      &c->pair_sum, &c->pair_cnt, &c->planes,  &c->raw};
+    for (DevBuf* b : bufs) b->release();
+    c->h_small.release();
+    c->h_csv.release();
+    for (auto e : c->chunk_events) cudaEventDestroy(e);
+    for (auto e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->ev_dec0) cudaEventDestroy(c->ev_dec0);
+    if (c->ev_dec1) cudaEventDestroy(c->ev_dec1);
+    cudaStreamDestroy(c->stream);
+    cudaStreamDestroy(c->copy_stream);
+    delete c;
+}
+
+int cvlg_run_pipeline(cvlg_context* ctx, const char* const* shard_paths, size_t n_shards,
+                      const cvlg_grid_spec* spec, const cvlg_filter_rules* rules,
+                      uint32_t n_partitions, uint32_t n_threads, uint32_t* planes,
+                      uint32_t* raw_count, cvlg_stats* stats) {
+    return guard([&] {
+        validate_grid(spec);
+        if (n_partitions == 0) fail(CVLG_E_ZERO_PARTITIONS, "ZeroPartitions: n_partitions must be >= 1");
+        if (n_shards && !shard_paths) fail(CVLG_E_INVALID_ARG, "shard_paths is NULL");
+        cvlg_context* c = ctx ? ctx : default_context();
+        if (!c) fail(CVLG_E_CUDA, "no CUDA context");
+        CK(cudaSetDevice(c->device));
+        // lexicographic rank of paths (aggregate.cpp:389-397)
+        std::vector<size_t> order(n_shards);
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+            return std::strcmp(shard_paths[a], shard_paths[b]) < 0;
+        });
+        std::vector<uint64_t> lens(n_shards), off(n_shards + 1, 0);
+        for (size_t r = 0; r < n_shards; ++r) {
+            struct stat st;
+            const char* p = shard_paths[order[r]];
+            if (::stat(p, &st) != 0 || !S_ISREG(st.st_mode))
+                fail(CVLG_E_IO, std::string("Io: cannot open shard ") + p);
+            lens[r] = static_cast<uint64_t>(st.st_size);
+            off[r + 1] = off[r] + lens[r];
+        }
+        c->h_csv.ensure(off[n_shards] + 16);
+        uint8_t* host = static_cast<uint8_t*>(c->h_csv.p);
+        unsigned workers = n_threads ? n_threads : std::max(1u, std::thread::hardware_concurrency());
+        workers = static_cast<unsigned>(std::min<size_t>(workers, std::max<size_t>(n_shards, 1)));
+        std::atomic<size_t> next{0};
+        std::vector<std::string> errors(workers);
+        std::vector<std::thread> pool;
+        for (unsigned w = 0; w < workers; ++w) {
+            pool.emplace_back([&, w] {
+                for (size_t r = next.fetch_add(1); r < n_shards; r = next.fetch_add(1)) {
+                    const char* p = shard_paths[order[r]];
+                    const int fd = ::open(p, O_RDONLY);
+                    if (fd < 0) {
+                        errors[w] = std::string("Io: cannot open shard ") + p;
+                        return;
+                    }
+                    uint64_t got = 0;
+                    while (got < lens[r]) {
+                        const ssize_t k = ::read(fd, host + off[r] + got, lens[r] - got);
+                        if (k <= 0) break;
+                        got += static_cast<uint64_t>(k);
+                    }
+                    ::close(fd);
+                    if (got != lens[r]) {
+                        errors[w] = std::string("Io: read failure on ") + p;
+                        return;
+                    }
+                }
+            });
+        }
+        for (auto& t : pool) t.join();
+        for (auto& e : errors)
+            if (!e.empty()) fail(CVLG_E_IO, e);
+        std::vector<const uint8_t*> bufs(n_shards);
+        for (size_t r = 0; r < n_shards; ++r) bufs[r] = host + off[r];
+        run_host(c, bufs.data(), lens.data(), n_shards, spec, rules, planes, raw_count, stats);
+    });
+}
+
+int cvlg_run_pipeline_host(cvlg_context* ctx, const uint8_t* const* shard_bufs,
+                           const uint64_t* shard_lens, size_t n_shards,
+                           const cvlg_grid_spec* spec, const cvlg_filter_rules* rules,
+                           uint32_t n_partitions, uint32_t* planes, uint32_t* raw_count,
+                           cvlg_stats* stats) {
+    return guard([&] {
+        validate_grid(spec);
+        if (n_partitions == 0) fail(CVLG_E_ZERO_PARTITIONS, "ZeroPartitions: n_partitions must be >= 1");
+        if (n_shards && (!shard_bufs || !shard_lens)) fail(CVLG_E_INVALID_ARG, "NULL shard arrays");
+        cvlg_context* c = ctx ? ctx : default_context();
+        if (!c) fail(CVLG_E_CUDA, "no CUDA context");
+        CK(cudaSetDevice(c->device));
+        run_host(c, shard_bufs, shard_lens, n_shards, spec, rules, planes, raw_count, stats);
+    });
+}
+
+int cvlg_run_pipeline_device(cvlg_context* ctx, const uint8_t* d_csv, const uint64_t* shard_offsets,
+                             size_t n_shards, const cvlg_grid_spec* spec,
+                             const cvlg_filter_rules* rules, uint32_t* d_planes,
+                             uint32_t* d_raw_count, cvlg_stats* stats, void* stream) {
+    return guard([&] {
+        validate_grid(spec);
+        if (!shard_offsets || !d_planes) fail(CVLG_E_INVALID_ARG, "NULL argument");
+        cvlg_context* c = ctx ? ctx : default_context();
+        if (!c) fail(CVLG_E_CUDA, "no CUDA context");
+        CK(cudaSetDevice(c->device));
+        std::vector<uint64_t> off(shard_offsets, shard_offsets + n_shards + 1);
+        if (off[0] != 0) fail(CVLG_E_INVALID_ARG, "shard_offsets[0] must be 0");
+        for (size_t i = 0; i < n_shards; ++i)
+            if (off[i + 1] < off[i]) fail(CVLG_E_INVALID_ARG, "shard_offsets must be non-decreasing");
+        cudaStream_t saved = c->stream;
+        if (stream) c->stream = static_cast<cudaStream_t>(stream);
+        try {
+            std::vector<ChunkMark> marks{ChunkMark{off.back(), off.back(), nullptr}};
+            run_core(c, d_csv, off, nullptr, nullptr, 0, spec, rules, d_planes, d_raw_count, stats,
+                     marks);
+        } catch (...) {
+            c->stream = saved;
+            throw;
+        }
+        c->stream = saved;
+    });
+}
+
+int cvlg_write_container(const uint32_t* planes, const cvlg_grid_spec* spec, int32_t day,
+                         const char* path, uint64_t* bytes_written) {
+    return guard([&] {
+        const Dims d = validate_grid(spec);
+        if (!planes || !path) fail(CVLG_E_INVALID_ARG, "NULL argument");
+        // NonFiniteValue check (lattice_store.cpp:92-95)
+        const uint64_t rc = d.RC;
+        for (uint32_t t = 0; t < d.T; ++t)
+            for (uint64_t i = 0; i < 4 * rc; ++i) {
+                const uint32_t u = planes[(static_cast<uint64_t>(t) * 8) * rc + i];
+                if ((u & 0x7F800000u) == 0x7F800000u)
+                    fail(CVLG_E_NON_FINITE_VALUE,
+                         "NonFiniteValue: NaN/Inf in speed plane of batch " + std::to_string(t));
+            }
+        std::ofstream out(path, std::ios::binary | std::ios::trunc);
+        if (!out) fail(CVLG_E_IO, std::string("Io: cannot open ") + path + " for writing");
+        uint8_t h[58];
+        size_t k = 0;
+        auto put = [&](const void* p, size_t n) {
+            std::memcpy(h + k, p, n);  // x86-64 / aarch64 hosts are little-endian
+            k += n;
+        };
+        const char magic[4] = {'C', 'V', 'L', '1'};
+        const uint16_t version = 1;
+        const uint16_t ms = static_cast<uint16_t>(spec->min_step), ds = static_cast<uint16_t>(spec->dxn_step);
+        put(magic, 4);
+        put(&version, 2);
+        put(&spec->lat_min, 8);
+        put(&spec->lat_step, 8);
+        put(&spec->lon_min, 8);
+        put(&spec->lon_step, 8);
+        put(&d.R, 4);
+        put(&d.C, 4);
+        put(&ms, 2);
+        put(&ds, 2);
+        put(&d.T, 4);
+        put(&day, 4);
+        out.write(reinterpret_cast<const char*>(h), 58);
+        uint64_t written = 58;
+        for (uint32_t t = 0; t < d.T; ++t) {
+            out.write(reinterpret_cast<const char*>(&t), 4);
+            out.write(reinterpret_cast<const char*>(planes + static_cast<uint64_t>(t) * 8 * rc),
+                      static_cast<std::streamsize>(8 * rc * 4));
+            written += 4 + 8 * rc * 4;
+        }
+        out.flush();
+        if (!out) fail(CVLG_E_IO, std::string("Io: short write to ") + path);
+        if (bytes_written) *bytes_written = written;
+    });
+}
+
+int cvlg_last_stage_ms(cvlg_context* ctx, float* ms, int n) {
+    if (!ctx || !ms) return CVLG_E_INVALID_ARG;
+    for (int i = 0; i < n && i < 5; ++i) ms[i] = ctx->stage_ms[i];
+    return CVLG_OK;
+}
+
+int cvlg_pin_host(void* ptr, size_t bytes) {
+    return guard([&] { CK(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault)); });
+}
+
+int cvlg_unpin_host(void* ptr) {
+    return guard([&] { CK(cudaHostUnregister(ptr)); });
+}
+
+uint64_t cvlg_launch_count(void) { return launch_count(); }
+
+int cvlg_last_error(char* buf, size_t len) {
+    if (!buf || !len) return CVLG_E_INVALID_ARG;
+    std::strncpy(buf, t_last_error.c_str(), len - 1);
+    buf[len - 1] = 0;
+    return CVLG_OK;
+}
+
+}  // extern "C"

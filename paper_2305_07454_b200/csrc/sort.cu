@@ -1,0 +1,247 @@
+// Stable LSD radix sort (u64 keys, u32 values) and a device-wide exclusive scan, written for
+// sm_100a without CUB/Thrust (north_star: no library sort as product code).
+//
+// Per 8-bit digit pass: (1) per-tile digit histograms, (2) digit-major exclusive scan of the
+// histograms so tile t's keys of digit d precede tile t+1's (stability), (3) per-tile stable
+// ranking with __match_any_sync peer groups and per-warp digit counters in shared memory, then
+// scatter. Passes whose digit is constant across all keys are skipped (decided on the host from a
+// device-side OR/AND reduction of the keys).
+#include "kernels.cuh"
+#include "sort_api.cuh"
+
+namespace cvlg {
+
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t* in, uint64_t n,
+                                                                   uint32_t* partial) {
+    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile;
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        const uint64_t idx = base + static_cast<uint64_t>(i) * kScanThreads + threadIdx.x;
+        if (idx < n) s += in[idx];
+    }
+    s = warp_sum(s);
+    __shared__ uint32_t ws[kScanThreads / 32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < kScanThreads / 32; ++w) t += ws[w];
+        partial[blockIdx.x] = t;
+    }
+}
+
+// single CTA: exclusive scan of partial[0..n) in place, total -> *total
+__global__ void __launch_bounds__(1024) scan_partials_kernel(uint32_t* partial, uint64_t n,
+                                                             uint32_t* total) {
+    __shared__ uint32_t sm[1024 / 32 + 1];
+    uint32_t carry = 0;
+    for (uint64_t base = 0; base < n; base += 1024) {
+        const uint64_t idx = base + threadIdx.x;
+        const uint32_t v = idx < n ? partial[idx] : 0u;
+        uint32_t tot;
+        const uint32_t ex = block_exclusive_scan<1024>(v, sm, tot);
+        if (idx < n) partial[idx] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0 && total) *total = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const uint32_t* in, uint32_t* out,
+                                                                 uint64_t n,
+                                                                 const uint32_t* partial) {
+    __shared__ uint32_t sm[kScanThreads / 32 + 1];
+    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile;
+    // blocked arrangement: thread t owns items [t*8, t*8+8)
+    uint32_t v[kScanItems];
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        const uint64_t idx = base + static_cast<uint64_t>(threadIdx.x) * kScanItems + i;
+        v[i] = idx < n ? in[idx] : 0u;
+        s += v[i];
+    }
+    uint32_t tot;
+    uint32_t ex = block_exclusive_scan<kScanThreads>(s, sm, tot) + partial[blockIdx.x];
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        const uint64_t idx = base + static_cast<uint64_t>(threadIdx.x) * kScanItems + i;
+        if (idx < n) out[idx] = ex;
+        ex += v[i];
+    }
+}
+
+// ---- radix ----------------------------------------------------------------------------------
+constexpr int kRThreads = 256;
+constexpr int kRItems = 16;
+constexpr int kRTile = kRThreads * kRItems;  // 4096 keys per tile
+constexpr int kRWarps = kRThreads / 32;
+constexpr int kRWarpKeys = kRTile / kRWarps;  // 512 keys per warp, 16 rounds of 32
+
+__global__ void __launch_bounds__(kRThreads) radix_hist_kernel(const uint64_t* keys, uint64_t n,
+                                                               int shift, uint32_t* counts,
+                                                               uint32_t n_tiles) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRTile;
+#pragma unroll 4
+    for (int i = 0; i < kRItems; ++i) {
+        const uint64_t idx = base + static_cast<uint64_t>(i) * kRThreads + threadIdx.x;
+        if (idx < n) {
+            const uint32_t d = static_cast<uint32_t>(keys[idx] >> shift) & 0xFFu;
+            atomicAdd(&h[d], 1u);
+        }
+    }
+    __syncthreads();
+    counts[static_cast<uint64_t>(threadIdx.x) * n_tiles + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kRThreads) radix_scatter_kernel(
+    const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_out, uint32_t* vals_out,
+    uint64_t n, int shift, const uint32_t* offsets, uint32_t n_tiles) {
+    __shared__ uint32_t wc[kRWarps][256];
+    __shared__ uint32_t tile_off[256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kRWarps * 256; i += kRThreads) (&wc[0][0])[i] = 0;
+    tile_off[threadIdx.x] = offsets[static_cast<uint64_t>(threadIdx.x) * n_tiles + blockIdx.x];
+    __syncthreads();
+    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRTile + static_cast<uint64_t>(warp) * kRWarpKeys;
+    uint64_t k[kRItems];
+    uint32_t v[kRItems];
+    uint32_t rank[kRItems];
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < kRItems; ++i) {
+        const uint64_t idx = base + static_cast<uint64_t>(i) * 32 + lane;
+        const bool valid = idx < n;
+        k[i] = valid ? keys_in[idx] : 0ull;
+        v[i] = valid ? vals_in[idx] : 0u;
+        const uint32_t d = valid ? (static_cast<uint32_t>(k[i] >> shift) & 0xFFu) : 256u;
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+        uint32_t r = 0;
+        if (valid) {
+            const uint32_t before = wc[warp][d];
+            r = before + __popc(peers & lt);
+        }
+        __syncwarp();
+        if (valid && (peers & lt) == 0) wc[warp][d] += __popc(peers);
+        __syncwarp();
+        rank[i] = r;
+    }
+    __syncthreads();
+    // exclusive prefix across warps, per digit
+    {
+        const int d = threadIdx.x;
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < kRWarps; ++w) {
+            const uint32_t t = wc[w][d];
+            wc[w][d] = run;
+            run += t;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kRItems; ++i) {
+        const uint64_t idx = base + static_cast<uint64_t>(i) * 32 + lane;
+        if (idx < n) {
+            const uint32_t d = static_cast<uint32_t>(k[i] >> shift) & 0xFFu;
+            const uint64_t pos = static_cast<uint64_t>(tile_off[d]) + wc[warp][d] + rank[i];
+            keys_out[pos] = k[i];
+            vals_out[pos] = v[i];
+        }
+    }
+}
+
+__global__ void key_or_and_kernel(const uint64_t* keys, uint64_t n, unsigned long long* acc) {
+    uint64_t o = 0, a = ~0ull;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        o |= keys[i];
+        a &= keys[i];
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        o |= __shfl_xor_sync(0xFFFFFFFFu, o, s);
+        a &= __shfl_xor_sync(0xFFFFFFFFu, a, s);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicOr(&acc[0], o);
+        atomicAnd(&acc[1], a);
+    }
+}
+
+}  // namespace
+
+uint64_t scan_temp_words(uint64_t n) { return (n + kScanTile - 1) / kScanTile + 2; }
+
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* d_total,
+                        uint32_t* d_tmp, cudaStream_t s) {
+    const uint64_t nb = (n + kScanTile - 1) / kScanTile;
+    if (nb == 0) {
+        if (d_total) cudaMemsetAsync(d_total, 0, 4, s);
+        return;
+    }
+    scan_reduce_kernel<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, n, d_tmp);
+    count_launch();
+    scan_partials_kernel<<<1, 1024, 0, s>>>(d_tmp, nb, d_total);
+    count_launch();
+    scan_down_kernel<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, out, n, d_tmp);
+    count_launch();
+}
+
+uint64_t radix_temp_bytes(uint64_t n) {
+    const uint64_t tiles = (n + kRTile - 1) / kRTile;
+    const uint64_t counts = 256 * tiles;
+    return (counts + scan_temp_words(counts) + 16) * 4 + 64;
+}
+
+void radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,
+                      uint64_t n, int begin_bit, int end_bit, void* d_tmp, cudaStream_t s,
+                      unsigned long long* d_orand, unsigned long long* h_orand) {
+    if (n <= 1 || end_bit <= begin_bit) return;
+    // constant-digit detection
+    uint64_t diff = ~0ull;
+    if (d_orand && h_orand) {
+        const unsigned long long init[2] = {0ull, ~0ull};
+        cudaMemcpyAsync(d_orand, init, 16, cudaMemcpyHostToDevice, s);
+        const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 2048));
+        key_or_and_kernel<<<blocks, 256, 0, s>>>(keys, n, d_orand);
+        count_launch();
+        cudaMemcpyAsync(h_orand, d_orand, 16, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        diff = h_orand[0] ^ h_orand[1];
+    }
+    const uint32_t n_tiles = static_cast<uint32_t>((n + kRTile - 1) / kRTile);
+    const uint64_t n_counts = 256ull * n_tiles;
+    uint32_t* counts = static_cast<uint32_t*>(d_tmp);
+    uint32_t* scan_tmp = counts + n_counts;
+    uint64_t* ki = keys;
+    uint32_t* vi = vals;
+    uint64_t* ko = keys_alt;
+    uint32_t* vo = vals_alt;
+    for (int shift = begin_bit; shift < end_bit; shift += 8) {
+        if (((diff >> shift) & 0xFFull) == 0) continue;  // digit constant: order unchanged
+        radix_hist_kernel<<<n_tiles, kRThreads, 0, s>>>(ki, n, shift, counts, n_tiles);
+        count_launch();
+        exclusive_scan_u32(counts, counts, n_counts, nullptr, scan_tmp, s);
+        radix_scatter_kernel<<<n_tiles, kRThreads, 0, s>>>(ki, vi, ko, vo, n, shift, counts,
+                                                           n_tiles);
+        count_launch();
+        std::swap(ki, ko);
+        std::swap(vi, vo);
+    }
+    if (ki != keys) {
+        cudaMemcpyAsync(keys, ki, n * 8, cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(vals, vi, n * 4, cudaMemcpyDeviceToDevice, s);
+    }
+}
+
+}  // namespace cvlg

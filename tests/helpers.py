@@ -1,0 +1,59 @@
+"""Shared test helpers: input builders and the frame comparator (compare_days analogue,
+proj/tests/acceptance.cpp:99-120, here bit-exact)."""
+from __future__ import annotations
+
+import random
+from pathlib import Path
+
+import numpy as np
+
+HEADER = b"Journey Id,Timestamp,Latitude,Longitude,Postal Code,Speed,Heading"
+
+
+def write_shards(dirpath: Path, contents: list[bytes], prefix="shard_") -> list[str]:
+    dirpath.mkdir(parents=True, exist_ok=True)
+    paths = []
+    for i, c in enumerate(contents):
+        p = dirpath / f"{prefix}{i:04d}.csv"
+        p.write_bytes(c)
+        paths.append(str(p))
+    return paths
+
+
+def shuffle_rows(paths: list[str], out_dir: Path, n_out: int, seed: int) -> list[str]:
+    """Adversarial variant: all data rows shuffled across n_out shards."""
+    rows = []
+    for p in paths:
+        lines = Path(p).read_bytes().split(b"\n")
+        rows.extend(l for l in lines[1:] if l)
+    rng = random.Random(seed)
+    rng.shuffle(rows)
+    contents = [HEADER + b"\n" + b"\n".join(rows[i::n_out]) + b"\n" for i in range(n_out)]
+    return write_shards(out_dir, contents)
+
+
+def diff_lattice(exp_planes, exp_raw, got_planes, got_raw) -> str:
+    """'' when bit-identical, else a description of the first divergence."""
+    if exp_planes.shape != got_planes.shape:
+        return f"shape {exp_planes.shape} vs {got_planes.shape}"
+    for ch in range(8):
+        a, b = exp_planes[:, ch], got_planes[:, ch]
+        if not np.array_equal(a, b):
+            idx = np.argwhere(a != b)[0]
+            what = "speed" if ch < 4 else "volume"
+            return (f"{what} d={ch % 4} differs at t={idx[0]} r={idx[1]} c={idx[2]}: "
+                    f"{a[tuple(idx)]:#x} vs {b[tuple(idx)]:#x} "
+                    f"({int((a != b).sum())} cells differ)")
+    if exp_raw is not None and got_raw is not None and not np.array_equal(exp_raw, got_raw):
+        idx = np.argwhere(exp_raw != got_raw)[0]
+        return f"raw_count differs at {tuple(idx)}: {exp_raw[tuple(idx)]} vs {got_raw[tuple(idx)]}"
+    return ""
+
+
+def stats_dict(st) -> dict:
+    return {
+        "rows_read": st.rows_read, "parsed": st.parsed,
+        "duplicates_dropped": st.duplicates_dropped,
+        "conflicting_duplicates": st.conflicting_duplicates, "accepted": st.accepted,
+        "rejected": dict(st.rejected), "filtered": dict(st.filtered),
+    }

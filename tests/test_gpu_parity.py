@@ -1,0 +1,254 @@
+"""GPU parity: the sm_100a pipeline (through the C ABI) against the UNMODIFIED reference
+cvl::run_pipeline (oracle/_ref) on the same shard files. Bar: bit-identical speed bits, volumes,
+raw counts and identical PipelineStats (SURVEY §8c parity plan iii/iv)."""
+from __future__ import annotations
+
+import random
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from helpers import HEADER, diff_lattice, shuffle_rows, stats_dict, write_shards
+
+pytestmark = pytest.mark.gpu
+
+
+def run_both(ref, paths, spec, rules=None, partitions=3):
+    import paper_2305_07454_b200 as cvlg
+    ep, er, est, _ = ref.run_pipeline(paths, spec, rules, n_partitions=partitions, n_threads=1)
+    st = cvlg.PipelineStats()
+    lat = cvlg.run_pipeline(paths, spec, rules or cvlg.FilterRules(), n_partitions=partitions,
+                            stats=st)
+    return (ep, er, est), (lat.planes, lat.raw, stats_dict(st))
+
+
+def assert_parity(ref, paths, spec, rules=None):
+    (ep, er, est), (gp, gr, gst) = run_both(ref, paths, spec, rules)
+    d = diff_lattice(ep, er, gp, gr)
+    assert d == "", d
+    assert gst == est
+    return est
+
+
+def spec_default():
+    import paper_2305_07454_b200 as cvlg
+    return cvlg.GridSpec()
+
+
+def spec_coarse():
+    import paper_2305_07454_b200 as cvlg
+    return cvlg.GridSpec(lat_step=0.25, lon_step=0.25)
+
+
+def spec_degenerate():
+    import paper_2305_07454_b200 as cvlg
+    return cvlg.GridSpec(lat_step=10.0, lon_step=10.0)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_synth_day_default_grid(ref, day_cache, seed):
+    paths, rows = day_cache(seed=seed, journeys=120, mean_duration=300.0)
+    est = assert_parity(ref, paths, spec_default())
+    assert est["rows_read"] == rows and est["accepted"] == rows
+
+
+@pytest.mark.parametrize("grid", ["coarse", "degenerate"])
+def test_acceptance_grids(ref, day_cache, grid):
+    # acceptance.cpp:130-159 grids
+    paths, _ = day_cache(seed=7, journeys=150, mean_duration=240.0)
+    assert_parity(ref, paths, spec_coarse() if grid == "coarse" else spec_degenerate())
+
+
+def test_grid_variants(ref, day_cache):
+    import paper_2305_07454_b200 as cvlg
+    paths, _ = day_cache(seed=11, journeys=80)
+    for spec in [cvlg.GridSpec(min_step=60), cvlg.GridSpec(dxn_offset=45.0),
+                 cvlg.GridSpec(dxn_step=180, min_step=1440), cvlg.GridSpec(dxn_step=360),
+                 cvlg.GridSpec(lat_step=0.013, lon_step=0.007, min_step=1),
+                 cvlg.GridSpec(lat_min=37.0, lat_max=38.0, lon_min=-93.0, lon_max=-92.0,
+                               lat_step=0.01, lon_step=0.01),
+                 cvlg.GridSpec(dxn_step=120, dxn_offset=-30.0)]:
+        assert_parity(ref, paths, spec)
+
+
+def test_duplicates_slow_path(ref, day_cache):
+    # sample_period 0.5 renders duplicate (journey, second) keys (test_synth.cpp:104-140)
+    paths, _ = day_cache(seed=5, journeys=60, sample_period=0.5)
+    est = assert_parity(ref, paths, spec_default())
+    assert est["duplicates_dropped"] > 0
+
+
+def test_shuffled_rows(ref, day_cache, tmp_path):
+    paths, _ = day_cache(seed=9, journeys=100)
+    sh = shuffle_rows(paths, tmp_path / "sh", 7, seed=3)
+    assert_parity(ref, sh, spec_default())
+    assert_parity(ref, sh, spec_degenerate())
+
+
+def test_shuffled_with_dups(ref, day_cache, tmp_path):
+    paths, _ = day_cache(seed=5, journeys=60, sample_period=0.5)
+    sh = shuffle_rows(paths, tmp_path / "sh", 5, seed=4)
+    est = assert_parity(ref, sh, spec_default())
+    assert est["duplicates_dropped"] > 0
+
+
+def test_manifest_order_and_partitions(ref, day_cache):
+    import paper_2305_07454_b200 as cvlg
+    paths, _ = day_cache(seed=2, journeys=90)
+    base = cvlg.run_pipeline(paths, spec_coarse(), n_partitions=1)
+    shuffled = list(paths)
+    random.Random(13).shuffle(shuffled)
+    for parts in (2, 4, 16):
+        other = cvlg.run_pipeline(shuffled, spec_coarse(), n_partitions=parts)
+        assert np.array_equal(base.planes, other.planes)
+    ep, _, _, _ = ref.run_pipeline(shuffled, spec_coarse(), n_partitions=4)
+    assert np.array_equal(ep, base.planes)
+
+
+def test_table1_rows(ref, tmp_path):
+    # acceptance.cpp:247-293 golden rows (dedup 4->3, volume 3, mean 51.45333)
+    rows = [
+        b"33456rd,2021-05-09 03:48:42,37.664087,-92.6546,65536,105.98,33",
+        b"31224tf,2021-05-09 03:49:42,37.667707,-92.6490,65536,0,53",
+        b"22124fs,2021-05-09 03:49:49,37.690978,-92.6490,65536,48.38,33",
+        b"33456rd,2021-05-09 03:48:42,37.664087,-92.6546,65536,105.98,33",
+    ]
+    paths = write_shards(tmp_path, [HEADER + b"\n" + b"\n".join(rows) + b"\n"])
+    est = assert_parity(ref, paths, spec_degenerate())
+    assert est["duplicates_dropped"] == 1 and est["accepted"] == 3
+    import paper_2305_07454_b200 as cvlg
+    lat = cvlg.run_pipeline(paths, spec_degenerate())
+    assert lat.volume[45, 0, 0, 0] == 3
+    assert abs(float(lat.speed[45, 0, 0, 0]) - 51.45333) < 1e-5
+
+
+def test_malformed_and_edge_inputs(ref, tmp_path):
+    import corpus
+    rng = random.Random(5)
+    body = corpus.line_corpus(rng, 3000)
+    good = [b"jj%03d,2021-05-09 %02d:%02d:%02d,%.6f,%.6f,65101,%.2f,%.2f" % (
+        i % 17, (i // 3600) % 24, (i // 60) % 60, i % 60, 36.1 + (i % 400) * 0.01,
+        -95.7 + (i % 600) * 0.011, (i * 7.3) % 140, (i * 13.7) % 360) for i in range(4000)]
+    mixed = body + good
+    rng.shuffle(mixed)
+    contents = [
+        HEADER + b"\r\n" + b"\r\n".join(mixed[:1500]) + b"\r\n",
+        HEADER + b"\n" + b"\n\n".join(mixed[1500:4000]),  # blank lines, no trailing newline
+        b"",  # empty shard: no header, no rows
+        b"nope,nope\n1,2\n",  # BadHeader
+        b"heading,speed,zip code,longitude,latitude,timestamp,journey-id\n" + b"\n".join(
+            b"%s,%s,%s,%s,%s,%s,%s" % tuple(reversed(l.split(b",")[:7])) for l in good[:800]
+            if len(l.split(b",")) == 7),
+        HEADER,  # header only, no newline
+        HEADER + b"\n" + b"\n".join(mixed[4000:]) + b"\n",
+    ]
+    paths = write_shards(tmp_path, contents)
+    for spec in (spec_default(), spec_degenerate()):
+        est = assert_parity(ref, paths, spec)
+    assert est["rejected"].get("BadHeader") == 1
+    assert sum(est["rejected"].values()) > 100
+
+
+def test_long_and_unusual_ids(ref, tmp_path):
+    rng = random.Random(8)
+    ids = (["vehicle-%012d" % i for i in range(40)] + ["j%07d" % i for i in range(999990, 1000010)]
+           + ["x" * n for n in range(1, 20)] + ["é%d" % i for i in range(5)]
+           + ["a\tb", "ab", "ab\x00", "ab\x00\x00", "\xff\xfe", "\x7f" * 16, "q" * 300])
+    lines = []
+    for k in range(6000):
+        jid = rng.choice(ids).encode("latin-1")
+        lines.append(b"%s,2021-05-09 %02d:%02d:%02d,%.6f,%.6f,65101,%.2f,%.2f" % (
+            jid, rng.randrange(24), rng.randrange(60), rng.randrange(60),
+            rng.uniform(36.0, 40.6), rng.uniform(-95.8, -89.1), rng.uniform(0, 140),
+            rng.uniform(0, 360)))
+    paths = write_shards(tmp_path, [HEADER + b"\n" + b"\n".join(lines[i::3]) + b"\n"
+                                    for i in range(3)])
+    for spec in (spec_default(), spec_degenerate()):
+        assert_parity(ref, paths, spec)
+
+
+def test_filters(ref, day_cache, tmp_path):
+    import paper_2305_07454_b200 as cvlg
+    paths, _ = day_cache(seed=4, journeys=80)
+    narrow = cvlg.GridSpec(lat_min=37.0, lat_max=39.0, lon_min=-94.0, lon_max=-91.0)
+    est = assert_parity(ref, paths, narrow)
+    assert est["filtered"]["OutOfGrid"] > 0
+    est = assert_parity(ref, paths, spec_default(), cvlg.FilterRules(speed_ceiling=80.0))
+    assert est["filtered"]["SpeedCeiling"] > 0
+
+
+def test_out_of_bounds_error(day_cache):
+    import paper_2305_07454_b200 as cvlg
+    paths, _ = day_cache(seed=4, journeys=40)
+    narrow = cvlg.GridSpec(lat_min=37.0, lat_max=39.0, lon_min=-94.0, lon_max=-91.0)
+    with pytest.raises(cvlg.CvlError) as e:
+        cvlg.run_pipeline(paths, narrow, cvlg.FilterRules(require_in_grid=False))
+    assert e.value.code == "OutOfBounds"
+
+
+def test_multi_day_fold(ref, day_cache):
+    # time_bin ignores the date (grid.cpp:69-71): two days fold onto one lattice
+    a, _ = day_cache(seed=21, journeys=60, day="2021-05-09")
+    b, _ = day_cache(seed=21, journeys=60, day="2021-05-10")
+    c, _ = day_cache(seed=22, journeys=60, day="2021-05-11")
+    assert_parity(ref, a + b + c, spec_default())
+
+
+def test_container_bytes(ref, day_cache, tmp_path):
+    import paper_2305_07454_b200 as cvlg
+    paths, _ = day_cache(seed=3, journeys=50)
+    spec = spec_coarse()
+    lat = cvlg.run_pipeline(paths, spec)
+    ours = tmp_path / "ours.cvl1"
+    theirs = tmp_path / "ref.cvl1"
+    n = cvlg.write_container(lat, spec, 18756, ours)
+    ep, _, _, _ = ref.run_pipeline(paths, spec)
+    m = ref.write_container(ep, spec, 18756, theirs)
+    assert n == m and ours.read_bytes() == theirs.read_bytes()
+
+
+def test_host_and_device_entry_points(ref, day_cache):
+    import torch
+    import paper_2305_07454_b200 as cvlg
+    paths, _ = day_cache(seed=6, journeys=70)
+    spec = spec_default()
+    ep, er, est, _ = ref.run_pipeline(sorted(paths), spec)
+    bufs = [Path(p).read_bytes() for p in sorted(paths)]
+    st = cvlg.PipelineStats()
+    lat = cvlg.run_pipeline_host(bufs, spec, stats=st)
+    assert diff_lattice(ep, er, lat.planes, lat.raw) == ""
+    assert stats_dict(st) == est
+    blob = b"".join(bufs)
+    offs = [0]
+    for b in bufs:
+        offs.append(offs[-1] + len(b))
+    d_csv = torch.frombuffer(bytearray(blob), dtype=torch.uint8).cuda()
+    t, _, r, c = spec.dims()
+    d_planes = torch.empty((t, 8, r, c), dtype=torch.int32, device="cuda")
+    d_raw = torch.empty((t, 4, r, c), dtype=torch.int32, device="cuda")
+    st2 = cvlg.PipelineStats()
+    cvlg.run_pipeline_device(d_csv.data_ptr(), offs, d_planes.data_ptr(), d_raw.data_ptr(), spec,
+                             stats=st2)
+    torch.cuda.synchronize()
+    gp = d_planes.cpu().numpy().view(np.uint32)
+    gr = d_raw.cpu().numpy().view(np.uint32)
+    assert diff_lattice(ep, er, gp, gr) == ""
+    assert stats_dict(st2) == est
+
+
+def test_empty_manifest(ref):
+    import paper_2305_07454_b200 as cvlg
+    st = cvlg.PipelineStats()
+    lat = cvlg.run_pipeline([], spec_default(), stats=st)
+    ep, er, est, _ = ref.run_pipeline([], spec_default())
+    assert diff_lattice(ep, er, lat.planes, lat.raw) == ""
+    assert stats_dict(st) == est
+
+
+def test_zero_partitions(day_cache):
+    import paper_2305_07454_b200 as cvlg
+    paths, _ = day_cache(seed=1, journeys=10)
+    with pytest.raises(cvlg.CvlError) as e:
+        cvlg.run_pipeline(paths, spec_default(), n_partitions=0)
+    assert e.value.code == "ZeroPartitions"
