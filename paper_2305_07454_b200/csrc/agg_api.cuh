@@ -3,9 +3,25 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace cvlg {
+
+struct DictParams {
+    const uint8_t* csv;
+    const uint64_t* shard_off;
+    const ColumnMap* cmap;
+    uint32_t n_shards;
+    const uint32_t* hslot;
+    const uint64_t* loff;
+    uint64_t n_heads;
+    unsigned long long* table;  // [2 * (mask + 1)]
+    uint64_t mask;
+    uint32_t* hdict;
+    unsigned long long* max_len;
+};
 
 struct FoldParams {
     // journeys: [jstart[j], jstart[j+1]) indexes `perm`
@@ -18,11 +34,18 @@ struct FoldParams {
     const double* speed;
     const uint32_t* code;
     const uint64_t* loff;
-    // (cell, journey) table
+    // (cell, journey) subtotals out: key = cell << rank_bits | rank
     uint64_t* pair_key;
     double* pair_sum;
     uint32_t* pair_cnt;
-    uint64_t pair_mask;
+    uint32_t* pair_count;
+    uint64_t pair_cap;
+    int rank_bits;
+    // spill table for journeys with > 32 distinct cells, key = cell << 32 | rank
+    uint64_t* spill_key;
+    double* spill_sum;
+    uint32_t* spill_cnt;
+    uint64_t spill_mask;
     // conflict re-parse
     const uint8_t* csv;
     const uint64_t* shard_off;
@@ -31,9 +54,10 @@ struct FoldParams {
     uint64_t* stats;
 };
 
-void launch_dict_insert(const DecodeOut& d, uint64_t n_heads, const uint8_t* csv,
-                        unsigned long long* table, uint64_t mask, uint32_t* hdict, uint64_t* stats,
-                        unsigned long long* max_len, cudaStream_t s);
+void launch_head_flags(const uint32_t* code, uint64_t n, uint32_t* flags, cudaStream_t s);
+void launch_head_compact(const uint32_t* flags, const uint32_t* pos, uint64_t n, uint32_t* hslot,
+                         cudaStream_t s);
+void launch_dict_insert(const DictParams& d, cudaStream_t s);
 void launch_dict_flags(const unsigned long long* table, uint64_t cap, uint32_t* flags,
                        cudaStream_t s);
 void launch_dict_compact(const uint32_t* flags, const uint32_t* pos, uint64_t cap, uint32_t* uslot,
@@ -50,18 +74,17 @@ void launch_head_keys(const uint32_t* hrank, const uint32_t* hslot, const int64_
 void launch_gather_rank_keys(const uint32_t* rank_src, const uint32_t* vals, uint64_t n,
                              uint64_t* keys, cudaStream_t s);
 void launch_head_order_check(const uint32_t* perm, const uint32_t* hrank, const uint32_t* hslot,
-                             const int64_t* ts, uint64_t n_heads, uint64_t n_slots,
-                             uint32_t* jstart, uint32_t* invalid, cudaStream_t s);
+                             const int64_t* ts, const uint32_t* code, uint64_t n_heads,
+                             uint64_t n_slots, uint32_t* jstart, uint32_t* invalid,
+                             cudaStream_t s);
 void launch_slot_keys(const uint32_t* hslot, const uint32_t* hrank, uint64_t n_heads,
-                      const int64_t* ts, uint64_t n_slots, int64_t ts_min, int tsbits, int mode,
-                      uint64_t* keys, uint32_t* vals, uint32_t* srank, cudaStream_t s);
-void launch_slot_jstart(const uint32_t* perm, const uint32_t* srank, uint64_t n, uint32_t* jstart,
-                        cudaStream_t s);
+                      const int64_t* ts, const uint32_t* code, uint64_t n_slots, int64_t ts_min,
+                      int tsbits, int mode, uint32_t reject_rank, uint64_t* keys, uint32_t* vals,
+                      uint32_t* srank, cudaStream_t s);
+void launch_slot_jstart(const uint32_t* perm, const uint32_t* srank, uint64_t n,
+                        uint32_t reject_rank, uint32_t* jstart, cudaStream_t s);
 void launch_fold(const FoldParams& p, bool slow, cudaStream_t s);
-void launch_pair_flags(const uint64_t* pair_key, uint64_t cap, uint32_t* flags, cudaStream_t s);
-void launch_pair_compact(const uint64_t* pair_key, const uint32_t* flags, const uint32_t* pos,
-                         uint64_t cap, int rank_bits, uint64_t* keys, uint32_t* vals,
-                         cudaStream_t s);
+void launch_pair_vals(uint32_t* vals, uint64_t n, cudaStream_t s);
 void launch_finalize(const uint64_t* keys, const uint32_t* vals, uint64_t n, int rank_bits,
                      const double* pair_sum, const uint32_t* pair_cnt, uint32_t D, uint64_t RC,
                      uint32_t* planes, uint32_t* raw, cudaStream_t s);

@@ -16,6 +16,7 @@ namespace cvlg {
 namespace {
 
 constexpr uint64_t kEmpty = ~0ull;
+constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
     x ^= x >> 33;
@@ -45,44 +46,97 @@ __device__ __forceinline__ bool bytes_equal(const uint8_t* a, const uint8_t* b, 
     return true;
 }
 
-// ---- D1: dictionary insert (one thread per run head) -----------------------------------------
-__global__ void dict_insert_kernel(const uint64_t* hk0, const uint64_t* hk1, const uint64_t* hidref,
-                                   const uint64_t* hhash, uint64_t n_heads, const uint8_t* csv,
-                                   unsigned long long* table, uint64_t mask, uint32_t* hdict,
-                                   uint64_t* stats, unsigned long long* max_len) {
-    const uint64_t h = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    if (h >= n_heads) return;
-    uint64_t e0, e1, slot;
-    const uint64_t k1 = hk1[h];
-    const bool is_long = (k1 & 0xFF) == 0xFF;
-    uint32_t len;
-    uint64_t off = 0;
-    if (!is_long) {
-        e0 = hk0[h];
-        e1 = k1;
-        len = static_cast<uint32_t>(k1 & 0xFF);
-        slot = mix64(e0 ^ mix64(e1)) & mask;
-    } else {
-        const uint64_t ref = hidref[h];
-        off = ref >> 24;
-        len = static_cast<uint32_t>(ref & 0xFFFFFF);
-        e0 = (hhash[h] & ~0xFFFFFFull) | len;
-        e1 = (off << 8) | 0xFF;
-        slot = mix64(hhash[h]) & mask;
+__device__ __forceinline__ uint32_t shard_of(const uint64_t* shard_off, uint32_t n_shards,
+                                             uint64_t p) {
+    uint32_t lo = 0, hi = n_shards;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) / 2;
+        if (shard_off[mid] <= p) lo = mid;
+        else hi = mid;
     }
-    if (len) atomicMax(max_len, static_cast<unsigned long long>(len));
-    for (uint64_t probe = 0; probe <= mask; ++probe) {
+    return lo;
+}
+
+// Journey id span of the (accepted) line at `loff`: field cmap.journey_id, trimmed
+// (ingest.cpp:31-53, 128).
+__device__ void locate_id(const uint8_t* csv, const uint64_t* shard_off, uint32_t n_shards,
+                          const ColumnMap* cmap, uint64_t loff, uint64_t& off, uint32_t& len) {
+    const uint32_t s = shard_of(shard_off, n_shards, loff);
+    const uint64_t end = shard_off[s + 1];
+    const int32_t col = cmap[s].journey_id;
+    int32_t field = 0;
+    uint64_t start = loff;
+    for (uint64_t x = loff;; ++x) {
+        const uint8_t c = x < end ? csv[x] : uint8_t('\n');
+        if (c == ',' || c == '\n') {
+            if (field == col) {
+                uint64_t b = start, e = x;
+                while (b < e && is_trim(csv[b])) ++b;
+                while (e > b && is_trim(csv[e - 1])) --e;
+                off = b;
+                len = static_cast<uint32_t>(e - b);
+                return;
+            }
+            if (c == '\n') break;
+            ++field;
+            start = x + 1;
+        }
+    }
+    off = loff;
+    len = 0;
+}
+
+// ---- H: run heads from the slot words --------------------------------------------------------
+__global__ void head_flags_kernel(const uint32_t* code, uint64_t n, uint32_t* flags) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) flags[i] = code[i] >> 31;
+}
+
+__global__ void head_compact_kernel(const uint32_t* flags, const uint32_t* pos, uint64_t n,
+                                    uint32_t* hslot) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i < n && flags[i]) hslot[pos[i]] = static_cast<uint32_t>(i);
+}
+
+// ---- D1: dictionary insert (one thread per run head) -----------------------------------------
+// Short ids (<= 15 bytes) are keyed exactly by (bytes 0..7 BE, bytes 8..14 BE << 8 | len);
+// longer ids by (FNV-1a high 40 bits | len, offset << 8 | 0xFF) with a byte comparison.
+__global__ void dict_insert_kernel(DictParams D) {
+    const uint64_t h = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (h >= D.n_heads) return;
+    uint64_t off;
+    uint32_t len;
+    locate_id(D.csv, D.shard_off, D.n_shards, D.cmap, D.loff[D.hslot[h]], off, len);
+    const uint8_t* p = D.csv + off;
+    uint64_t e0, e1, slot;
+    const bool is_long = len > 15;
+    if (!is_long) {
+        uint64_t k0 = 0, k1 = 0;
+        for (uint32_t i = 0; i < 8; ++i) k0 = (k0 << 8) | (i < len ? p[i] : 0u);
+        for (uint32_t i = 8; i < 15; ++i) k1 = (k1 << 8) | (i < len ? p[i] : 0u);
+        e0 = k0;
+        e1 = (k1 << 8) | len;
+        slot = mix64(e0 ^ mix64(e1)) & D.mask;
+    } else {
+        uint64_t fnv = 1469598103934665603ull;
+        for (uint32_t i = 0; i < len; ++i) fnv = (fnv ^ p[i]) * 1099511628211ull;
+        e0 = (fnv & ~0xFFFFFFull) | (len & 0xFFFFFFu);
+        e1 = (off << 8) | 0xFF;
+        slot = mix64(fnv) & D.mask;
+    }
+    atomicMax(D.max_len, static_cast<unsigned long long>(len));
+    for (uint64_t probe = 0; probe <= D.mask; ++probe) {
         uint64_t o0, o1;
-        cas128(&table[2 * slot], kEmpty, kEmpty, e0, e1, o0, o1);
+        cas128(&D.table[2 * slot], kEmpty, kEmpty, e0, e1, o0, o1);
         if (o0 == kEmpty && o1 == kEmpty) break;  // inserted
         if (!is_long) {
             if (o0 == e0 && o1 == e1) break;
         } else if ((o1 & 0xFF) == 0xFF && o0 == e0) {
-            if (bytes_equal(csv + (o1 >> 8), csv + off, len)) break;
+            if (bytes_equal(D.csv + (o1 >> 8), p, len)) break;
         }
-        slot = (slot + 1) & mask;
+        slot = (slot + 1) & D.mask;
     }
-    hdict[h] = static_cast<uint32_t>(slot);
+    D.hdict[h] = static_cast<uint32_t>(slot);
 }
 
 // ---- D2: occupied slots -> flags for compaction ---------------------------------------------
@@ -100,7 +154,7 @@ __global__ void dict_compact_kernel(const uint32_t* flags, const uint32_t* pos, 
 }
 
 // chunk c (bytes 8c..8c+7, big-endian, zero padded) or the length (c == -1) of unique entry
-// perm[i], for the LSD string sort.
+// perm[i], for the LSD string sort (padded bytes, then length, is std::string order).
 __global__ void dict_chunk_kernel(const unsigned long long* table, const uint32_t* uslot,
                                   const uint32_t* perm, uint64_t n, int c, const uint8_t* csv,
                                   uint64_t* keys) {
@@ -163,8 +217,9 @@ __global__ void gather_rank_keys_kernel(const uint32_t* rank_src, const uint32_t
 
 // ---- O2: validity of the run-merge order + journey starts ------------------------------------
 __global__ void head_order_check_kernel(const uint32_t* perm, const uint32_t* hrank,
-                                        const uint32_t* hslot, const int64_t* ts, uint64_t n_heads,
-                                        uint64_t n_slots, uint32_t* jstart, uint32_t* invalid) {
+                                        const uint32_t* hslot, const int64_t* ts,
+                                        const uint32_t* code, uint64_t n_heads, uint64_t n_slots,
+                                        uint32_t* jstart, uint32_t* invalid) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (i >= n_heads) return;
     const uint32_t h = perm[i];
@@ -174,55 +229,56 @@ __global__ void head_order_check_kernel(const uint32_t* perm, const uint32_t* hr
         return;
     }
     const uint32_t hp = perm[i - 1];
-    const uint64_t end_prev = (hp + 1 < n_heads) ? hslot[hp + 1] : n_slots;
-    const int64_t last_prev = ts[end_prev - 1];
-    const int64_t first_cur = ts[hslot[h]];
-    if (!(last_prev < first_cur)) *invalid = 1u;
+    uint64_t last = ((hp + 1 < n_heads) ? hslot[hp + 1] : n_slots) - 1;
+    while ((code[last] & kCodeMask) == kCodeRejected) --last;  // run head is accepted
+    if (!(ts[last] < ts[hslot[h]])) *invalid = 1u;
 }
 
 // ---- S: slow path: per-slot journey rank, sort keys ------------------------------------------
 __global__ void slot_keys_kernel(const uint32_t* hslot, const uint32_t* hrank, uint64_t n_heads,
-                                 const int64_t* ts, uint64_t n_slots, int64_t ts_min, int tsbits,
-                                 int mode, uint64_t* keys, uint32_t* vals, uint32_t* srank) {
+                                 const int64_t* ts, const uint32_t* code, uint64_t n_slots,
+                                 int64_t ts_min, int tsbits, int mode, uint32_t reject_rank,
+                                 uint64_t* keys, uint32_t* vals, uint32_t* srank) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (i >= n_slots) return;
-    // run = last head with hslot <= i
-    uint64_t lo = 0, hi = n_heads;
-    while (hi - lo > 1) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (hslot[mid] <= i) lo = mid;
-        else hi = mid;
+    uint32_t r;
+    uint64_t t = 0;
+    if ((code[i] & kCodeMask) == kCodeRejected || n_heads == 0 || hslot[0] > i) {
+        r = reject_rank;  // sorts after every journey and is never folded
+    } else {
+        uint64_t lo = 0, hi = n_heads;  // run = last head with hslot <= i
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (hslot[mid] <= i) lo = mid;
+            else hi = mid;
+        }
+        r = hrank[lo];
+        t = static_cast<uint64_t>(ts[i] - ts_min);
     }
-    const uint32_t r = hrank[lo];
-    const uint64_t t = static_cast<uint64_t>(ts[i] - ts_min);
     keys[i] = mode == 0 ? ((static_cast<uint64_t>(r) << tsbits) | t) : t;
     vals[i] = static_cast<uint32_t>(i);
     srank[i] = r;
 }
 
 __global__ void slot_jstart_kernel(const uint32_t* perm, const uint32_t* srank, uint64_t n,
-                                   uint32_t* jstart) {
+                                   uint32_t reject_rank, uint32_t* jstart) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (i >= n) return;
     const uint32_t r = srank[perm[i]];
     if (i == 0 || srank[perm[i - 1]] != r) jstart[r] = static_cast<uint32_t>(i);
+    (void)reject_rank;  // jstart[reject_rank] marks the end of the last journey
 }
 
 // ---- payload re-parse for the duplicate-conflict check (aggregate.cpp:286) -------------------
 __device__ bool parse_at(const FoldParams& P, uint64_t loff, Parsed& pr, const uint8_t*& line) {
-    uint32_t lo = 0, hi = P.n_shards;
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) / 2;
-        if (P.shard_off[mid] <= loff) lo = mid;
-        else hi = mid;
-    }
-    const uint64_t s_end = P.shard_off[lo + 1];
+    const uint32_t s = shard_of(P.shard_off, P.n_shards, loff);
+    const uint64_t s_end = P.shard_off[s + 1];
     uint64_t e = loff;
     while (e < s_end && P.csv[e] != '\n') ++e;
     int32_t len = static_cast<int32_t>(e - loff);
     line = P.csv + loff;
     if (len > 0 && line[len - 1] == '\r') --len;
-    return parse_line(line, len, P.cmap[lo], pr) == kAccepted;
+    return parse_line(line, len, P.cmap[s], pr) == kAccepted;
 }
 
 __device__ bool payload_equal(const FoldParams& P, uint64_t la, uint64_t lb) {
@@ -235,136 +291,225 @@ __device__ bool payload_equal(const FoldParams& P, uint64_t la, uint64_t lb) {
     return bytes_equal(pa + a.postal_begin, pb + b.postal_begin, static_cast<uint32_t>(a.postal_len));
 }
 
-// ---- F: per-journey fold into the (cell, journey) table --------------------------------------
-__device__ __forceinline__ uint64_t pair_find_or_insert(const FoldParams& P, uint64_t key,
-                                                        bool& fresh) {
-    uint64_t slot = mix64(key) & P.pair_mask;
-    for (uint64_t probe = 0; probe <= P.pair_mask; ++probe) {
-        const unsigned long long old =
-            atomicCAS(reinterpret_cast<unsigned long long*>(&P.pair_key[slot]), kEmpty, key);
-        if (old == kEmpty) {
-            fresh = true;
-            return slot;
+// ---- F: per-journey fold -----------------------------------------------------------------------
+// One warp per journey. Records arrive 32 at a time in (rank, ts) order; __match_any_sync groups
+// a window's records by cell; each distinct cell of the journey is owned by one lane, which adds
+// its group's speeds in lane (= timestamp) order: the per-(cell, journey) subtotal is exactly the
+// reference's sequential left fold (aggregate.cpp:349-356). A journey with more than 32 distinct
+// cells spills least-recently-assigned accumulators to a (cell, journey) hash table and reloads
+// them on re-entry, preserving the fold order.
+__device__ __forceinline__ uint64_t spill_find(const FoldParams& P, uint64_t key, bool insert) {
+    uint64_t slot = mix64(key) & P.spill_mask;
+    for (uint64_t probe = 0; probe <= P.spill_mask; ++probe) {
+        uint64_t cur = P.spill_key[slot];
+        if (cur == kEmpty && insert) {
+            cur = atomicCAS(reinterpret_cast<unsigned long long*>(&P.spill_key[slot]), kEmpty, key);
+            if (cur == kEmpty) {
+                P.spill_sum[slot] = 0.0;
+                P.spill_cnt[slot] = 0;
+                return slot;
+            }
         }
-        if (old == key) {
-            fresh = false;
-            return slot;
-        }
-        slot = (slot + 1) & P.pair_mask;
+        if (cur == key) return slot;
+        if (cur == kEmpty) return kEmpty;  // not present (find only)
+        slot = (slot + 1) & P.spill_mask;
     }
-    fresh = false;
-    return kEmpty;  // table full (bounded by construction)
+    return kEmpty;
 }
 
 template <bool kSlow>
-__global__ void __launch_bounds__(128) fold_kernel(FoldParams P) {
-    const uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+__global__ void __launch_bounds__(256) fold_warp_kernel(FoldParams P) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
     uint32_t c_acc = 0, c_oog = 0, c_spd = 0, c_miss = 0, c_unb = 0, c_dup = 0, c_conf = 0,
              c_ovf = 0;
-    if (j < P.n_journeys) {
-        const uint64_t rank_bits = static_cast<uint64_t>(j);
-        uint32_t cur_code = kCodeOutOfGrid;  // "none"
-        uint64_t cur_slot = kEmpty;
-        double cur_sum = 0.0;
-        uint32_t cur_cnt = 0;
-        const uint32_t b = P.jstart[j], e = P.jstart[j + 1];
-        int64_t prev_ts = 0;
-        uint64_t surv_slot = 0;
-        bool have_prev = false;
-        // iterate the journey's records in (rank, ts) order
-        uint32_t i = b;
+    for (uint64_t j = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+         j < P.n_journeys; j += warps) {
+        uint32_t own_g = kNone;
+        double own_sum = 0.0;
+        uint32_t own_cnt = 0;
+        uint32_t n_owned = 0, evict = 0;
+        bool spilled = false;
+        const uint32_t jb = P.jstart[j], je = P.jstart[j + 1];
+        // slow path dedup carry
+        int64_t carry_ts = 0;
+        uint64_t carry_surv = 0;
+        bool have_carry = false;
+        uint32_t r = jb;
         uint64_t run_pos = 0, run_end = 0;
         while (true) {
-            uint64_t slot;
+            // ---- next window of up to 32 records ----------------------------------------------
+            uint64_t slot = 0;
+            bool valid;
             if (kSlow) {
-                if (i >= e) break;
-                slot = P.perm[i++];
+                if (r >= je) break;
+                const uint32_t i = r + lane;
+                valid = i < je;
+                if (valid) slot = P.perm[i];
+                r += 32;
             } else {
                 if (run_pos >= run_end) {
-                    if (i >= e) break;
-                    const uint32_t h = P.perm[i++];
+                    if (r >= je) break;
+                    const uint32_t h = P.perm[r++];
                     run_pos = P.hslot[h];
                     run_end = (h + 1 < P.n_heads) ? P.hslot[h + 1] : P.n_slots;
                 }
-                slot = run_pos++;
+                slot = run_pos + lane;
+                valid = slot < run_end;
+                run_pos += 32;
             }
+            uint32_t code = valid ? (P.code[slot] & kCodeMask) : kCodeRejected;
+            const double v = valid ? P.speed[slot] : 0.0;
+            bool dup = false;
             if (kSlow) {
-                const int64_t t = P.ts[slot];
-                if (have_prev && t == prev_ts) {
-                    ++c_dup;
-                    if (!payload_equal(P, P.loff[slot], P.loff[surv_slot])) ++c_conf;
-                    continue;
+                const int64_t t = valid ? P.ts[slot] : 0;
+                const int64_t prev = __shfl_up_sync(0xFFFFFFFFu, t, 1);
+                const bool has_prev = lane > 0 ? true : have_carry;
+                const int64_t pt = lane > 0 ? prev : carry_ts;
+                dup = valid && has_prev && t == pt;
+                const uint32_t heads = __ballot_sync(0xFFFFFFFFu, valid && !dup);
+                if (__ballot_sync(0xFFFFFFFFu, dup)) {
+                    // survivor = nearest earlier non-duplicate lane (min provenance of the
+                    // key group, aggregate.cpp:287-289), or the carried survivor
+                    const uint32_t hb = heads & lt;
+                    const int sl = hb ? 31 - __clz(hb) : lane;
+                    const uint64_t s_from_lane = __shfl_sync(0xFFFFFFFFu, slot, sl);
+                    if (dup) {
+                        ++c_dup;
+                        const uint64_t surv = hb ? s_from_lane : carry_surv;
+                        if (!payload_equal(P, P.loff[slot], P.loff[surv])) ++c_conf;
+                    }
                 }
-                have_prev = true;
-                prev_ts = t;
-                surv_slot = slot;
+                // carry: last valid lane's ts and the survivor at that point
+                const uint32_t vm = __ballot_sync(0xFFFFFFFFu, valid);
+                if (vm) {
+                    const int last = 31 - __clz(vm);
+                    carry_ts = __shfl_sync(0xFFFFFFFFu, t, last);
+                    const uint32_t hb = heads & (last == 31 ? 0xFFFFFFFFu : ((2u << last) - 1u));
+                    if (hb) carry_surv = __shfl_sync(0xFFFFFFFFu, slot, 31 - __clz(hb));
+                    have_carry = true;
+                }
+                if (dup) code = kCodeRejected;  // dropped before filtering (aggregate.cpp:291-293)
             }
-            const uint32_t code = P.code[slot];
-            if (code >= kCodeFirstSpecial) {
+            // ---- filter accounting --------------------------------------------------------------
+            const bool active = code < kCodeFirstSpecial;
+            if (valid && !dup && !active) {
                 if (code == kCodeOutOfGrid) ++c_oog;
                 else if (code == kCodeSpeedCeiling) ++c_spd;
                 else if (code == kCodeMissingField) ++c_miss;
-                else ++c_unb;
-                continue;
+                else if (code == kCodeUnbinnable) ++c_unb;
+                // kCodeRejected: parse rejects are counted by decode
             }
-            ++c_acc;
-            const double v = P.speed[slot];
-            if (code != cur_code) {
-                if (cur_slot != kEmpty) {
-                    P.pair_sum[cur_slot] = cur_sum;
-                    P.pair_cnt[cur_slot] = cur_cnt;
-                }
-                bool fresh;
-                cur_slot = pair_find_or_insert(P, (static_cast<uint64_t>(code) << 32) | rank_bits, fresh);
-                if (cur_slot == kEmpty) {
-                    ++c_ovf;
-                    cur_code = kCodeOutOfGrid;
-                    continue;
-                }
-                cur_code = code;
-                if (fresh) {
-                    cur_sum = 0.0;
-                    cur_cnt = 0;
+            c_acc += active ? 1u : 0u;
+            const uint32_t g = active ? code : kNone;
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, g);
+            uint32_t lmask = __ballot_sync(0xFFFFFFFFu, active && (peers & lt) == 0);
+            uint32_t my_group = 0;
+            while (lmask) {
+                const int L = __ffs(lmask) - 1;
+                lmask &= lmask - 1;
+                const uint32_t gq = __shfl_sync(0xFFFFFFFFu, g, L);
+                const uint32_t grp = __shfl_sync(0xFFFFFFFFu, peers, L);
+                const uint32_t om = __ballot_sync(0xFFFFFFFFu, own_g == gq);
+                int owner;
+                if (om) {
+                    owner = __ffs(om) - 1;
                 } else {
-                    cur_sum = P.pair_sum[cur_slot];
-                    cur_cnt = P.pair_cnt[cur_slot];
+                    if (n_owned < 32) {
+                        owner = static_cast<int>(n_owned++);
+                    } else {
+                        owner = static_cast<int>(evict);
+                        evict = (evict + 1) & 31;
+                        if (lane == owner) {  // spill the evicted accumulator
+                            const uint64_t s = spill_find(P, (static_cast<uint64_t>(own_g) << 32) | j, true);
+                            if (s == kEmpty) ++c_ovf;
+                            else {
+                                P.spill_sum[s] = own_sum;
+                                P.spill_cnt[s] = own_cnt;
+                            }
+                        }
+                        spilled = true;
+                    }
+                    if (lane == owner) {
+                        own_g = gq;
+                        own_sum = 0.0;
+                        own_cnt = 0;
+                        if (spilled) {
+                            const uint64_t s = spill_find(P, (static_cast<uint64_t>(gq) << 32) | j, false);
+                            if (s != kEmpty) {
+                                own_sum = P.spill_sum[s];
+                                own_cnt = P.spill_cnt[s];
+                            }
+                        }
+                    }
+                }
+                if (lane == owner) my_group = grp;
+            }
+            // sequential adds in lane order, one owner lane per cell
+            while (__any_sync(0xFFFFFFFFu, my_group != 0)) {
+                const int src = my_group ? __ffs(my_group) - 1 : lane;
+                const double x = __shfl_sync(0xFFFFFFFFu, v, src);
+                if (my_group) {
+                    own_sum = __dadd_rn(own_sum, x);
+                    ++own_cnt;
+                    my_group &= my_group - 1;
                 }
             }
-            cur_sum = __dadd_rn(cur_sum, v);  // left fold in (rank, ts) order (aggregate.cpp:354)
-            ++cur_cnt;
         }
-        if (cur_slot != kEmpty) {
-            P.pair_sum[cur_slot] = cur_sum;
-            P.pair_cnt[cur_slot] = cur_cnt;
+        // ---- emit this journey's (cell, journey) subtotals ----------------------------------------
+        if (!spilled) {
+            uint32_t base = 0;
+            if (lane == 0 && n_owned) base = atomicAdd(P.pair_count, n_owned);
+            base = __shfl_sync(0xFFFFFFFFu, base, 0);
+            if (static_cast<uint32_t>(lane) < n_owned) {
+                const uint64_t pos = base + lane;
+                if (pos < P.pair_cap) {
+                    P.pair_key[pos] = (static_cast<uint64_t>(own_g) << P.rank_bits) | j;
+                    P.pair_sum[pos] = own_sum;
+                    P.pair_cnt[pos] = own_cnt;
+                } else {
+                    ++c_ovf;
+                }
+            }
+        } else if (own_g != kNone) {
+            const uint64_t s = spill_find(P, (static_cast<uint64_t>(own_g) << 32) | j, true);
+            if (s == kEmpty) ++c_ovf;
+            else {
+                P.spill_sum[s] = own_sum;
+                P.spill_cnt[s] = own_cnt;
+            }
         }
     }
-    unsigned long long v[8] = {c_acc, c_oog, c_spd, c_miss, c_unb, c_dup, c_conf, c_ovf};
+    unsigned long long vals[8] = {c_acc, c_oog, c_spd, c_miss, c_unb, c_dup, c_conf, c_ovf};
     const int idx[8] = {kStAccepted, kStFiltOutOfGrid, kStFiltSpeed, kStFiltMissing,
                         kStUnbinnable, kStDups, kStConflicts, kStOverflow};
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        const unsigned long long s = warp_sum(v[k]);
-        if ((threadIdx.x & 31) == 0 && s)
-            atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[idx[k]]), s);
+        const unsigned long long s = warp_sum(vals[k]);
+        if (lane == 0 && s) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[idx[k]]), s);
     }
 }
 
-// ---- P: pairs -> sorted (g, rank) ------------------------------------------------------------
-__global__ void pair_flags_kernel(const uint64_t* pair_key, uint64_t cap, uint32_t* flags) {
+// spilled journeys' subtotals -> pair list
+__global__ void spill_drain_kernel(FoldParams P) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    if (i >= cap) return;
-    flags[i] = pair_key[i] != kEmpty ? 1u : 0u;
+    if (i > P.spill_mask) return;
+    const uint64_t k = P.spill_key[i];
+    if (k == kEmpty) return;
+    const uint32_t pos = atomicAdd(P.pair_count, 1u);
+    if (pos >= P.pair_cap) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[kStOverflow]), 1ull);
+        return;
+    }
+    P.pair_key[pos] = ((k >> 32) << P.rank_bits) | (k & 0xFFFFFFFFull);
+    P.pair_sum[pos] = P.spill_sum[i];
+    P.pair_cnt[pos] = P.spill_cnt[i];
 }
 
-__global__ void pair_compact_kernel(const uint64_t* pair_key, const uint32_t* flags,
-                                    const uint32_t* pos, uint64_t cap, int rank_bits,
-                                    uint64_t* keys, uint32_t* vals) {
+__global__ void pair_vals_kernel(uint32_t* vals, uint64_t n) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    if (i >= cap || !flags[i]) return;
-    const uint64_t k = pair_key[i];
-    const uint64_t g = k >> 32, r = k & 0xFFFFFFFFull;
-    keys[pos[i]] = (g << rank_bits) | r;
-    vals[pos[i]] = static_cast<uint32_t>(i);
+    if (i < n) vals[i] = static_cast<uint32_t>(i);
 }
 
 // ---- Z: canonical per-cell fold (finalize_range, aggregate.cpp:161-187) ----------------------
@@ -397,13 +542,22 @@ inline unsigned grid_for(uint64_t n, int bs) { return static_cast<unsigned>((n +
 }  // namespace
 
 // ================================ host launchers ================================================
-void launch_dict_insert(const DecodeOut& d, uint64_t n_heads, const uint8_t* csv,
-                        unsigned long long* table, uint64_t mask, uint32_t* hdict, uint64_t* stats,
-                        unsigned long long* max_len, cudaStream_t s) {
-    if (!n_heads) return;
-    dict_insert_kernel<<<grid_for(n_heads, 256), 256, 0, s>>>(d.hk0, d.hk1, d.hidref, d.hhash,
-                                                              n_heads, csv, table, mask, hdict,
-                                                              stats, max_len);
+void launch_head_flags(const uint32_t* code, uint64_t n, uint32_t* flags, cudaStream_t s) {
+    if (!n) return;
+    head_flags_kernel<<<grid_for(n, 256), 256, 0, s>>>(code, n, flags);
+    count_launch();
+}
+
+void launch_head_compact(const uint32_t* flags, const uint32_t* pos, uint64_t n, uint32_t* hslot,
+                         cudaStream_t s) {
+    if (!n) return;
+    head_compact_kernel<<<grid_for(n, 256), 256, 0, s>>>(flags, pos, n, hslot);
+    count_launch();
+}
+
+void launch_dict_insert(const DictParams& d, cudaStream_t s) {
+    if (!d.n_heads) return;
+    dict_insert_kernel<<<grid_for(d.n_heads, 256), 256, 0, s>>>(d);
     count_launch();
 }
 
@@ -452,46 +606,46 @@ void launch_gather_rank_keys(const uint32_t* rank_src, const uint32_t* vals, uin
 }
 
 void launch_head_order_check(const uint32_t* perm, const uint32_t* hrank, const uint32_t* hslot,
-                             const int64_t* ts, uint64_t n_heads, uint64_t n_slots,
-                             uint32_t* jstart, uint32_t* invalid, cudaStream_t s) {
-    head_order_check_kernel<<<grid_for(n_heads, 256), 256, 0, s>>>(perm, hrank, hslot, ts,
+                             const int64_t* ts, const uint32_t* code, uint64_t n_heads,
+                             uint64_t n_slots, uint32_t* jstart, uint32_t* invalid,
+                             cudaStream_t s) {
+    head_order_check_kernel<<<grid_for(n_heads, 256), 256, 0, s>>>(perm, hrank, hslot, ts, code,
                                                                    n_heads, n_slots, jstart,
                                                                    invalid);
     count_launch();
 }
 
 void launch_slot_keys(const uint32_t* hslot, const uint32_t* hrank, uint64_t n_heads,
-                      const int64_t* ts, uint64_t n_slots, int64_t ts_min, int tsbits, int mode,
-                      uint64_t* keys, uint32_t* vals, uint32_t* srank, cudaStream_t s) {
-    slot_keys_kernel<<<grid_for(n_slots, 256), 256, 0, s>>>(hslot, hrank, n_heads, ts, n_slots,
-                                                            ts_min, tsbits, mode, keys, vals,
-                                                            srank);
+                      const int64_t* ts, const uint32_t* code, uint64_t n_slots, int64_t ts_min,
+                      int tsbits, int mode, uint32_t reject_rank, uint64_t* keys, uint32_t* vals,
+                      uint32_t* srank, cudaStream_t s) {
+    slot_keys_kernel<<<grid_for(n_slots, 256), 256, 0, s>>>(hslot, hrank, n_heads, ts, code,
+                                                            n_slots, ts_min, tsbits, mode,
+                                                            reject_rank, keys, vals, srank);
     count_launch();
 }
 
-void launch_slot_jstart(const uint32_t* perm, const uint32_t* srank, uint64_t n, uint32_t* jstart,
-                        cudaStream_t s) {
-    slot_jstart_kernel<<<grid_for(n, 256), 256, 0, s>>>(perm, srank, n, jstart);
+void launch_slot_jstart(const uint32_t* perm, const uint32_t* srank, uint64_t n,
+                        uint32_t reject_rank, uint32_t* jstart, cudaStream_t s) {
+    slot_jstart_kernel<<<grid_for(n, 256), 256, 0, s>>>(perm, srank, n, reject_rank, jstart);
     count_launch();
 }
 
 void launch_fold(const FoldParams& p, bool slow, cudaStream_t s) {
-    if (!p.n_journeys) return;
-    if (slow) fold_kernel<true><<<grid_for(p.n_journeys, 128), 128, 0, s>>>(p);
-    else fold_kernel<false><<<grid_for(p.n_journeys, 128), 128, 0, s>>>(p);
+    if (p.n_journeys) {
+        const uint64_t warps = p.n_journeys;
+        const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((warps + 7) / 8, 148ull * 64));
+        if (slow) fold_warp_kernel<true><<<blocks, 256, 0, s>>>(p);
+        else fold_warp_kernel<false><<<blocks, 256, 0, s>>>(p);
+        count_launch();
+    }
+    spill_drain_kernel<<<grid_for(p.spill_mask + 1, 256), 256, 0, s>>>(p);
     count_launch();
 }
 
-void launch_pair_flags(const uint64_t* pair_key, uint64_t cap, uint32_t* flags, cudaStream_t s) {
-    pair_flags_kernel<<<grid_for(cap, 256), 256, 0, s>>>(pair_key, cap, flags);
-    count_launch();
-}
-
-void launch_pair_compact(const uint64_t* pair_key, const uint32_t* flags, const uint32_t* pos,
-                         uint64_t cap, int rank_bits, uint64_t* keys, uint32_t* vals,
-                         cudaStream_t s) {
-    pair_compact_kernel<<<grid_for(cap, 256), 256, 0, s>>>(pair_key, flags, pos, cap, rank_bits,
-                                                           keys, vals);
+void launch_pair_vals(uint32_t* vals, uint64_t n, cudaStream_t s) {
+    if (!n) return;
+    pair_vals_kernel<<<grid_for(n, 256), 256, 0, s>>>(vals, n);
     count_launch();
 }
 

@@ -65,6 +65,73 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* smem, T& total) {
     return res;
 }
 
+// Decoupled look-back, single u64 counter, split into publish (as early as possible) and a
+// CTA-wide resolve (as late as possible): every thread of the CTA inspects one predecessor, so a
+// window of NT tiles is examined per step. flag: 0 = not ready, 1 = aggregate, 2 = inclusive.
+struct Lookback1 {
+    uint32_t* flag;
+    uint64_t* agg;
+    uint64_t* inc;
+};
+
+__device__ __forceinline__ void lookback1_publish(const Lookback1& st, uint32_t tile, uint64_t a) {
+    if (tile == 0) {
+        st_relaxed_u64(&st.inc[0], a);
+        st_release_u32(&st.flag[0], 2u);
+    } else {
+        st_relaxed_u64(&st.agg[tile], a);
+        st_release_u32(&st.flag[tile], 1u);
+    }
+}
+
+// All NT threads call. Returns the exclusive prefix of `tile` and publishes its inclusive value.
+template <int NT>
+__device__ __forceinline__ uint64_t lookback1_resolve(const Lookback1& st, uint32_t tile, uint64_t a,
+                                                      uint64_t* smem64 /* NT/32 + 2 */) {
+    if (tile == 0) return 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = NT / 32;
+    uint64_t total = 0;
+    int64_t j = static_cast<int64_t>(tile) - 1;
+    __shared__ int s_stop;
+    while (true) {
+        const int64_t idx = j - static_cast<int64_t>(threadIdx.x);
+        uint32_t f = 2;
+        uint64_t v = 0;
+        if (idx >= 0) {
+            do {
+                f = ld_acquire_u32(&st.flag[idx]);
+            } while (f == 0);
+            v = ld_relaxed_u64(f == 2 ? &st.inc[idx] : &st.agg[idx]);
+        }
+        // nearest inclusive predecessor = lowest thread index with f == 2
+        if (threadIdx.x == 0) s_stop = NT;
+        __syncthreads();
+        if (f == 2) atomicMin(&s_stop, static_cast<int>(threadIdx.x));
+        __syncthreads();
+        const int stop = s_stop;
+        if (static_cast<int>(threadIdx.x) > stop) v = 0;
+        v = warp_sum(v);
+        if (lane == 0) smem64[warp] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t s = 0;
+            for (int w = 0; w < NW; ++w) s += smem64[w];
+            smem64[NW] = s;
+        }
+        __syncthreads();
+        total += smem64[NW];
+        __syncthreads();
+        if (stop < NT) break;
+        j -= NT;
+    }
+    if (threadIdx.x == 0) {
+        st_relaxed_u64(&st.inc[tile], total + a);
+        st_release_u32(&st.flag[tile], 2u);
+    }
+    return total;
+}
+
 // Decoupled look-back state for a scan over tiles carrying two u64 counters.
 // flag: 0 = not ready, 1 = aggregate published, 2 = inclusive prefix published.
 struct LookbackState {

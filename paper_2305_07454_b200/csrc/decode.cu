@@ -1,46 +1,193 @@
 // K0 (shard header map) and K1 (tile decode) for sm_100a.
 //
-// K1 is a single pass over the concatenated CSV shards in HBM. Each CTA takes one 16 KB tile
-// (dynamic tile order, so decoupled look-back always makes progress), stages tile + halo in
-// shared memory with 128-bit loads, builds a '\n' bitmap cooperatively, lists the lines that
-// START in the tile, parses one line per thread (ingest.cpp:119-157 semantics via parse.cuh),
-// fuses filter + binning (grid.cuh), compacts accepted records in shared memory in line order,
-// marks run heads (journey id changes or timestamp stops increasing), and finally publishes
-// (accepted, heads) through a decoupled look-back so every record lands at its global ordinal.
-// Because shards are concatenated in lexicographic path order, a record's slot order equals the
-// reference's (shard_rank, line) provenance order (aggregate.cpp:287-289).
+// K1 makes a single pass over the concatenated CSV shards in HBM. Each CTA takes one 16 KB tile
+// (dynamic tile order, so decoupled look-back always makes progress) and:
+//   1. stages tile + 1 KB halo (+16 B before) in shared memory with one TMA bulk copy
+//      (cp.async.bulk + mbarrier); edge tiles use bounded vector loads;
+//   2. builds '\n' and ',' bitmaps cooperatively (SIMD-within-a-register byte compares);
+//   3. lists the DATA lines that start in the tile (non-empty, not a header, good shard) — this
+//      needs no parsing, so the tile publishes its line count to the decoupled look-back
+//      immediately and learns its global slot base before any record is parsed;
+//   4. parses one line per thread: a fast path for plain fields (comma bitmap walk, fixed
+//      19-byte timestamp, Clinger decimal conversion), falling back to the general restatement
+//      of parse_record_impl (parse.cuh) for anything unusual; then filter + binning (grid.cuh);
+//   5. marks run heads (journey id changes or timestamp stops increasing vs. the previous data
+//      line) and writes ts / speed / cell code / line offset at slot = base + line index, so
+//      consecutive threads write consecutive slots.
+// Slots follow byte order; shards are concatenated in lexicographic path order, so slot order
+// equals the reference's (shard_rank, line) provenance order (aggregate.cpp:287-289).
 #include "kernels.cuh"
 
 namespace cvlg {
 
 namespace {
 
-struct Staged {
-    long long ts;
-    double speed;
-    uint32_t code;
-    uint32_t line_rel;  // line start relative to tile begin
-    uint32_t id_rel;    // id start relative to tile begin
-    uint32_t id_len;
-};
+__constant__ double kPow10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,
+                                  1e8,  1e9,  1e10, 1e11, 1e12, 1e13, 1e14, 1e15,
+                                  1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
 
-__device__ __forceinline__ uint32_t nl_mask16(uint4 v) {
-    // bit i set iff byte i of the 16 bytes is '\n'
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@p bra.uni DONE%=;\n\t"
+        "bra.uni WAIT%=;\n"
+        "DONE%=:\n\t}" ::"r"(smem_addr(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// bit i set iff byte i (of 16) equals c4's byte value
+__device__ __forceinline__ uint32_t eq_mask16(uint4 v, uint32_t c4) {
     uint32_t m = 0;
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const uint32_t eq = __vcmpeq4(w[k], 0x0A0A0A0Au) & 0x08040201u;
-        const uint32_t nib = (eq * 0x01010101u) >> 24;  // sum of the 4 selected bits
-        m |= nib << (4 * k);
+        const uint32_t eq = __vcmpeq4(w[k], c4) & 0x08040201u;
+        m |= ((eq * 0x01010101u) >> 24) << (4 * k);
     }
     return m;
 }
 
-__device__ __forceinline__ uint64_t fnv1a(const uint8_t* p, uint32_t n) {
-    uint64_t h = 1469598103934665603ull;
-    for (uint32_t i = 0; i < n; ++i) h = (h ^ p[i]) * 1099511628211ull;
-    return h;
+// [-]digits[.digits] with <= 19 digits and mantissa <= 2^53: the Clinger case of
+// parse_double, computed identically (one correctly rounded IEEE operation). Returns false
+// when the general parser must decide (anything else, including trim characters).
+__device__ __forceinline__ bool fast_number(const uint8_t* __restrict__ s, uint32_t n, double& v) {
+    uint32_t i = 0;
+    const bool neg = s[0] == '-';
+    if (neg) i = 1;
+    uint32_t w32 = 0;  // first 9 digits in 32-bit arithmetic
+    uint32_t nd = 0, dot = 0xFFFFFFFFu;
+    for (; i < n && nd < 9; ++i) {
+        const uint32_t d = static_cast<uint32_t>(s[i]) - '0';
+        if (d < 10) {
+            w32 = w32 * 10 + d;
+            ++nd;
+        } else if (d == static_cast<uint32_t>('.' - '0') && dot == 0xFFFFFFFFu) {
+            dot = nd;
+        } else {
+            return false;
+        }
+    }
+    uint64_t w = w32;
+    for (; i < n; ++i) {
+        const uint32_t d = static_cast<uint32_t>(s[i]) - '0';
+        if (d < 10) {
+            w = w * 10 + d;
+            ++nd;
+        } else if (d == static_cast<uint32_t>('.' - '0') && dot == 0xFFFFFFFFu) {
+            dot = nd;
+        } else {
+            return false;
+        }
+    }
+    if (nd == 0 || nd > 19 || w > (1ull << 53)) return false;
+    const uint32_t fd = dot == 0xFFFFFFFFu ? 0u : nd - dot;
+    const double m = static_cast<double>(w);
+    const double r = fd ? __ddiv_rn(m, kPow10[fd]) : m;
+    v = neg ? -r : r;
+    return true;
+}
+
+struct LineOut {
+    int64_t ts;
+    double lat, lon, speed, heading;
+    uint32_t id_rel, id_len;  // tile-relative id span
+};
+
+constexpr uint8_t kNeedGeneral = 255;
+
+// Fast path of parse_record_impl for a line entirely staged in shared memory whose required
+// fields are all plain: returns kAccepted or kRangeViolation, or kNeedGeneral whenever the
+// general restatement (parse_line) has to decide (trim characters, empty/missing fields, bad
+// timestamps, non-Clinger numbers, required columns beyond the 8th field).
+__device__ __forceinline__ uint8_t fast_parse(const uint8_t* __restrict__ tile,
+                                              const uint32_t* __restrict__ cm, uint32_t p,
+                                              uint32_t e, const ColumnMap& map, LineOut& o) {
+    // positions of the first 8 commas (e when absent)
+    uint32_t c[8];
+    {
+        uint32_t w = p >> 5;
+        uint32_t m = cm[w] & (0xFFFFFFFFu << (p & 31));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            while (m == 0 && ((w + 1) << 5) < e) m = cm[++w];
+            uint32_t x = e;
+            if (m) {
+                const uint32_t pos = (w << 5) + (__ffs(m) - 1);
+                m &= m - 1;
+                if (pos < e) x = pos;
+            }
+            c[k] = x;
+        }
+    }
+    auto fbeg = [&](int32_t f) -> uint32_t {
+        uint32_t b = p;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (f == k + 1) b = c[k] + 1;
+        return b;
+    };
+    auto fend = [&](int32_t f) -> uint32_t {
+        uint32_t x = e;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (f == k) x = c[k];
+        return x;
+    };
+    const int32_t cols[6] = {map.journey_id, map.timestamp, map.latitude,
+                             map.longitude, map.speed,     map.heading};
+    uint32_t fb[6], fe[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        if (cols[k] > 7) return kNeedGeneral;
+        fb[k] = fbeg(cols[k]);
+        fe[k] = fend(cols[k]);
+        // a field that runs into the end of the line without its comma does not exist
+        if (fb[k] > e) return kNeedGeneral;
+        if (fe[k] <= fb[k]) return kNeedGeneral;  // empty (MissingField) -> general decides
+    }
+    // id must not need trimming; numbers/timestamp reject trim characters themselves
+    if (is_trim(tile[fb[0]]) || is_trim(tile[fe[0] - 1])) return kNeedGeneral;
+    if (fe[1] - fb[1] != 19 || !parse_timestamp(tile + fb[1], 19, o.ts)) return kNeedGeneral;
+    if (!fast_number(tile + fb[2], fe[2] - fb[2], o.lat) ||
+        !fast_number(tile + fb[3], fe[3] - fb[3], o.lon) ||
+        !fast_number(tile + fb[4], fe[4] - fb[4], o.speed) ||
+        !fast_number(tile + fb[5], fe[5] - fb[5], o.heading))
+        return kNeedGeneral;
+    if (o.heading == 360.0) o.heading = 0.0;
+    o.id_rel = fb[0];
+    o.id_len = fe[0] - fb[0];
+    if (!(o.lat >= -90.0 && o.lat <= 90.0) || !(o.lon >= -180.0 && o.lon <= 180.0) ||
+        !(o.speed >= 0.0) || !(o.heading >= 0.0 && o.heading < 360.0))
+        return kRangeViolation;  // fast numbers are always finite
+    return kAccepted;
 }
 
 }  // namespace
@@ -82,23 +229,34 @@ void launch_parse_headers(const uint8_t* csv, const uint64_t* shard_off, uint32_
 // ---------------------------------------------------------------------------------------------
 // K1
 constexpr int kStage = kPre + kTile + kHalo;
-constexpr int kNlWords = (kTile + kHalo) / 32;
+constexpr int kWords = (kTile + kHalo) / 32;
 constexpr int kMaxShardsInTile = 32;
 
-__global__ void __launch_bounds__(kDecodeThreads) decode_kernel(DecodeParams P) {
-    __shared__ __align__(16) uint8_t buf[kStage];
-    __shared__ uint32_t nl[kNlWords];
-    __shared__ uint16_t starts[kLineCap];
-    __shared__ Staged stage[kMaxAccPerTile];
+__global__ void __launch_bounds__(kDecodeThreads, 4) decode_kernel(DecodeParams P) {
+    __shared__ __align__(128) uint8_t buf[kStage];
+    __shared__ uint32_t nl[kWords];
+    __shared__ uint32_t cm[kWords];
+    __shared__ uint32_t starts[kLineCap];  // p_rel | shard_delta << 16
     __shared__ uint32_t scan_smem[kDecodeThreads / 32 + 1];
-    __shared__ uint64_t sh_off[kMaxShardsInTile + 2];  // shard starts (sh_first .. ) in tile
-    __shared__ uint32_t sh_first, sh_count, sh_overflow;
-    __shared__ uint32_t s_tile;
-    __shared__ unsigned long long s_base_acc, s_base_head;
-    __shared__ uint8_t head_flag[kMaxAccPerTile];
-
+    __shared__ uint64_t sh_off[kMaxShardsInTile + 2];
+    __shared__ uint32_t sh_first, sh_count, sh_overflow, s_tile;
+    __shared__ unsigned long long s_base;
+    __shared__ __align__(8) uint64_t bar;
+    // parsed lines of the current pass (staged until the slot base is known)
+    __shared__ long long st_ts[kLineCap];
+    __shared__ double st_speed[kLineCap];
+    __shared__ uint32_t st_code[kLineCap];
+    __shared__ uint32_t st_id[kLineCap];   // tile-relative id start
+    __shared__ uint32_t st_len[kLineCap];  // id length | accepted << 31
+    __shared__ long long c_ts;
+    __shared__ uint32_t c_id, c_len, c_code;
+    __shared__ uint32_t s_cnt[8];  // rejects[4], heads, transitions, accepted
+    __shared__ uint64_t s_lb[kDecodeThreads / 32 + 2];
     const int tid = threadIdx.x;
-    if (tid == 0) s_tile = atomicAdd(P.tile_counter, 1u);
+    if (tid == 0) {
+        s_tile = atomicAdd(P.tile_counter, 1u);
+        mbar_init(&bar, 1);
+    }
     __syncthreads();
     const uint32_t tile = s_tile;
     if (tile >= P.tile_end) return;
@@ -106,35 +264,16 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_kernel(DecodeParams P) 
     const uint64_t tb = static_cast<uint64_t>(tile) * kTile;
     const uint64_t te = min(tb + kTile, P.total_end);
     const uint32_t tlen = static_cast<uint32_t>(te - tb);
-    // staged bytes: [tb - kPre, tb + kTile + kHalo) clipped to [0, avail_end)
     const uint64_t stage_end = min(tb + kTile + kHalo, P.avail_end);
     const uint32_t staged_len = static_cast<uint32_t>(stage_end - tb);  // valid bytes from tb
+    const uint8_t* tile_s = buf + kPre;
 
-    // ---- stage bytes -------------------------------------------------------------------------
-    if (P.aligned16) {
-        const uint4* src = reinterpret_cast<const uint4*>(P.csv);
-        uint4* dst = reinterpret_cast<uint4*>(buf);
-        const int64_t base_vec = static_cast<int64_t>(tb / 16) - 1;  // kPre == 16
-        for (int v = tid; v < kStage / 16; v += kDecodeThreads) {
-            const int64_t gv = base_vec + v;
-            const int64_t gb = gv * 16;
-            uint4 val;
-            if (gb >= 0 && static_cast<uint64_t>(gb + 16) <= stage_end) {
-                val = __ldg(src + gv);
-            } else {
-                union {
-                    uint4 v;
-                    uint8_t b[16];
-                } tmp;
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const int64_t a = gb + k;
-                    tmp.b[k] = a < 0 ? uint8_t('\n')
-                                     : (static_cast<uint64_t>(a) < stage_end ? P.csv[a] : uint8_t(0));
-                }
-                val = tmp.v;
-            }
-            dst[v] = val;
+    // ---- 1. stage bytes --------------------------------------------------------------------
+    const bool use_tma = P.aligned16 && tb >= kPre && tb + kTile + kHalo <= P.avail_end;
+    if (use_tma) {
+        if (tid == 0) {
+            mbar_expect_tx(&bar, kStage);
+            tma_load_1d(buf, P.csv + tb - kPre, kStage, &bar);
         }
     } else {
         for (int v = tid; v < kStage; v += kDecodeThreads) {
@@ -143,35 +282,49 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_kernel(DecodeParams P) 
                            : (static_cast<uint64_t>(a) < stage_end ? P.csv[a] : uint8_t(0));
         }
     }
-    if (tid == 0) {
-        // shard containing tb: last s with shard_off[s] <= tb
-        uint32_t lo = 0, hi = P.n_shards;  // answer in [0, n_shards-1]
+    if (tid == 32) {  // shard containing tb (overlaps the copy)
+        uint32_t lo = 0, hi = P.n_shards;
         while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) / 2;
             if (P.shard_off[mid] <= tb) lo = mid;
             else hi = mid;
         }
         sh_first = lo;
-        uint32_t c = 0;
-        uint32_t s = lo + 1;
-        while (s <= P.n_shards && P.shard_off[s] < te && c < kMaxShardsInTile) {
-            sh_off[c++] = P.shard_off[s];
-            ++s;
-        }
+        uint32_t c = 0, s = lo + 1;
+        while (s <= P.n_shards && P.shard_off[s] < te && c < kMaxShardsInTile) sh_off[c++] = P.shard_off[s++];
         sh_overflow = (s <= P.n_shards && P.shard_off[s] < te) ? 1u : 0u;
         sh_count = c;
     }
+    if (use_tma) mbar_wait(&bar, 0);
     __syncthreads();
 
-    // ---- newline bitmap over [tb, tb + kTile + kHalo) ------------------------------------------
-    for (int w = tid; w < kNlWords; w += kDecodeThreads) {
-        const uint4* p = reinterpret_cast<const uint4*>(buf + kPre + 32 * w);
-        nl[w] = nl_mask16(p[0]) | (nl_mask16(p[1]) << 16);
+    // ---- 2. '\n' and ',' bitmaps over [tb, tb + kTile + kHalo) ---------------------------------
+    for (int w = tid; w < kWords; w += kDecodeThreads) {
+        const uint4* p = reinterpret_cast<const uint4*>(tile_s + 32 * w);
+        const uint4 a = p[0], b = p[1];
+        nl[w] = eq_mask16(a, 0x0A0A0A0Au) | (eq_mask16(b, 0x0A0A0A0Au) << 16);
+        cm[w] = eq_mask16(a, 0x2C2C2C2Cu) | (eq_mask16(b, 0x2C2C2C2Cu) << 16);
     }
     __syncthreads();
 
-    // ---- line starts in [0, tlen): positions after a '\n' --------------------------------------
-    // each thread owns words 2*tid, 2*tid+1 of the tile (kTile/32 = 512 words, 256 threads)
+    auto shard_of = [&](uint64_t p) -> uint32_t {
+        if (!sh_overflow) {
+            uint32_t s = sh_first;
+            for (uint32_t k = 0; k < sh_count; ++k)
+                if (sh_off[k] <= p) s = sh_first + 1 + k;
+            return s;
+        }
+        uint32_t lo = 0, hi = P.n_shards;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (P.shard_off[mid] <= p) lo = mid;
+            else hi = mid;
+        }
+        return lo;
+    };
+
+    // ---- 3. data lines starting in [0, tlen) ----------------------------------------------------
+    // thread t owns tile words 2t, 2t+1 (kTile / 32 = 512 words)
     uint32_t smask[2];
     uint32_t my_count = 0;
 #pragma unroll
@@ -182,19 +335,44 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_kernel(DecodeParams P) 
         const int lo = 32 * w;
         if (lo >= static_cast<int>(tlen)) m = 0;
         else if (lo + 32 > static_cast<int>(tlen)) m &= (1u << (tlen - lo)) - 1u;
-        smask[k] = m;
-        my_count += __popc(m);
+        // keep only data lines: not a shard start (header), good shard, non-empty
+        uint32_t keep = m;
+        while (m) {
+            const int bit = __ffs(m) - 1;
+            m &= m - 1;
+            const uint32_t pr = static_cast<uint32_t>(lo + bit);
+            const uint64_t p = tb + pr;
+            const uint32_t s = shard_of(p);
+            const uint64_t s_end = P.shard_off[s + 1];
+            bool data = p != P.shard_off[s] && P.shard_good[s];
+            if (data) {
+                const uint8_t c0 = tile_s[pr];
+                if (c0 == '\n') data = false;
+                else if (c0 == '\r' && (p + 1 == s_end || tile_s[pr + 1] == '\n')) data = false;
+            }
+            if (!data) keep &= ~(1u << bit);
+        }
+        smask[k] = keep;
+        my_count += __popc(keep);
     }
-    uint32_t total_starts;
-    const uint32_t my_off = block_exclusive_scan<kDecodeThreads>(my_count, scan_smem, total_starts);
+    uint32_t n_data;
+    const uint32_t my_off = block_exclusive_scan<kDecodeThreads>(my_count, scan_smem, n_data);
 
-    // per-thread stats
-    uint32_t c_rows = 0, c_rej[4] = {0, 0, 0, 0}, c_trans = 0;
+    // ---- publish the tile's line count now; resolve the slot base after parsing ------------------
+    if (tid == 0) lookback1_publish(P.lb, tile, n_data);
+    if (tid < 8) s_cnt[tid] = 0;
+    if (tid == 0) {
+        c_len = 0;  // "no previous data line" for the first line of the tile
+        c_ts = 0;
+        c_id = 0;
+        c_code = kCodeRejected;
+    }
+    uint64_t base = 0;
+    bool resolved = false;
     long long ts_min = LLONG_MAX, ts_max = LLONG_MIN;
-    uint32_t n_acc = 0;  // uniform across the block
+    uint32_t c_acc = 0;
 
-    for (uint32_t pass_base = 0; pass_base < total_starts; pass_base += kLineCap) {
-        // scatter this pass's starts
+    for (uint32_t pass_base = 0; pass_base < n_data; pass_base += kLineCap) {
         {
             uint32_t idx = my_off;
 #pragma unroll
@@ -204,195 +382,150 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_kernel(DecodeParams P) 
                     const int bit = __ffs(m) - 1;
                     m &= m - 1;
                     if (idx >= pass_base && idx < pass_base + kLineCap)
-                        starts[idx - pass_base] = static_cast<uint16_t>(32 * (2 * tid + k) + bit);
+                        starts[idx - pass_base] = static_cast<uint32_t>(32 * (2 * tid + k) + bit);
                     ++idx;
                 }
             }
         }
         __syncthreads();
-        const uint32_t n_pass = min(static_cast<uint32_t>(kLineCap), total_starts - pass_base);
-        for (uint32_t r0 = 0; r0 < n_pass; r0 += kDecodeThreads) {
-            const uint32_t li = r0 + tid;
-            uint32_t accepted = 0;
-            Staged rec;
-            if (li < n_pass) {
-                const uint32_t p_rel = starts[li];
-                const uint64_t p = tb + p_rel;
-                // shard of p
-                uint32_t s;
-                if (!sh_overflow) {
-                    s = sh_first;
-                    for (uint32_t k = 0; k < sh_count; ++k)
-                        if (sh_off[k] <= p) s = sh_first + 1 + k;
-                } else {
-                    uint32_t lo = 0, hi = P.n_shards;
-                    while (hi - lo > 1) {
-                        const uint32_t mid = (lo + hi) / 2;
-                        if (P.shard_off[mid] <= p) lo = mid;
-                        else hi = mid;
-                    }
-                    s = lo;
-                }
-                const uint64_t s_begin = P.shard_off[s];
-                const uint64_t s_end = P.shard_off[s + 1];
-                if (p != s_begin && P.shard_good[s]) {
-                    // line end: next '\n' at or after p
-                    uint64_t e = 0;
-                    bool found = false;
-                    {
-                        uint32_t w = p_rel >> 5;
-                        uint32_t m = nl[w] & (0xFFFFFFFFu << (p_rel & 31));
-                        while (true) {
-                            if (m) {
-                                const uint32_t x = 32 * w + (__ffs(m) - 1);
-                                if (x < staged_len) {
-                                    e = tb + x;
-                                    found = true;
-                                }
-                                break;
-                            }
-                            if (++w >= static_cast<uint32_t>(kNlWords)) break;
-                            if (32 * w >= staged_len) break;
-                            m = nl[w];
+        const uint32_t n_pass = min(static_cast<uint32_t>(kLineCap), n_data - pass_base);
+        // ---- 4. parse: one data line per thread, results staged in shared memory -----------------
+        for (uint32_t li = tid; li < n_pass; li += kDecodeThreads) {
+            uint8_t why;
+            LineOut o;
+            o.ts = 0;
+            o.speed = 0.0;
+            o.id_rel = 0;
+            o.id_len = 0;
+            uint32_t code = kCodeRejected;
+            const uint32_t p_rel = starts[li];
+            const uint64_t p = tb + p_rel;
+            const uint32_t s = shard_of(p);
+            const uint64_t s_end = P.shard_off[s + 1];
+            // line end: next '\n' at or after p, clamped to the shard end
+            uint64_t e = 0;
+            bool found = false;
+            {
+                uint32_t w = p_rel >> 5;
+                uint32_t m = nl[w] & (0xFFFFFFFFu << (p_rel & 31));
+                while (true) {
+                    if (m) {
+                        const uint32_t x = 32 * w + (__ffs(m) - 1);
+                        if (x < staged_len) {
+                            e = tb + x;
+                            found = true;
                         }
+                        break;
                     }
-                    if (!found) {
-                        uint64_t x = tb + min(staged_len, static_cast<uint32_t>(kTile + kHalo));
-                        if (x < p) x = p;
-                        while (x < P.avail_end && x < s_end && P.csv[x] != '\n') ++x;
-                        e = x;
-                    }
-                    if (e > s_end) e = s_end;
-                    const bool in_smem = e <= stage_end;
-                    const uint8_t* line = in_smem ? (buf + kPre + p_rel) : (P.csv + p);
-                    int32_t len = static_cast<int32_t>(e - p);
-                    if (len > 0 && line[len - 1] == '\r') --len;
-                    if (len > 0) {
-                        ++c_rows;
-                        Parsed pr;
-                        const uint8_t why = parse_line(line, len, P.cmap[s], pr);
-                        if (why == kAccepted) {
-                            accepted = 1;
-                            rec.ts = pr.epoch;
-                            rec.speed = pr.speed;
-                            rec.code = cell_code(pr.epoch, pr.lat, pr.lon, pr.speed, pr.heading,
-                                                 P.grid);
-                            rec.line_rel = p_rel;
-                            rec.id_rel = p_rel + static_cast<uint32_t>(pr.id_begin);
-                            rec.id_len = static_cast<uint32_t>(pr.id_len);
-                            ts_min = min(ts_min, static_cast<long long>(pr.epoch));
-                            ts_max = max(ts_max, static_cast<long long>(pr.epoch));
-                        } else {
-                            ++c_rej[why - 1];
-                        }
-                    }
+                    if (++w >= static_cast<uint32_t>(kWords) || 32 * w >= staged_len) break;
+                    m = nl[w];
                 }
             }
-            uint32_t n_round;
-            const uint32_t pos = block_exclusive_scan<kDecodeThreads>(accepted, scan_smem, n_round);
-            if (accepted && n_acc + pos < static_cast<uint32_t>(kMaxAccPerTile))
-                stage[n_acc + pos] = rec;
-            n_acc += n_round;
+            if (!found) {
+                uint64_t x = tb + staged_len;
+                while (x < P.avail_end && x < s_end && P.csv[x] != '\n') ++x;
+                e = x;
+            }
+            if (e > s_end) e = s_end;
+            const bool in_smem = e <= stage_end;
+            const uint8_t* gline = P.csv + p;
+            uint32_t len = static_cast<uint32_t>(e - p);
+            const uint8_t last = in_smem ? tile_s[p_rel + len - 1] : gline[len - 1];
+            if (last == '\r') --len;  // len > 0: empty lines are not data lines
+            const ColumnMap map = P.cmap[s];
+            why = kNeedGeneral;
+            if (in_smem) why = fast_parse(tile_s, cm, p_rel, p_rel + len, map, o);
+            if (why == kNeedGeneral) {
+                const uint8_t* line = in_smem ? tile_s + p_rel : gline;
+                Parsed pr;
+                why = parse_line(line, static_cast<int32_t>(len), map, pr);
+                if (why == kAccepted) {
+                    o.ts = pr.epoch;
+                    o.lat = pr.lat;
+                    o.lon = pr.lon;
+                    o.speed = pr.speed;
+                    o.heading = pr.heading;
+                    o.id_rel = p_rel + static_cast<uint32_t>(pr.id_begin);
+                    o.id_len = static_cast<uint32_t>(pr.id_len);
+                }
+            }
+            if (why == kAccepted) {
+                code = cell_code(o.ts, o.lat, o.lon, o.speed, o.heading, P.grid);
+                ts_min = min(ts_min, static_cast<long long>(o.ts));
+                ts_max = max(ts_max, static_cast<long long>(o.ts));
+                ++c_acc;
+            } else {
+                atomicAdd(&s_cnt[why - 1], 1u);  // rare
+            }
+            st_ts[li] = o.ts;
+            st_speed[li] = o.speed;
+            st_code[li] = code;
+            st_id[li] = o.id_rel;
+            st_len[li] = o.id_len | (why == kAccepted ? 0x80000000u : 0u);
+        }
+        if (!resolved) {
+            // predecessors have had a full parse phase to publish: the walk is short
+            base = lookback1_resolve<kDecodeThreads>(P.lb, tile, n_data, s_lb);
+            resolved = true;
+            if (tid == 0 && base + n_data > P.out.slot_cap)
+                atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[kStOverflow]), 1ull);
+        } else {
+            __syncthreads();
+        }
+        const bool fits = base + n_data <= P.out.slot_cap;
+        // ---- 5. run heads + coalesced writes ------------------------------------------------------
+        uint32_t my_heads = 0, my_trans = 0;
+        for (uint32_t k = tid; k < n_pass; k += kDecodeThreads) {
+            const uint32_t ln = st_len[k];
+            uint32_t code = st_code[k];
+            if (ln >> 31) {
+                const uint32_t pl = k ? st_len[k - 1] : c_len;
+                const long long pts = k ? st_ts[k - 1] : c_ts;
+                const uint32_t idl = ln & 0x7FFFFFFFu;
+                bool head = true;
+                if ((pl >> 31) && (pl & 0x7FFFFFFFu) == idl && pts < st_ts[k]) {
+                    const uint32_t pid = k ? st_id[k - 1] : c_id;
+                    const uint32_t mid = st_id[k];
+                    const uint8_t* pa = (pid + idl <= staged_len) ? tile_s + pid : P.csv + tb + pid;
+                    const uint8_t* pb = (mid + idl <= staged_len) ? tile_s + mid : P.csv + tb + mid;
+                    bool same = true;
+                    for (uint32_t i = 0; i < idl; ++i)
+                        if (pa[i] != pb[i]) {
+                            same = false;
+                            break;
+                        }
+                    head = !same;
+                }
+                if (head) {
+                    ++my_heads;
+                    code |= kHeadBit;
+                } else if ((k ? st_code[k - 1] : c_code) != code) {
+                    ++my_trans;
+                }
+            }
+            if (fits) {
+                const uint64_t slot = base + pass_base + k;
+                P.out.ts[slot] = st_ts[k];
+                P.out.speed[slot] = st_speed[k];
+                P.out.code[slot] = code;
+                P.out.loff[slot] = tb + starts[k];
+            }
+        }
+        if (my_heads) atomicAdd(&s_cnt[4], my_heads);
+        if (my_trans) atomicAdd(&s_cnt[5], my_trans);
+        __syncthreads();
+        if (tid == 0) {  // carry the pass's last line
+            c_ts = st_ts[n_pass - 1];
+            c_id = st_id[n_pass - 1];
+            c_len = st_len[n_pass - 1];
+            c_code = st_code[n_pass - 1];
         }
         __syncthreads();
     }
-    if (n_acc > static_cast<uint32_t>(kMaxAccPerTile)) {
-        // impossible by the 30-byte bound; keep the invariant loud rather than corrupt memory
-        if (tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[kStOverflow]), 1ull);
-        n_acc = kMaxAccPerTile;
-    }
-    __syncthreads();
+    if (!resolved) lookback1_resolve<kDecodeThreads>(P.lb, tile, n_data, s_lb);
 
-    // ---- run heads --------------------------------------------------------------------------
-    uint32_t my_heads = 0;
-    for (uint32_t k = tid; k < n_acc; k += kDecodeThreads) {
-        uint8_t head = 1;
-        if (k > 0) {
-            const Staged& a = stage[k - 1];
-            const Staged& b = stage[k];
-            if (b.ts > a.ts && a.id_len == b.id_len) {
-                const uint8_t* pa = (a.id_rel + a.id_len <= staged_len) ? buf + kPre + a.id_rel
-                                                                         : P.csv + tb + a.id_rel;
-                const uint8_t* pb = (b.id_rel + b.id_len <= staged_len) ? buf + kPre + b.id_rel
-                                                                         : P.csv + tb + b.id_rel;
-                bool same = true;
-                for (uint32_t i = 0; i < a.id_len; ++i)
-                    if (pa[i] != pb[i]) {
-                        same = false;
-                        break;
-                    }
-                head = same ? 0 : 1;
-            }
-            if (!head && a.code != b.code) ++c_trans;
-        }
-        head_flag[k] = head;
-        my_heads += head;
-    }
-    uint32_t n_heads;
-    block_exclusive_scan<kDecodeThreads>(my_heads, scan_smem, n_heads);
-
-    // ---- look-back -----------------------------------------------------------------------------
-    if (tid < 32) {
-        uint64_t ea, eb;
-        lookback_publish_and_scan(P.lb, tile, n_acc, n_heads, ea, eb);
-        if (tid == 0) {
-            s_base_acc = ea;
-            s_base_head = eb;
-        }
-    }
-    __syncthreads();
-    const uint64_t base_acc = s_base_acc, base_head = s_base_head;
-    const bool fits = base_acc + n_acc <= P.out.slot_cap && base_head + n_heads <= P.out.head_cap;
-    if (!fits && tid == 0)
-        atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[kStOverflow]), 1ull);
-
-    // ---- write records + heads (line order) ----------------------------------------------------
-    uint32_t head_done = 0;
-    for (uint32_t r0 = 0; r0 < n_acc; r0 += kDecodeThreads) {
-        const uint32_t k = r0 + tid;
-        const uint32_t h = (k < n_acc) ? head_flag[k] : 0u;
-        uint32_t n_round;
-        const uint32_t hpos = block_exclusive_scan<kDecodeThreads>(h, scan_smem, n_round);
-        if (k < n_acc && fits) {
-            const Staged& s = stage[k];
-            const uint64_t slot = base_acc + k;
-            P.out.ts[slot] = s.ts;
-            P.out.speed[slot] = s.speed;
-            P.out.code[slot] = s.code;
-            P.out.loff[slot] = tb + s.line_rel;
-            if (h) {
-                const uint64_t hi = base_head + head_done + hpos;
-                const uint8_t* pid = (s.id_rel + s.id_len <= staged_len) ? buf + kPre + s.id_rel
-                                                                         : P.csv + tb + s.id_rel;
-                uint64_t k0 = 0, k1 = 0;
-                const uint32_t n = s.id_len;
-                for (uint32_t i = 0; i < 8; ++i) k0 = (k0 << 8) | (i < n ? pid[i] : 0u);
-                for (uint32_t i = 8; i < 15; ++i) k1 = (k1 << 8) | (i < n ? pid[i] : 0u);
-                k1 = (k1 << 8) | (n <= 15 ? n : 0xFFu);
-                P.out.hslot[hi] = static_cast<uint32_t>(slot);
-                P.out.hk0[hi] = k0;
-                P.out.hk1[hi] = k1;
-                P.out.hidref[hi] = ((tb + s.id_rel) << 24) | (n < 0xFFFFFFu ? n : 0xFFFFFFu);
-                P.out.hhash[hi] = fnv1a(pid, n);
-            }
-        }
-        head_done += n_round;
-    }
-
-    // ---- stats ---------------------------------------------------------------------------------
-    unsigned long long v[6] = {c_rows, c_rej[0], c_rej[1], c_rej[2], c_rej[3], c_trans};
-#pragma unroll
-    for (int i = 0; i < 6; ++i) {
-        const unsigned long long sum = warp_sum(v[i]);
-        if ((tid & 31) == 0 && sum) {
-            const int idx = (i == 0) ? kStRowsRead : (i == 5 ? kStGTransitions : kStRejBase + i - 1);
-            atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[idx]), sum);
-        }
-    }
-    if (tid == 0)
-        atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[kStParsed]),
-                  static_cast<unsigned long long>(n_acc));
-    // ts min/max (warp reduce then atomics)
+    // ---- stats -----------------------------------------------------------------------------------
+    if (c_acc) atomicAdd(&s_cnt[6], c_acc);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         ts_min = min(ts_min, __shfl_xor_sync(0xFFFFFFFFu, ts_min, o));
@@ -401,6 +534,16 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_kernel(DecodeParams P) 
     if ((tid & 31) == 0 && ts_min <= ts_max) {
         atomicMin(&P.ts_minmax[0], ts_min);
         atomicMax(&P.ts_minmax[1], ts_max);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long* st = reinterpret_cast<unsigned long long*>(P.stats);
+        if (n_data) atomicAdd(&st[kStRowsRead], static_cast<unsigned long long>(n_data));
+        for (int i = 0; i < 4; ++i)
+            if (s_cnt[i]) atomicAdd(&st[kStRejBase + i], static_cast<unsigned long long>(s_cnt[i]));
+        if (s_cnt[4]) atomicAdd(&st[kStHeads], static_cast<unsigned long long>(s_cnt[4]));
+        if (s_cnt[5]) atomicAdd(&st[kStGTransitions], static_cast<unsigned long long>(s_cnt[5]));
+        if (s_cnt[6]) atomicAdd(&st[kStParsed], static_cast<unsigned long long>(s_cnt[6]));
     }
 }
 

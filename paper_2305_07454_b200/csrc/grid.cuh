@@ -13,13 +13,15 @@
 
 namespace cvlg {
 
-// Per-record cell code. Values >= kCodeFirstSpecial are not cells.
+// Per-record cell code (31 bits; bit 31 of the slot word is the run-head flag).
+// Values >= kCodeFirstSpecial are not cells, so grids must have < 2^31 - 16 cells.
 enum : uint32_t {
-    kCodeOutOfGrid = 0xFFFFFFFFu,     // filtered: OutOfGrid
-    kCodeSpeedCeiling = 0xFFFFFFFEu,  // filtered: SpeedCeiling
-    kCodeMissingField = 0xFFFFFFFDu,  // filtered: MissingField (empty id; unreachable after parse)
-    kCodeUnbinnable = 0xFFFFFFFCu,    // require_in_grid=false and off-grid: OutOfBounds if kept
-    kCodeFirstSpecial = 0xFFFFFFFCu,
+    kCodeOutOfGrid = 0x7FFFFFFFu,     // filtered: OutOfGrid
+    kCodeSpeedCeiling = 0x7FFFFFFEu,  // filtered: SpeedCeiling
+    kCodeMissingField = 0x7FFFFFFDu,  // filtered: MissingField (empty id; unreachable after parse)
+    kCodeUnbinnable = 0x7FFFFFFCu,    // require_in_grid=false and off-grid: OutOfBounds if kept
+    kCodeRejected = 0x7FFFFFFBu,      // data line rejected by parse (counted in decode)
+    kCodeFirstSpecial = 0x7FFFFFF0u,
 };
 
 struct GridParams {

@@ -14,10 +14,11 @@ constexpr int kTile = 16384;  // CSV bytes per decode tile
 constexpr int kHalo = 1024;   // bytes staged past the tile end (lines finishing in the next tile)
 constexpr int kPre = 16;      // bytes staged before the tile (previous-byte '\n' test)
 constexpr int kDecodeThreads = 256;
-// An accepted line holds >= 6 non-empty fields (id, 19-byte timestamp, 4 numbers), 5 commas and
-// a terminator: >= 30 bytes. So a tile starts at most kTile/30 + 1 accepted records.
-constexpr int kMaxAccPerTile = kTile / 30 + 2;
-constexpr int kLineCap = 1024;  // line starts handled per pass over a tile
+constexpr int kLineCap = 512;  // data lines handled per pass over a tile
+
+// Slot word (one per data line): bits 0..30 = cell code (grid.cuh kCode*), bit 31 = run head.
+constexpr uint32_t kHeadBit = 0x80000000u;
+constexpr uint32_t kCodeMask = 0x7FFFFFFFu;
 
 // Stats counters in device memory (u64 each).
 enum : int {
@@ -31,23 +32,21 @@ enum : int {
     kStFiltOutOfGrid = 10,
     kStFiltSpeed = 11,
     kStFiltMissing = 12,
-    kStGTransitions = 13,  // (run, cell) changes seen in decode: bound on (cell, journey) pairs
+    kStGTransitions = 13,  // cell changes inside runs seen in decode: bound on (cell, journey) pairs
     kStUnbinnable = 14,    // kept records that would throw OutOfBounds
     kStOverflow = 15,      // capacity overflow (hash tables / slot arrays)
-    kStCount = 16,
+    kStHeads = 16,
+    kStCount = 17,
 };
 
+// Per data line ("slot", in provenance order). Rejected lines keep their slot with
+// code kCodeRejected so that slot assignment never waits for parsing.
 struct DecodeOut {
     int64_t* ts;      // [slot] epoch seconds
     double* speed;    // [slot]
-    uint32_t* code;   // [slot] cell code (g or kCode*)
+    uint32_t* code;   // [slot] cell code | kHeadBit
     uint64_t* loff;   // [slot] absolute line offset in the CSV buffer
-    uint32_t* hslot;  // [head] first slot of the run
-    uint64_t* hk0;    // [head] inline journey key, bytes 0..7 big-endian
-    uint64_t* hk1;    // [head] bytes 8..14 big-endian << 8 | (len <= 15 ? len : 0xFF)
-    uint64_t* hidref; // [head] (absolute id offset << 24) | min(len, 2^24-1)
-    uint64_t* hhash;  // [head] FNV-1a 64 of the id (ingest.cpp:287-291)
-    uint64_t slot_cap, head_cap;
+    uint64_t slot_cap;
 };
 
 struct DecodeParams {
@@ -60,7 +59,7 @@ struct DecodeParams {
     uint32_t n_shards;
     uint32_t tile_end;
     uint32_t* tile_counter;
-    LookbackState lb;
+    Lookback1 lb;
     GridParams grid;
     DecodeOut out;
     uint64_t* stats;

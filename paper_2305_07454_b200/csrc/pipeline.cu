@@ -197,10 +197,10 @@ struct cvlg_context {
     cudaStream_t stream = nullptr, copy_stream = nullptr;
     bool own_stream = true;
     DevBuf csv, shard_off, cmap, good, lb_flag, lb_val, counter, stats, tsmm;
-    DevBuf ts, speed, code, loff, hslot, hk0, hk1, hidref, hhash;
+    DevBuf ts, speed, code, loff, hslot;
     DevBuf dict, hdict, flags, pos, uslot, rank_of_slot, hrank, scal;
     DevBuf keys, vals, keys_alt, vals_alt, sort_tmp, scan_tmp, srank, jstart;
-    DevBuf pair_key, pair_sum, pair_cnt;
+    DevBuf pair_key, pair_sum, pair_cnt, spill_key, spill_sum, spill_cnt;
     DevBuf planes, raw;
     HostPinned h_small, h_csv;
     std::vector<cudaEvent_t> chunk_events;
@@ -237,13 +237,13 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
 
     c->h_small.ensure(4096);
     uint64_t* hs = h_small64(c);
+    uint64_t* d_stats = nullptr;
 
     CK(cudaEventRecord(c->ev[0], s));
     // ---- setup -----------------------------------------------------------------------------
     c->stats.ensure(kStCount * 8);
     c->tsmm.ensure(16);
-    init_run_kernel<<<1, 32, 0, s>>>(c->stats.as<uint64_t>(), c->tsmm.as<long long>());
-    count_launch();
+    d_stats = c->stats.as<uint64_t>();
     c->shard_off.ensure((n_shards + 1) * 8);
     CK(cudaMemcpyAsync(c->shard_off.p, shard_off.data(), (n_shards + 1) * 8, cudaMemcpyHostToDevice, s));
     c->cmap.ensure(std::max<uint32_t>(n_shards, 1) * sizeof(ColumnMap));
@@ -251,32 +251,12 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
     if (h_cmap) {
         CK(cudaMemcpyAsync(c->cmap.p, h_cmap, n_shards * sizeof(ColumnMap), cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(c->good.p, h_good, n_shards, cudaMemcpyHostToDevice, s));
-        if (bad_headers) {
-            hs[0] = bad_headers;
-            CK(cudaMemcpyAsync(c->stats.as<uint64_t>() + kStBadHeader, hs, 8, cudaMemcpyHostToDevice, s));
-        }
-    } else {
-        launch_parse_headers(d_csv, c->shard_off.as<uint64_t>(), n_shards, c->cmap.as<ColumnMap>(),
-                             c->good.as<uint8_t>(), c->stats.as<uint64_t>(), s);
-        count_launch();
     }
-    const uint64_t slot_cap = total / 30 + n_shards + 2;
-    c->ts.ensure(slot_cap * 8);
-    c->speed.ensure(slot_cap * 8);
-    c->code.ensure(slot_cap * 4);
-    c->loff.ensure(slot_cap * 8);
-    c->hslot.ensure(slot_cap * 4);
-    c->hk0.ensure(slot_cap * 8);
-    c->hk1.ensure(slot_cap * 8);
-    c->hidref.ensure(slot_cap * 8);
-    c->hhash.ensure(slot_cap * 8);
     c->lb_flag.ensure(std::max<uint64_t>(n_tiles, 1) * 4);
     c->lb_val.ensure(std::max<uint64_t>(n_tiles, 1) * 32);
     c->counter.ensure(4);
-    CK(cudaMemsetAsync(c->lb_flag.p, 0, std::max<uint64_t>(n_tiles, 1) * 4, s));
-    CK(cudaMemsetAsync(c->counter.p, 0, 4, s));
 
-    // ---- K1 decode ---------------------------------------------------------------------------
+    // ---- K1 decode (slot per data line) ----------------------------------------------------------
     DecodeParams P;
     P.csv = d_csv;
     P.total_end = total;
@@ -289,52 +269,76 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
     P.lb.agg = c->lb_val.as<uint64_t>();
     P.lb.inc = c->lb_val.as<uint64_t>() + 2 * std::max<uint64_t>(n_tiles, 1);
     P.grid = gp;
-    P.out.ts = c->ts.as<int64_t>();
-    P.out.speed = c->speed.as<double>();
-    P.out.code = c->code.as<uint32_t>();
-    P.out.loff = c->loff.as<uint64_t>();
-    P.out.hslot = c->hslot.as<uint32_t>();
-    P.out.hk0 = c->hk0.as<uint64_t>();
-    P.out.hk1 = c->hk1.as<uint64_t>();
-    P.out.hidref = c->hidref.as<uint64_t>();
-    P.out.hhash = c->hhash.as<uint64_t>();
-    P.out.slot_cap = slot_cap;
-    P.out.head_cap = slot_cap;
-    P.stats = c->stats.as<uint64_t>();
+    P.stats = d_stats;
     P.ts_minmax = c->tsmm.as<long long>();
     P.aligned16 = (reinterpret_cast<uintptr_t>(d_csv) % 16) == 0;
-    CK(cudaEventRecord(c->ev_dec0, s));
-    uint64_t tiles_done = 0;
-    for (size_t m = 0; m < marks.size(); ++m) {
-        const bool last = m + 1 == marks.size();
-        const uint64_t t_hi = last ? n_tiles : std::min<uint64_t>(marks[m].safe_end / kTile, n_tiles);
-        if (marks[m].ready) CK(cudaStreamWaitEvent(s, marks[m].ready, 0));
-        if (t_hi > tiles_done) {
-            P.avail_end = marks[m].avail_end;
-            P.tile_end = static_cast<uint32_t>(t_hi);
-            launch_decode(P, static_cast<uint32_t>(t_hi - tiles_done), s);
+    // A data line holds >= 30 bytes when it parses; rejects can be shorter, so the first
+    // attempt may overflow on pathological inputs and is then re-run with the exact count.
+    uint64_t slot_cap = total / 24 + n_shards + 1024;
+    uint64_t N = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        c->ts.ensure(slot_cap * 8);
+        c->speed.ensure(slot_cap * 8);
+        c->code.ensure(slot_cap * 4);
+        c->loff.ensure(slot_cap * 8);
+        P.out.ts = c->ts.as<int64_t>();
+        P.out.speed = c->speed.as<double>();
+        P.out.code = c->code.as<uint32_t>();
+        P.out.loff = c->loff.as<uint64_t>();
+        P.out.slot_cap = slot_cap;
+        init_run_kernel<<<1, 32, 0, s>>>(d_stats, c->tsmm.as<long long>());
+        count_launch();
+        if (h_cmap) {
+            if (bad_headers) {
+                hs[0] = bad_headers;
+                CK(cudaMemcpyAsync(d_stats + kStBadHeader, hs, 8, cudaMemcpyHostToDevice, s));
+            }
+        } else {
+            launch_parse_headers(d_csv, P.shard_off, n_shards, c->cmap.as<ColumnMap>(),
+                                 c->good.as<uint8_t>(), d_stats, s);
             count_launch();
-            tiles_done = t_hi;
         }
+        CK(cudaMemsetAsync(c->lb_flag.p, 0, std::max<uint64_t>(n_tiles, 1) * 4, s));
+        CK(cudaMemsetAsync(c->counter.p, 0, 4, s));
+        CK(cudaEventRecord(c->ev_dec0, s));
+        uint64_t tiles_done = 0;
+        if (attempt == 0) {
+            for (size_t m = 0; m < marks.size(); ++m) {
+                const bool last = m + 1 == marks.size();
+                const uint64_t t_hi =
+                    last ? n_tiles : std::min<uint64_t>(marks[m].safe_end / kTile, n_tiles);
+                if (marks[m].ready) CK(cudaStreamWaitEvent(s, marks[m].ready, 0));
+                if (t_hi > tiles_done) {
+                    P.avail_end = marks[m].avail_end;
+                    P.tile_end = static_cast<uint32_t>(t_hi);
+                    launch_decode(P, static_cast<uint32_t>(t_hi - tiles_done), s);
+                    count_launch();
+                    tiles_done = t_hi;
+                }
+            }
+        } else if (n_tiles) {
+            P.avail_end = total;
+            P.tile_end = static_cast<uint32_t>(n_tiles);
+            launch_decode(P, static_cast<uint32_t>(n_tiles), s);
+            count_launch();
+        }
+        CK(cudaEventRecord(c->ev_dec1, s));
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(hs, d_stats, kStCount * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hs + 32, c->tsmm.p, 16, cudaMemcpyDeviceToHost, s));
+        sync(c);
+        N = hs[kStRowsRead];
+        if (N <= slot_cap) break;
+        slot_cap = N;  // exact count from the look-back totals
     }
-    CK(cudaEventRecord(c->ev_dec1, s));
-    CK(cudaGetLastError());
-
-    // ---- read back sizes ---------------------------------------------------------------------
-    CK(cudaMemcpyAsync(hs, c->stats.p, kStCount * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hs + kStCount, c->tsmm.p, 16, cudaMemcpyDeviceToHost, s));
-    if (n_tiles)
-        CK(cudaMemcpyAsync(hs + kStCount + 2, P.lb.inc + 2 * (n_tiles - 1), 16, cudaMemcpyDeviceToHost, s));
-    sync(c);
     CK(cudaEventRecord(c->ev[1], s));
     if (hs[kStOverflow]) fail(CVLG_E_INTERNAL, "decode capacity invariant violated");
-    const uint64_t N = n_tiles ? hs[kStCount + 2] : 0;
-    const uint64_t H = n_tiles ? hs[kStCount + 3] : 0;
-    const int64_t ts_min = static_cast<int64_t>(hs[kStCount]);
-    const int64_t ts_max = static_cast<int64_t>(hs[kStCount + 1]);
+    const uint64_t n_parsed = hs[kStParsed];
     const uint64_t transitions = hs[kStGTransitions];
-    if (N != hs[kStParsed]) fail(CVLG_E_INTERNAL, "decode count mismatch");
-    if (N >= (1ull << 32) - 1) fail(CVLG_E_UNSUPPORTED, ">= 2^32-1 records on one device");
+    const uint64_t H = hs[kStHeads];
+    const int64_t ts_min = static_cast<int64_t>(hs[32]);
+    const int64_t ts_max = static_cast<int64_t>(hs[33]);
+    if (N >= (1ull << 32) - 1) fail(CVLG_E_UNSUPPORTED, ">= 2^32-1 data lines on one device");
 
     const uint64_t lattice_words = static_cast<uint64_t>(dims.T) * 8 * dims.RC;
     const uint64_t raw_words = static_cast<uint64_t>(dims.T) * 4 * dims.RC;
@@ -343,22 +347,46 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
 
     bool slow = false;
     uint64_t J = 0;
-    if (N > 0) {
-        // ---- journey dictionary ----------------------------------------------------------------
-        const uint64_t dcap = pow2_at_least(2 * H);
-        c->dict.ensure(dcap * 16);
-        c->hdict.ensure(H * 4);
+    if (n_parsed > 0) {
         c->scal.ensure(64);
-        CK(cudaMemsetAsync(c->dict.p, 0xFF, dcap * 16, s));
         CK(cudaMemsetAsync(c->scal.p, 0, 64, s));
         unsigned long long* d_maxlen = c->scal.as<unsigned long long>();
-        launch_dict_insert(P.out, H, d_csv, c->dict.as<unsigned long long>(), dcap - 1,
-                           c->hdict.as<uint32_t>(), c->stats.as<uint64_t>(), d_maxlen, s);
-        c->flags.ensure(std::max<uint64_t>(dcap, N + 1) * 4 + 16);
-        c->pos.ensure(std::max<uint64_t>(dcap, N + 1) * 4 + 16);
-        c->scan_tmp.ensure(scan_temp_words(std::max<uint64_t>(dcap, N + 1)) * 4 + 64);
-        launch_dict_flags(c->dict.as<unsigned long long>(), dcap, c->flags.as<uint32_t>(), s);
         uint32_t* d_total = c->scal.as<uint32_t>() + 4;
+        unsigned long long* d_orand = c->scal.as<unsigned long long>() + 4;
+        unsigned long long* h_orand = reinterpret_cast<unsigned long long*>(hs + 40);
+        uint32_t* d_invalid = c->scal.as<uint32_t>() + 12;
+        const uint64_t dcap = pow2_at_least(2 * H);
+        const uint64_t flag_n = std::max<uint64_t>(dcap, N + 1);
+        c->flags.ensure(flag_n * 4 + 16);
+        c->pos.ensure(flag_n * 4 + 16);
+        c->scan_tmp.ensure(scan_temp_words(flag_n) * 4 + 64);
+
+        // ---- run heads -> compact list -----------------------------------------------------------
+        c->hslot.ensure(H * 4 + 4);
+        launch_head_flags(c->code.as<uint32_t>(), N, c->flags.as<uint32_t>(), s);
+        exclusive_scan_u32(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), N, nullptr,
+                           c->scan_tmp.as<uint32_t>(), s);
+        launch_head_compact(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), N,
+                            c->hslot.as<uint32_t>(), s);
+
+        // ---- journey dictionary ----------------------------------------------------------------
+        c->dict.ensure(dcap * 16);
+        c->hdict.ensure(H * 4);
+        CK(cudaMemsetAsync(c->dict.p, 0xFF, dcap * 16, s));
+        DictParams DP;
+        DP.csv = d_csv;
+        DP.shard_off = P.shard_off;
+        DP.cmap = P.cmap;
+        DP.n_shards = n_shards;
+        DP.hslot = c->hslot.as<uint32_t>();
+        DP.loff = c->loff.as<uint64_t>();
+        DP.n_heads = H;
+        DP.table = c->dict.as<unsigned long long>();
+        DP.mask = dcap - 1;
+        DP.hdict = c->hdict.as<uint32_t>();
+        DP.max_len = d_maxlen;
+        launch_dict_insert(DP, s);
+        launch_dict_flags(c->dict.as<unsigned long long>(), dcap, c->flags.as<uint32_t>(), s);
         exclusive_scan_u32(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), dcap, d_total,
                            c->scan_tmp.as<uint32_t>(), s);
         CK(cudaMemcpyAsync(hs, c->scal.p, 32, cudaMemcpyDeviceToHost, s));
@@ -376,8 +404,6 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         c->vals.ensure(sort_n * 4);
         c->vals_alt.ensure(sort_n * 4);
         c->sort_tmp.ensure(radix_temp_bytes(sort_n));
-        unsigned long long* d_orand = c->scal.as<unsigned long long>() + 4;
-        unsigned long long* h_orand = reinterpret_cast<unsigned long long*>(hs + 8);
         iota_kernel<<<blocks_for(J, 256), 256, 0, s>>>(c->vals.as<uint32_t>(), J);
         count_launch();
         const int n_chunks = static_cast<int>((max_len + 7) / 8);
@@ -385,12 +411,10 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             const int cc = ch < 0 ? -1 : n_chunks - 1 - ch;
             launch_dict_chunk(c->dict.as<unsigned long long>(), c->uslot.as<uint32_t>(),
                               c->vals.as<uint32_t>(), J, cc, d_csv, c->keys.as<uint64_t>(), s);
-            // keys are gathered in current perm order; sort (keys, perm) stably
             radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(),
                              c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), J, 0, 64,
                              c->sort_tmp.p, s, d_orand, h_orand);
         }
-        // vals now holds unique indices in lexicographic order
         c->rank_of_slot.ensure(dcap * 4);
         launch_dict_rank(c->uslot.as<uint32_t>(), c->vals.as<uint32_t>(), J,
                          c->rank_of_slot.as<uint32_t>(), s);
@@ -400,38 +424,44 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
 
         // ---- canonical order -----------------------------------------------------------------
         const int tsbits = bits_for(static_cast<uint64_t>(ts_max - ts_min));
-        const int rbits = bits_for(J - 1);
-        const int mode = (tsbits + rbits <= 64) ? 0 : 1;
         c->jstart.ensure((J + 1) * 4);
         c->srank.ensure(sort_n * 4);
-        uint32_t* d_invalid = c->scal.as<uint32_t>() + 12;
-        CK(cudaMemsetAsync(d_invalid, 0, 4, s));
-        launch_head_keys(c->hrank.as<uint32_t>(), c->hslot.as<uint32_t>(), c->ts.as<int64_t>(), H,
-                         ts_min, tsbits, mode, c->keys.as<uint64_t>(), c->vals.as<uint32_t>(), s);
-        radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(), c->keys_alt.as<uint64_t>(),
-                         c->vals_alt.as<uint32_t>(), H, 0, mode == 0 ? tsbits + rbits : tsbits,
-                         c->sort_tmp.p, s, d_orand, h_orand);
-        if (mode == 1) {
-            launch_gather_rank_keys(c->hrank.as<uint32_t>(), c->vals.as<uint32_t>(), H,
-                                    c->keys.as<uint64_t>(), s);
-            radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(),
-                             c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), H, 0, rbits,
-                             c->sort_tmp.p, s, d_orand, h_orand);
-        }
-        launch_head_order_check(c->vals.as<uint32_t>(), c->hrank.as<uint32_t>(),
-                                c->hslot.as<uint32_t>(), c->ts.as<int64_t>(), H, N,
-                                c->jstart.as<uint32_t>(), d_invalid, s);
-        CK(cudaMemcpyAsync(hs, d_invalid, 4, cudaMemcpyDeviceToHost, s));
-        sync(c);
-        slow = static_cast<uint32_t*>(static_cast<void*>(hs))[0] != 0;
         uint32_t* jstart = c->jstart.as<uint32_t>();
+        {
+            const int rbits = bits_for(J - 1);
+            const int mode = (tsbits + rbits <= 64) ? 0 : 1;
+            CK(cudaMemsetAsync(d_invalid, 0, 4, s));
+            launch_head_keys(c->hrank.as<uint32_t>(), c->hslot.as<uint32_t>(), c->ts.as<int64_t>(),
+                             H, ts_min, tsbits, mode, c->keys.as<uint64_t>(),
+                             c->vals.as<uint32_t>(), s);
+            radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(),
+                             c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), H, 0,
+                             mode == 0 ? tsbits + rbits : tsbits, c->sort_tmp.p, s, d_orand, h_orand);
+            if (mode == 1) {
+                launch_gather_rank_keys(c->hrank.as<uint32_t>(), c->vals.as<uint32_t>(), H,
+                                        c->keys.as<uint64_t>(), s);
+                radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(),
+                                 c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), H, 0,
+                                 rbits, c->sort_tmp.p, s, d_orand, h_orand);
+            }
+            launch_head_order_check(c->vals.as<uint32_t>(), c->hrank.as<uint32_t>(),
+                                    c->hslot.as<uint32_t>(), c->ts.as<int64_t>(),
+                                    c->code.as<uint32_t>(), H, N, jstart, d_invalid, s);
+            CK(cudaMemcpyAsync(hs, d_invalid, 4, cudaMemcpyDeviceToHost, s));
+            sync(c);
+            slow = static_cast<uint32_t*>(static_cast<void*>(hs))[0] != 0;
+        }
         if (!slow) {
             set_u32_kernel<<<1, 1, 0, s>>>(jstart + J, static_cast<uint32_t>(H));
             count_launch();
         } else {
-            // full (rank, ts) sort of every record; provenance order breaks ties (stable)
+            // full (rank, ts) sort of every data line; provenance order breaks ties (stable);
+            // rejected lines take rank J and sort after every journey
+            const int rbits = bits_for(J);
+            const int mode = (tsbits + rbits <= 64) ? 0 : 1;
             launch_slot_keys(c->hslot.as<uint32_t>(), c->hrank.as<uint32_t>(), H,
-                             c->ts.as<int64_t>(), N, ts_min, tsbits, mode, c->keys.as<uint64_t>(),
+                             c->ts.as<int64_t>(), c->code.as<uint32_t>(), N, ts_min, tsbits, mode,
+                             static_cast<uint32_t>(J), c->keys.as<uint64_t>(),
                              c->vals.as<uint32_t>(), c->srank.as<uint32_t>(), s);
             radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(),
                              c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), N, 0,
@@ -444,19 +474,26 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
                                  c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), N, 0,
                                  rbits, c->sort_tmp.p, s, d_orand, h_orand);
             }
-            launch_slot_jstart(c->vals.as<uint32_t>(), c->srank.as<uint32_t>(), N, jstart, s);
-            set_u32_kernel<<<1, 1, 0, s>>>(jstart + J, static_cast<uint32_t>(N));
+            launch_slot_jstart(c->vals.as<uint32_t>(), c->srank.as<uint32_t>(), N,
+                               static_cast<uint32_t>(J), jstart, s);
+            set_u32_kernel<<<1, 1, 0, s>>>(jstart + J, static_cast<uint32_t>(n_parsed));
             count_launch();
         }
         CK(cudaEventRecord(c->ev[2], s));
 
         // ---- per-journey fold ------------------------------------------------------------------
-        const uint64_t pair_bound = slow ? N : std::min<uint64_t>(N, H + transitions);
-        const uint64_t pcap = pow2_at_least(2 * pair_bound);
-        c->pair_key.ensure(pcap * 8);
-        c->pair_sum.ensure(pcap * 8);
-        c->pair_cnt.ensure(pcap * 4);
-        CK(cudaMemsetAsync(c->pair_key.p, 0xFF, pcap * 8, s));
+        const int rbits = bits_for(J - 1);
+        const uint64_t pair_bound = slow ? n_parsed : std::min<uint64_t>(n_parsed, H + transitions);
+        const uint64_t scap = pow2_at_least(2 * pair_bound);
+        c->pair_key.ensure(pair_bound * 8 + 8);
+        c->pair_sum.ensure(pair_bound * 8 + 8);
+        c->pair_cnt.ensure(pair_bound * 4 + 4);
+        c->spill_key.ensure(scap * 8);
+        c->spill_sum.ensure(scap * 8);
+        c->spill_cnt.ensure(scap * 4);
+        CK(cudaMemsetAsync(c->spill_key.p, 0xFF, scap * 8, s));
+        uint32_t* d_pairs = c->scal.as<uint32_t>() + 13;
+        CK(cudaMemsetAsync(d_pairs, 0, 4, s));
         FoldParams F;
         F.n_journeys = J;
         F.jstart = jstart;
@@ -471,38 +508,35 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         F.pair_key = c->pair_key.as<uint64_t>();
         F.pair_sum = c->pair_sum.as<double>();
         F.pair_cnt = c->pair_cnt.as<uint32_t>();
-        F.pair_mask = pcap - 1;
+        F.pair_count = d_pairs;
+        F.pair_cap = pair_bound;
+        F.rank_bits = rbits;
+        F.spill_key = c->spill_key.as<uint64_t>();
+        F.spill_sum = c->spill_sum.as<double>();
+        F.spill_cnt = c->spill_cnt.as<uint32_t>();
+        F.spill_mask = scap - 1;
         F.csv = d_csv;
-        F.shard_off = c->shard_off.as<uint64_t>();
-        F.cmap = c->cmap.as<ColumnMap>();
+        F.shard_off = P.shard_off;
+        F.cmap = P.cmap;
         F.n_shards = n_shards;
-        F.stats = c->stats.as<uint64_t>();
+        F.stats = d_stats;
         launch_fold(F, slow, s);
-        CK(cudaEventRecord(c->ev[3], s));
-
-        // ---- (cell, journey) pairs -> canonical per-cell fold ----------------------------------
-        c->flags.ensure(pcap * 4 + 16);
-        c->pos.ensure(pcap * 4 + 16);
-        c->scan_tmp.ensure(scan_temp_words(pcap) * 4 + 64);
-        launch_pair_flags(c->pair_key.as<uint64_t>(), pcap, c->flags.as<uint32_t>(), s);
-        exclusive_scan_u32(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), pcap, d_total,
-                           c->scan_tmp.as<uint32_t>(), s);
-        CK(cudaMemcpyAsync(hs, d_total, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hs, d_pairs, 4, cudaMemcpyDeviceToHost, s));
         sync(c);
-        const uint64_t n_pairs = static_cast<uint32_t*>(static_cast<void*>(hs))[0];
-        c->keys.ensure(std::max<uint64_t>(n_pairs, sort_n) * 8);
+        CK(cudaEventRecord(c->ev[3], s));
+        const uint64_t n_pairs = std::min<uint64_t>(static_cast<uint32_t*>(static_cast<void*>(hs))[0], pair_bound);
+
+        // ---- (cell, journey) subtotals -> canonical per-cell fold ----------------------------------
         c->keys_alt.ensure(std::max<uint64_t>(n_pairs, sort_n) * 8);
         c->vals.ensure(std::max<uint64_t>(n_pairs, sort_n) * 4);
         c->vals_alt.ensure(std::max<uint64_t>(n_pairs, sort_n) * 4);
         c->sort_tmp.ensure(radix_temp_bytes(std::max<uint64_t>(n_pairs, sort_n)));
-        launch_pair_compact(c->pair_key.as<uint64_t>(), c->flags.as<uint32_t>(),
-                            c->pos.as<uint32_t>(), pcap, rbits, c->keys.as<uint64_t>(),
-                            c->vals.as<uint32_t>(), s);
+        launch_pair_vals(c->vals.as<uint32_t>(), n_pairs, s);
         const int gbits = bits_for(dims.cells - 1);
-        radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(), c->keys_alt.as<uint64_t>(),
-                         c->vals_alt.as<uint32_t>(), n_pairs, 0, gbits + rbits, c->sort_tmp.p, s,
-                         d_orand, h_orand);
-        launch_finalize(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(), n_pairs, rbits,
+        radix_sort_pairs(c->pair_key.as<uint64_t>(), c->vals.as<uint32_t>(),
+                         c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), n_pairs, 0,
+                         gbits + rbits, c->sort_tmp.p, s, d_orand, h_orand);
+        launch_finalize(c->pair_key.as<uint64_t>(), c->vals.as<uint32_t>(), n_pairs, rbits,
                         c->pair_sum.as<double>(), c->pair_cnt.as<uint32_t>(), dims.D, dims.RC,
                         d_planes, d_raw, s);
     } else {
@@ -510,7 +544,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         CK(cudaEventRecord(c->ev[3], s));
     }
     CK(cudaEventRecord(c->ev[4], s));
-    CK(cudaMemcpyAsync(hs, c->stats.p, kStCount * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hs, d_stats, kStCount * 8, cudaMemcpyDeviceToHost, s));
     sync(c);
     CK(cudaGetLastError());
     if (hs[kStOverflow]) fail(CVLG_E_INTERNAL, "aggregation capacity invariant violated");
@@ -715,8 +749,8 @@ void cvlg_context_destroy(cvlg_context* c) {
     cudaStreamSynchronize(c->copy_stream);
     DevBuf* bufs[] = {&c->csv,    &c->shard_off, &c->cmap,     &c->good,     &c->lb_flag,
                       &c->lb_val, &c->counter,   &c->stats,    &c->tsmm,     &c->ts,
-                      &c->speed,  &c->code,      &c->loff,     &c->hslot,    &c->hk0,
-                      &c->hk1,    &c->hidref,    &c->hhash,    &c->dict,     &c->hdict,
+                      &c->speed,  &c->code,      &c->loff,     &c->hslot,    &c->spill_key,
+                      &c->spill_sum, &c->spill_cnt, &c->dict,     &c->hdict,
                       &c->flags,  &c->pos,       &c->uslot,    &c->rank_of_slot, &c->hrank,
                       &c->scal,   &c->keys,      &c->vals,     &c->keys_alt, &c->vals_alt,
                       &c->sort_tmp, &c->scan_tmp, &c->srank,   &c->jstart,   &c->pair_key,

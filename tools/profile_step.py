@@ -1,0 +1,29 @@
+"""Runs the device-resident pipeline on the c2 workload for ncu captures:
+    ncu ... python tools/profile_step.py [--journeys N] [--steps S]"""
+import argparse
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch  # noqa: E402
+
+import paper_2305_07454_b200 as cvlg  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--journeys", type=int, default=100_000)
+ap.add_argument("--shards", type=int, default=16)
+ap.add_argument("--steps", type=int, default=1)
+ap.add_argument("--shuffle", action="store_true")
+a = ap.parse_args()
+blob, offs, rows = cvlg.synth_day(seed=1, journeys=a.journeys, shards=a.shards, mean_duration=500.0)
+spec = cvlg.GridSpec()
+T, _, R, C = spec.dims()
+d_csv = torch.from_numpy(blob).cuda()
+d_planes = torch.empty((T, 8, R, C), dtype=torch.int32, device="cuda")
+d_raw = torch.empty((T, 4, R, C), dtype=torch.int32, device="cuda")
+ctx = cvlg.Context()
+for _ in range(a.steps):
+    cvlg.run_pipeline_device(d_csv.data_ptr(), offs, d_planes.data_ptr(), d_raw.data_ptr(), spec,
+                             ctx=ctx)
+print("rows", rows, "stage_ms", ctx.stage_ms())
