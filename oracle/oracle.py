@@ -126,6 +126,8 @@ class Ref:
                                                 ctypes.POINTER(ctypes.c_int64)]
             lib.ref_journey_hash.argtypes = [ctypes.c_char_p, ctypes.c_size_t]
             lib.ref_journey_hash.restype = ctypes.c_uint64
+            lib.ref_from_chars.argtypes = [ctypes.c_char_p, ctypes.c_size_t,
+                                           ctypes.POINTER(ctypes.c_double)]
             lib.ref_deduplicate.argtypes = [ctypes.POINTER(ctypes.c_char_p), ctypes.c_size_t,
                                             vp, vp, vp, ctypes.c_int64,
                                             ctypes.POINTER(ctypes.c_uint64)]
@@ -213,7 +215,88 @@ class Ref:
     def journey_hash(self, s: bytes) -> int:
         return self.lib.ref_journey_hash(s, len(s))
 
+    def from_chars(self, s: bytes):
+        out = ctypes.c_double()
+        ok = self.lib.ref_from_chars(s, len(s), ctypes.byref(out))
+        return out.value if ok else None
+
     def timestamp(self, s: bytes):
         out = ctypes.c_int64()
         ok = self.lib.ref_timestamp_parse(s, len(s), ctypes.byref(out))
         return out.value if ok else None
+
+
+class Restated:
+    """The plain-C restatement (oracle/cvl_oracle.c)."""
+
+    _lib = None
+
+    def __init__(self):
+        if Restated._lib is None:
+            if not ORACLE_LIB.exists():
+                raise FileNotFoundError(f"{ORACLE_LIB} not built (make -C oracle oracle)")
+            lib = ctypes.CDLL(str(ORACLE_LIB))
+            vp = ctypes.c_void_p
+            lib.ora_run_pipeline.argtypes = [ctypes.POINTER(ctypes.c_char_p), ctypes.c_size_t,
+                                             ctypes.POINTER(CGrid), ctypes.POINTER(CRules), vp, vp,
+                                             ctypes.POINTER(CStats), ctypes.c_char_p,
+                                             ctypes.c_size_t]
+            lib.ora_parse_double.argtypes = [ctypes.c_char_p, ctypes.c_size_t,
+                                             ctypes.POINTER(ctypes.c_double)]
+            lib.ora_parse_timestamp.argtypes = [ctypes.c_char_p, ctypes.c_size_t,
+                                                ctypes.POINTER(ctypes.c_int64)]
+            lib.ora_parse_header.argtypes = [ctypes.c_char_p, ctypes.c_size_t, vp]
+            lib.ora_parse_record.argtypes = [ctypes.c_char_p, ctypes.c_size_t, vp, vp]
+            lib.ora_grid_dims.argtypes = [ctypes.POINTER(CGrid)] + [ctypes.POINTER(ctypes.c_uint32)] * 4
+            lib.ora_journey_hash.argtypes = [ctypes.c_char_p, ctypes.c_size_t]
+            lib.ora_journey_hash.restype = ctypes.c_uint64
+            lib.ora_write_container.argtypes = [vp, ctypes.POINTER(CGrid), ctypes.c_int32,
+                                                ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint64)]
+            Restated._lib = lib
+        self.lib = Restated._lib
+
+    @staticmethod
+    def available() -> bool:
+        return ORACLE_LIB.exists()
+
+    def dims(self, spec):
+        t, d, r, c = (ctypes.c_uint32() for _ in range(4))
+        rc = self.lib.ora_grid_dims(ctypes.byref(grid_struct(spec)), ctypes.byref(t), ctypes.byref(d),
+                                    ctypes.byref(r), ctypes.byref(c))
+        if rc:
+            raise RefError(rc, "BadGrid")
+        return t.value, d.value, r.value, c.value
+
+    def run_pipeline(self, paths, spec, rules=None, raw=True):
+        t, _, r, c = self.dims(spec)
+        planes = np.zeros((t, 8, r, c), dtype=np.uint32)
+        rawa = np.zeros((t, 4, r, c), dtype=np.uint32) if raw else None
+        arr = (ctypes.c_char_p * max(len(paths), 1))(*[str(p).encode() for p in paths])
+        st = CStats()
+        err = ctypes.create_string_buffer(512)
+        rc = self.lib.ora_run_pipeline(arr, len(paths), ctypes.byref(grid_struct(spec)),
+                                       ctypes.byref(rules_struct(rules)),
+                                       planes.ctypes.data_as(ctypes.c_void_p),
+                                       None if rawa is None else rawa.ctypes.data_as(ctypes.c_void_p),
+                                       ctypes.byref(st), err, 512)
+        if rc:
+            raise RefError(rc, err.value.decode())
+        return planes, rawa, st.as_dict()
+
+    def parse_double(self, s: bytes):
+        out = ctypes.c_double()
+        ok = self.lib.ora_parse_double(s, len(s), ctypes.byref(out))
+        return out.value if ok else None
+
+    def parse_timestamp(self, s: bytes):
+        out = ctypes.c_int64()
+        ok = self.lib.ora_parse_timestamp(s, len(s), ctypes.byref(out))
+        return out.value if ok else None
+
+    def parse_header(self, line: bytes):
+        cols = (ctypes.c_int32 * 8)()
+        ok = self.lib.ora_parse_header(line, len(line), cols)
+        return list(cols) if ok else None
+
+    def journey_hash(self, s: bytes) -> int:
+        return self.lib.ora_journey_hash(s, len(s))

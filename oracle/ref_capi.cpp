@@ -14,6 +14,7 @@
 //   ref_bins              -> lat_bin/lon_bin/time_bin/dxn_bin/global_index  grid.hpp:49-56
 //   ref_journey_hash      -> cvl::journey_hash            proj/include/cvl/ingest.hpp:68
 //   ref_deduplicate       -> cvl::deduplicate             proj/include/cvl/ingest.hpp:63
+#include <charconv>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -322,6 +323,14 @@ int ref_timestamp_parse(const char* text, size_t len, int64_t* out) {
     if (!ts) return 0;
     *out = ts->epoch_sec;
     return 1;
+}
+
+// parse_double (ingest.cpp:66-72) is file-local in the reference; it is exactly this call of the
+// libstdc++ std::from_chars the reference links against.
+int ref_from_chars(const char* s, size_t len, double* out) {
+    if (len == 0) return 0;
+    auto [ptr, ec] = std::from_chars(s, s + len, *out);
+    return ec == std::errc() && ptr == s + len;
 }
 
 uint64_t ref_journey_hash(const char* id, size_t len) {
