@@ -359,6 +359,11 @@ __global__ void __launch_bounds__(256) fold_warp_kernel(FoldParams P) {
                 valid = slot < run_end;
                 run_pos += 32;
             }
+            if (!kSlow && slot + 64 < run_end) {
+                // the warp's next windows of this run: pull them toward L2 while this one folds
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(P.code + slot + 64));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(P.speed + slot + 64));
+            }
             uint32_t code = valid ? (P.code[slot] & kCodeMask) : kCodeRejected;
             const double v = valid ? P.speed[slot] : 0.0;
             bool dup = false;

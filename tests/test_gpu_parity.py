@@ -237,6 +237,39 @@ def test_host_and_device_entry_points(ref, day_cache):
     assert stats_dict(st2) == est
 
 
+def test_cpp_dropin_with_reference_types(day_cache):
+    """include/cvlg.hpp: cvl::gpu::run_pipeline over the reference's own C++ types, compared
+    in C++ with cvl::run_pipeline (BatchFrame::bitwise_equal, raw counts, stats, container
+    bytes) — tests/native/dropin_main.cpp."""
+    import subprocess
+    exe = Path(__file__).resolve().parent / "native" / "_build" / "dropin"
+    if not exe.exists():
+        pytest.skip("drop-in demo not built (needs the reference headers at build time)")
+    paths, _ = day_cache(seed=12, journeys=50)
+    for step in ("0.1", "0.25", "10"):
+        r = subprocess.run([str(exe), step, *paths], capture_output=True, text=True)
+        assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+    golden = Path(__file__).resolve().parent / "golden" / "days" / "malformed"
+    r = subprocess.run([str(exe), "0.5", *sorted(str(p) for p in golden.glob("*.csv"))],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+
+
+def test_golden_days_gpu():
+    """Committed reference fixtures (no reference needed at run time)."""
+    import json
+    import paper_2305_07454_b200 as cvlg
+    root = Path(__file__).resolve().parent / "golden" / "days"
+    for case in ("synth_small", "dups_shuffled", "malformed", "table1"):
+        meta = json.loads((root / case / "expected.json").read_text())
+        exp = np.load(root / case / "expected.npz")
+        st = cvlg.PipelineStats()
+        lat = cvlg.run_pipeline([str(root / case / s) for s in meta["shards"]],
+                                cvlg.GridSpec(**meta["grid"]), stats=st)
+        assert diff_lattice(exp["planes"], exp["raw"], lat.planes, lat.raw) == "", case
+        assert stats_dict(st) == meta["stats"], case
+
+
 def test_empty_manifest(ref):
     import paper_2305_07454_b200 as cvlg
     st = cvlg.PipelineStats()
