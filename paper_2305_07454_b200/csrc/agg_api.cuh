@@ -41,7 +41,8 @@ struct FoldParams {
     uint32_t* pair_count;
     uint64_t pair_cap;
     int rank_bits;
-    // spill table for journeys with > 32 distinct cells, key = cell << 32 | rank
+    uint64_t* journey_counter;  // dynamic journey assignment (zeroed before the fold)
+    // (cell, journey) table, key = cell << 32 | rank
     uint64_t* spill_key;
     double* spill_sum;
     uint32_t* spill_cnt;

@@ -292,197 +292,212 @@ __device__ bool payload_equal(const FoldParams& P, uint64_t la, uint64_t lb) {
 }
 
 // ---- F: per-journey fold -----------------------------------------------------------------------
-// One warp per journey. Records arrive 32 at a time in (rank, ts) order; __match_any_sync groups
-// a window's records by cell; each distinct cell of the journey is owned by one lane, which adds
-// its group's speeds in lane (= timestamp) order: the per-(cell, journey) subtotal is exactly the
-// reference's sequential left fold (aggregate.cpp:349-356). A journey with more than 32 distinct
-// cells spills least-recently-assigned accumulators to a (cell, journey) hash table and reloads
-// them on re-entry, preserving the fold order.
-__device__ __forceinline__ uint64_t spill_find(const FoldParams& P, uint64_t key, bool insert) {
+// One LANE per journey (dynamic assignment), so the inherently sequential per-(cell, journey)
+// left fold (aggregate.cpp:349-356) runs with every lane busy. Each window the warp stages the
+// next kChunk records of all 32 lanes' streams into shared memory with coalesced loads (two
+// lanes' chunks per instruction), then every lane walks its own chunk in (rank, ts) order.
+// Accumulators live in registers while consecutive records share a cell; on a cell change the
+// running (sum, count) is parked in the (cell, journey) hash table and the new cell's is loaded
+// (re-entries continue the same fold), so per-(cell, journey) subtotals are exact.
+constexpr int kFoldWarps = 4;
+constexpr int kChunk = 8;
+constexpr int kLaneCellsFast = 16;  // per-lane cell table; a journey visits ~9 cells
+constexpr int kLaneCellsSlow = 12;  // (slow path also stages slot ids: less shared memory left)
+
+__device__ __forceinline__ uint64_t table_find(const FoldParams& P, uint64_t key, bool insert,
+                                               bool& fresh) {
     uint64_t slot = mix64(key) & P.spill_mask;
+    fresh = false;
     for (uint64_t probe = 0; probe <= P.spill_mask; ++probe) {
         uint64_t cur = P.spill_key[slot];
         if (cur == kEmpty && insert) {
             cur = atomicCAS(reinterpret_cast<unsigned long long*>(&P.spill_key[slot]), kEmpty, key);
             if (cur == kEmpty) {
-                P.spill_sum[slot] = 0.0;
-                P.spill_cnt[slot] = 0;
+                fresh = true;
                 return slot;
             }
         }
         if (cur == key) return slot;
-        if (cur == kEmpty) return kEmpty;  // not present (find only)
+        if (cur == kEmpty) return kEmpty;
         slot = (slot + 1) & P.spill_mask;
     }
     return kEmpty;
 }
 
 template <bool kSlow>
-__global__ void __launch_bounds__(256) fold_warp_kernel(FoldParams P) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t lt = (1u << lane) - 1u;
-    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+__global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P) {
+    constexpr int kLaneCells = kSlow ? kLaneCellsSlow : kLaneCellsFast;
+    __shared__ uint32_t s_code[kFoldWarps][32][kChunk + 1];
+    __shared__ double s_speed[kFoldWarps][32][kChunk + 1];
+    __shared__ uint32_t s_slot[kSlow ? kFoldWarps : 1][32][kChunk + 1];
+    // per-lane (cell -> running subtotal) table, entry e of lane l at [e][l]
+    __shared__ uint32_t t_g[kFoldWarps][kLaneCells][32];
+    __shared__ uint32_t t_c[kFoldWarps][kLaneCells][32];
+    __shared__ double t_s[kFoldWarps][kLaneCells][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t c_acc = 0, c_oog = 0, c_spd = 0, c_miss = 0, c_unb = 0, c_dup = 0, c_conf = 0,
              c_ovf = 0;
-    for (uint64_t j = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
-         j < P.n_journeys; j += warps) {
-        uint32_t own_g = kNone;
-        double own_sum = 0.0;
-        uint32_t own_cnt = 0;
-        uint32_t n_owned = 0, evict = 0;
-        bool spilled = false;
-        const uint32_t jb = P.jstart[j], je = P.jstart[j + 1];
-        // slow path dedup carry
-        int64_t carry_ts = 0;
-        uint64_t carry_surv = 0;
-        bool have_carry = false;
-        uint32_t r = jb;
-        uint64_t run_pos = 0, run_end = 0;
-        while (true) {
-            // ---- next window of up to 32 records ----------------------------------------------
-            uint64_t slot = 0;
-            bool valid;
+
+    uint64_t j = atomicAdd(reinterpret_cast<unsigned long long*>(P.journey_counter), 1ull);
+    bool active = j < P.n_journeys;
+    uint32_t ri = 0, re = 0;    // fast path: remaining runs of the journey, [ri, re) in perm
+    uint64_t pos = 0, end = 0;  // current stream window: slots (fast) / perm positions (slow)
+    uint32_t n_cells = 0;       // entries used in this lane's table
+    uint32_t cur = 0;           // table entry of the current cell (valid when n_cells > 0)
+    uint32_t cur_g = kNone;
+    double cur_sum = 0.0;
+    uint32_t cur_cnt = 0;
+    uint32_t evict = 0;
+    bool spilled = false;
+    int64_t prev_ts = 0;
+    uint64_t surv = 0;
+    bool have_prev = false;
+
+    auto open_run = [&](uint32_t h) {
+        pos = P.hslot[h];
+        end = (h + 1 < P.n_heads) ? P.hslot[h + 1] : P.n_slots;
+    };
+    auto start_journey = [&]() {
+        cur_g = kNone;
+        n_cells = 0;
+        evict = 0;
+        spilled = false;
+        have_prev = false;
+        if (kSlow) {
+            pos = P.jstart[j];
+            end = P.jstart[j + 1];
+        } else {
+            ri = P.jstart[j];
+            re = P.jstart[j + 1];
+            open_run(P.perm[ri++]);
+        }
+    };
+    auto spill_store = [&](uint32_t g, double s, uint32_t c) {
+        bool fresh;
+        const uint64_t t = table_find(P, (static_cast<uint64_t>(g) << 32) | j, true, fresh);
+        if (t == kEmpty) {
+            ++c_ovf;
+            return;
+        }
+        P.spill_sum[t] = s;
+        P.spill_cnt[t] = c;
+    };
+    // write the whole journey out: appended pairs, or the spill table once it has spilled
+    auto flush_journey = [&]() {
+        if (cur_g != kNone) {
+            t_s[warp][cur][lane] = cur_sum;
+            t_c[warp][cur][lane] = cur_cnt;
+        }
+        if (!spilled) {
+            const uint32_t base = n_cells ? atomicAdd(P.pair_count, n_cells) : 0u;
+            for (uint32_t e = 0; e < n_cells; ++e) {
+                const uint64_t at = static_cast<uint64_t>(base) + e;
+                if (at >= P.pair_cap) {
+                    ++c_ovf;
+                    continue;
+                }
+                P.pair_key[at] = (static_cast<uint64_t>(t_g[warp][e][lane]) << P.rank_bits) | j;
+                P.pair_sum[at] = t_s[warp][e][lane];
+                P.pair_cnt[at] = t_c[warp][e][lane];
+            }
+        } else {
+            for (uint32_t e = 0; e < n_cells; ++e)
+                spill_store(t_g[warp][e][lane], t_s[warp][e][lane], t_c[warp][e][lane]);
+        }
+    };
+    if (active) start_journey();
+
+    while (__any_sync(0xFFFFFFFFu, active)) {
+        const uint64_t left = end - pos;
+        const uint32_t avail = !active ? 0u : (left < kChunk ? static_cast<uint32_t>(left) : kChunk);
+        // ---- stage every lane's next chunk: 32/kChunk lane chunks per coalesced load ----------
+        constexpr int kPer = 32 / kChunk;
+#pragma unroll
+        for (int l = 0; l < 32; l += kPer) {
+            const int src = l + lane / kChunk;
+            const uint64_t p0 = __shfl_sync(0xFFFFFFFFu, pos, src);
+            const uint32_t a = __shfl_sync(0xFFFFFFFFu, avail, src);
+            const int k = lane % kChunk;
+            if (static_cast<uint32_t>(k) < a) {
+                const uint64_t slot = kSlow ? P.perm[p0 + k] : p0 + k;
+                s_code[warp][src][k] = P.code[slot];
+                s_speed[warp][src][k] = P.speed[slot];
+                if (kSlow) s_slot[warp][src][k] = static_cast<uint32_t>(slot);
+            }
+        }
+        __syncwarp();
+        // ---- sequential walk of this lane's chunk ---------------------------------------------
+        for (uint32_t k = 0; k < avail; ++k) {
+            const uint32_t code = s_code[warp][lane][k] & kCodeMask;
             if (kSlow) {
-                if (r >= je) break;
-                const uint32_t i = r + lane;
-                valid = i < je;
-                if (valid) slot = P.perm[i];
-                r += 32;
-            } else {
-                if (run_pos >= run_end) {
-                    if (r >= je) break;
-                    const uint32_t h = P.perm[r++];
-                    run_pos = P.hslot[h];
-                    run_end = (h + 1 < P.n_heads) ? P.hslot[h + 1] : P.n_slots;
+                const uint32_t slot = s_slot[warp][lane][k];
+                const int64_t t = P.ts[slot];
+                if (have_prev && t == prev_ts) {  // duplicate key: dropped before filtering
+                    ++c_dup;
+                    if (!payload_equal(P, P.loff[slot], P.loff[surv])) ++c_conf;
+                    continue;
                 }
-                slot = run_pos + lane;
-                valid = slot < run_end;
-                run_pos += 32;
+                have_prev = true;
+                prev_ts = t;
+                surv = slot;
             }
-            if (!kSlow && slot + 64 < run_end) {
-                // the warp's next windows of this run: pull them toward L2 while this one folds
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(P.code + slot + 64));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(P.speed + slot + 64));
-            }
-            uint32_t code = valid ? (P.code[slot] & kCodeMask) : kCodeRejected;
-            const double v = valid ? P.speed[slot] : 0.0;
-            bool dup = false;
-            if (kSlow) {
-                const int64_t t = valid ? P.ts[slot] : 0;
-                const int64_t prev = __shfl_up_sync(0xFFFFFFFFu, t, 1);
-                const bool has_prev = lane > 0 ? true : have_carry;
-                const int64_t pt = lane > 0 ? prev : carry_ts;
-                dup = valid && has_prev && t == pt;
-                const uint32_t heads = __ballot_sync(0xFFFFFFFFu, valid && !dup);
-                if (__ballot_sync(0xFFFFFFFFu, dup)) {
-                    // survivor = nearest earlier non-duplicate lane (min provenance of the
-                    // key group, aggregate.cpp:287-289), or the carried survivor
-                    const uint32_t hb = heads & lt;
-                    const int sl = hb ? 31 - __clz(hb) : lane;
-                    const uint64_t s_from_lane = __shfl_sync(0xFFFFFFFFu, slot, sl);
-                    if (dup) {
-                        ++c_dup;
-                        const uint64_t surv = hb ? s_from_lane : carry_surv;
-                        if (!payload_equal(P, P.loff[slot], P.loff[surv])) ++c_conf;
-                    }
-                }
-                // carry: last valid lane's ts and the survivor at that point
-                const uint32_t vm = __ballot_sync(0xFFFFFFFFu, valid);
-                if (vm) {
-                    const int last = 31 - __clz(vm);
-                    carry_ts = __shfl_sync(0xFFFFFFFFu, t, last);
-                    const uint32_t hb = heads & (last == 31 ? 0xFFFFFFFFu : ((2u << last) - 1u));
-                    if (hb) carry_surv = __shfl_sync(0xFFFFFFFFu, slot, 31 - __clz(hb));
-                    have_carry = true;
-                }
-                if (dup) code = kCodeRejected;  // dropped before filtering (aggregate.cpp:291-293)
-            }
-            // ---- filter accounting --------------------------------------------------------------
-            const bool active = code < kCodeFirstSpecial;
-            if (valid && !dup && !active) {
+            if (code >= kCodeFirstSpecial) {
                 if (code == kCodeOutOfGrid) ++c_oog;
                 else if (code == kCodeSpeedCeiling) ++c_spd;
                 else if (code == kCodeMissingField) ++c_miss;
                 else if (code == kCodeUnbinnable) ++c_unb;
-                // kCodeRejected: parse rejects are counted by decode
+                continue;  // kCodeRejected: counted by decode
             }
-            c_acc += active ? 1u : 0u;
-            const uint32_t g = active ? code : kNone;
-            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, g);
-            uint32_t lmask = __ballot_sync(0xFFFFFFFFu, active && (peers & lt) == 0);
-            uint32_t my_group = 0;
-            while (lmask) {
-                const int L = __ffs(lmask) - 1;
-                lmask &= lmask - 1;
-                const uint32_t gq = __shfl_sync(0xFFFFFFFFu, g, L);
-                const uint32_t grp = __shfl_sync(0xFFFFFFFFu, peers, L);
-                const uint32_t om = __ballot_sync(0xFFFFFFFFu, own_g == gq);
-                int owner;
-                if (om) {
-                    owner = __ffs(om) - 1;
+            ++c_acc;
+            if (code != cur_g) {
+                if (cur_g != kNone) {  // park the current subtotal in its table entry
+                    t_s[warp][cur][lane] = cur_sum;
+                    t_c[warp][cur][lane] = cur_cnt;
+                }
+                uint32_t e = 0;
+                while (e < n_cells && t_g[warp][e][lane] != code) ++e;
+                if (e < n_cells) {
+                    cur_sum = t_s[warp][e][lane];
+                    cur_cnt = t_c[warp][e][lane];
                 } else {
-                    if (n_owned < 32) {
-                        owner = static_cast<int>(n_owned++);
-                    } else {
-                        owner = static_cast<int>(evict);
-                        evict = (evict + 1) & 31;
-                        if (lane == owner) {  // spill the evicted accumulator
-                            const uint64_t s = spill_find(P, (static_cast<uint64_t>(own_g) << 32) | j, true);
-                            if (s == kEmpty) ++c_ovf;
-                            else {
-                                P.spill_sum[s] = own_sum;
-                                P.spill_cnt[s] = own_cnt;
-                            }
-                        }
+                    if (n_cells < kLaneCells) {
+                        e = n_cells++;
+                    } else {  // table full: move the oldest-assigned entry to the spill table
+                        e = evict;
+                        evict = (evict + 1) % kLaneCells;
+                        spill_store(t_g[warp][e][lane], t_s[warp][e][lane], t_c[warp][e][lane]);
                         spilled = true;
                     }
-                    if (lane == owner) {
-                        own_g = gq;
-                        own_sum = 0.0;
-                        own_cnt = 0;
-                        if (spilled) {
-                            const uint64_t s = spill_find(P, (static_cast<uint64_t>(gq) << 32) | j, false);
-                            if (s != kEmpty) {
-                                own_sum = P.spill_sum[s];
-                                own_cnt = P.spill_cnt[s];
-                            }
+                    cur_sum = 0.0;
+                    cur_cnt = 0;
+                    if (spilled) {  // the cell may have been evicted earlier: continue its fold
+                        bool fresh;
+                        const uint64_t t = table_find(P, (static_cast<uint64_t>(code) << 32) | j,
+                                                      false, fresh);
+                        if (t != kEmpty) {
+                            cur_sum = P.spill_sum[t];
+                            cur_cnt = P.spill_cnt[t];
                         }
                     }
+                    t_g[warp][e][lane] = code;
                 }
-                if (lane == owner) my_group = grp;
+                cur = e;
+                cur_g = code;
             }
-            // sequential adds in lane order, one owner lane per cell
-            while (__any_sync(0xFFFFFFFFu, my_group != 0)) {
-                const int src = my_group ? __ffs(my_group) - 1 : lane;
-                const double x = __shfl_sync(0xFFFFFFFFu, v, src);
-                if (my_group) {
-                    own_sum = __dadd_rn(own_sum, x);
-                    ++own_cnt;
-                    my_group &= my_group - 1;
-                }
-            }
+            cur_sum = __dadd_rn(cur_sum, s_speed[warp][lane][k]);  // aggregate.cpp:354
+            ++cur_cnt;
         }
-        // ---- emit this journey's (cell, journey) subtotals ----------------------------------------
-        if (!spilled) {
-            uint32_t base = 0;
-            if (lane == 0 && n_owned) base = atomicAdd(P.pair_count, n_owned);
-            base = __shfl_sync(0xFFFFFFFFu, base, 0);
-            if (static_cast<uint32_t>(lane) < n_owned) {
-                const uint64_t pos = base + lane;
-                if (pos < P.pair_cap) {
-                    P.pair_key[pos] = (static_cast<uint64_t>(own_g) << P.rank_bits) | j;
-                    P.pair_sum[pos] = own_sum;
-                    P.pair_cnt[pos] = own_cnt;
-                } else {
-                    ++c_ovf;
-                }
-            }
-        } else if (own_g != kNone) {
-            const uint64_t s = spill_find(P, (static_cast<uint64_t>(own_g) << 32) | j, true);
-            if (s == kEmpty) ++c_ovf;
-            else {
-                P.spill_sum[s] = own_sum;
-                P.spill_cnt[s] = own_cnt;
+        __syncwarp();
+        // ---- advance the stream ----------------------------------------------------------------
+        pos += avail;
+        if (active && pos >= end) {
+            if (!kSlow && ri < re) {
+                open_run(P.perm[ri++]);
+            } else {
+                flush_journey();
+                j = atomicAdd(reinterpret_cast<unsigned long long*>(P.journey_counter), 1ull);
+                active = j < P.n_journeys;
+                if (active) start_journey();
             }
         }
     }
@@ -640,8 +655,11 @@ void launch_fold(const FoldParams& p, bool slow, cudaStream_t s) {
     if (p.n_journeys) {
         const uint64_t warps = p.n_journeys;
         const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((warps + 7) / 8, 148ull * 64));
-        if (slow) fold_warp_kernel<true><<<blocks, 256, 0, s>>>(p);
-        else fold_warp_kernel<false><<<blocks, 256, 0, s>>>(p);
+        (void)blocks;
+        // enough lanes for every journey, capped at the resident capacity (dynamic assignment)
+        const unsigned lb = static_cast<unsigned>(std::min<uint64_t>((p.n_journeys + kFoldWarps * 32 - 1) / (kFoldWarps * 32), 148ull * 16));
+        if (slow) fold_lane_kernel<true><<<lb, kFoldWarps * 32, 0, s>>>(p);
+        else fold_lane_kernel<false><<<lb, kFoldWarps * 32, 0, s>>>(p);
         count_launch();
     }
     spill_drain_kernel<<<grid_for(p.spill_mask + 1, 256), 256, 0, s>>>(p);

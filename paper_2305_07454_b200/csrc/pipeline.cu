@@ -132,7 +132,7 @@ Dims validate_grid(const cvlg_grid_spec* s) {
              "dxn_step < 90: BatchFrame holds 4 direction planes (aggregate.hpp:52-54); the "
              "reference indexes past them (undefined behaviour)");
     if (d.cells >= kCodeFirstSpecial)
-        fail(CVLG_E_UNSUPPORTED, "grid has >= 2^32-4 cells; the device cell code is 32-bit");
+        fail(CVLG_E_UNSUPPORTED, "grid has >= 2^31-16 cells; the device cell code is 31-bit");
     return d;
 }
 
@@ -221,6 +221,17 @@ uint64_t* h_small64(cvlg_context* c) { return static_cast<uint64_t*>(c->h_small.
 
 void sync(cvlg_context* c) { CK(cudaStreamSynchronize(c->stream)); }
 
+// CVLG_TRACE=1: host timestamps of the pipeline phases on stderr (diagnostics only)
+struct Tracer {
+    bool on = std::getenv("CVLG_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void operator()(const char* what) const {
+        if (!on) return;
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        std::fprintf(stderr, "[cvlg] %9.3f ms  %s\n", ms, what);
+    }
+};
+
 // The pipeline proper over CSV bytes in HBM. `marks` drive incremental decode while the bytes
 // stream in; the last mark must cover everything.
 void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>& shard_off,
@@ -238,6 +249,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
     c->h_small.ensure(4096);
     uint64_t* hs = h_small64(c);
     uint64_t* d_stats = nullptr;
+    const Tracer TRACE;
 
     CK(cudaEventRecord(c->ev[0], s));
     // ---- setup -----------------------------------------------------------------------------
@@ -332,6 +344,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         slot_cap = N;  // exact count from the look-back totals
     }
     CK(cudaEventRecord(c->ev[1], s));
+        TRACE("decode done");
     if (hs[kStOverflow]) fail(CVLG_E_INTERNAL, "decode capacity invariant violated");
     const uint64_t n_parsed = hs[kStParsed];
     const uint64_t transitions = hs[kStGTransitions];
@@ -386,6 +399,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         DP.hdict = c->hdict.as<uint32_t>();
         DP.max_len = d_maxlen;
         launch_dict_insert(DP, s);
+        TRACE("dict inserted");
         launch_dict_flags(c->dict.as<unsigned long long>(), dcap, c->flags.as<uint32_t>(), s);
         exclusive_scan_u32(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), dcap, d_total,
                            c->scan_tmp.as<uint32_t>(), s);
@@ -394,6 +408,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         const uint64_t max_len = hs[0];
         J = static_cast<uint32_t*>(static_cast<void*>(hs))[4];
         c->uslot.ensure(J * 4);
+        TRACE("dict compacted");
         launch_dict_compact(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), dcap,
                             c->uslot.as<uint32_t>(), s);
 
@@ -421,9 +436,11 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         c->hrank.ensure(H * 4);
         launch_head_rank(c->hdict.as<uint32_t>(), c->rank_of_slot.as<uint32_t>(), H,
                          c->hrank.as<uint32_t>(), s);
+        TRACE("dict sorted");
 
         // ---- canonical order -----------------------------------------------------------------
         const int tsbits = bits_for(static_cast<uint64_t>(ts_max - ts_min));
+        TRACE("ranks done");
         c->jstart.ensure((J + 1) * 4);
         c->srank.ensure(sort_n * 4);
         uint32_t* jstart = c->jstart.as<uint32_t>();
@@ -479,21 +496,16 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             set_u32_kernel<<<1, 1, 0, s>>>(jstart + J, static_cast<uint32_t>(n_parsed));
             count_launch();
         }
+        TRACE("order done");
         CK(cudaEventRecord(c->ev[2], s));
 
         // ---- per-journey fold ------------------------------------------------------------------
         const int rbits = bits_for(J - 1);
         const uint64_t pair_bound = slow ? n_parsed : std::min<uint64_t>(n_parsed, H + transitions);
-        const uint64_t scap = pow2_at_least(2 * pair_bound);
         c->pair_key.ensure(pair_bound * 8 + 8);
         c->pair_sum.ensure(pair_bound * 8 + 8);
         c->pair_cnt.ensure(pair_bound * 4 + 4);
-        c->spill_key.ensure(scap * 8);
-        c->spill_sum.ensure(scap * 8);
-        c->spill_cnt.ensure(scap * 4);
-        CK(cudaMemsetAsync(c->spill_key.p, 0xFF, scap * 8, s));
         uint32_t* d_pairs = c->scal.as<uint32_t>() + 13;
-        CK(cudaMemsetAsync(d_pairs, 0, 4, s));
         FoldParams F;
         F.n_journeys = J;
         F.jstart = jstart;
@@ -511,18 +523,35 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         F.pair_count = d_pairs;
         F.pair_cap = pair_bound;
         F.rank_bits = rbits;
-        F.spill_key = c->spill_key.as<uint64_t>();
-        F.spill_sum = c->spill_sum.as<double>();
-        F.spill_cnt = c->spill_cnt.as<uint32_t>();
-        F.spill_mask = scap - 1;
+        F.journey_counter = c->scal.as<uint64_t>() + 7;
         F.csv = d_csv;
         F.shard_off = P.shard_off;
         F.cmap = P.cmap;
         F.n_shards = n_shards;
         F.stats = d_stats;
-        launch_fold(F, slow, s);
-        CK(cudaMemcpyAsync(hs, d_pairs, 4, cudaMemcpyDeviceToHost, s));
-        sync(c);
+        // The spill table only holds journeys with more distinct cells than a lane keeps in
+        // shared memory; start small and re-run with the exact bound if it ever fills.
+        uint64_t scap = pow2_at_least(std::max<uint64_t>(1u << 18, pair_bound / 2));
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            c->spill_key.ensure(scap * 8);
+            c->spill_sum.ensure(scap * 8);
+            c->spill_cnt.ensure(scap * 4);
+            CK(cudaMemsetAsync(c->spill_key.p, 0xFF, scap * 8, s));
+            CK(cudaMemsetAsync(d_pairs, 0, 4, s));
+            CK(cudaMemsetAsync(F.journey_counter, 0, 8, s));
+            CK(cudaMemsetAsync(d_stats + kStDups, 0, (kStFiltMissing - kStDups + 1) * 8, s));
+            CK(cudaMemsetAsync(d_stats + kStUnbinnable, 0, 2 * 8, s));
+            F.spill_key = c->spill_key.as<uint64_t>();
+            F.spill_sum = c->spill_sum.as<double>();
+            F.spill_cnt = c->spill_cnt.as<uint32_t>();
+            F.spill_mask = scap - 1;
+            launch_fold(F, slow, s);
+            CK(cudaMemcpyAsync(hs, d_pairs, 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(hs + 1, d_stats + kStOverflow, 8, cudaMemcpyDeviceToHost, s));
+            sync(c);
+            if (hs[1] == 0) break;
+            scap = pow2_at_least(2 * pair_bound);
+        }
         CK(cudaEventRecord(c->ev[3], s));
         const uint64_t n_pairs = std::min<uint64_t>(static_cast<uint32_t*>(static_cast<void*>(hs))[0], pair_bound);
 
