@@ -134,7 +134,7 @@ def generate(journeys: int, shards: int, mean_duration: float, seed: int, mod: i
     from paper_2305_07454_b200.cvlg import synth_day
     if mod == 1:
         return synth_day(seed=seed, journeys=journeys, shards=shards, mean_duration=mean_duration)
-    from paper_2305_07454_b200.cvlg import synth_day_owned
+    from paper_2305_07454_b200.distributed import synth_day_owned
     return synth_day_owned(seed=seed, journeys=journeys * mod, shards=shards,
                            mean_duration=mean_duration, mod=mod, rem=rem)
 
@@ -195,7 +195,13 @@ def run_ours(args):
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    # CVLG_FORCE_DIST=1 exercises the multi-GPU combine path on a single GPU (tests)
+    use_dist = world > 1 or os.environ.get("CVLG_FORCE_DIST") == "1"
+    if use_dist:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2305_07454_b200 as cvlg
 
@@ -216,9 +222,20 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     st = cvlg.PipelineStats()
 
+    if use_dist:
+        from paper_2305_07454_b200.distributed import run_pipeline_distributed
+        dstats: dict = {}
+
     def step():
-        cvlg.run_pipeline_device(d_csv.data_ptr(), offs, d_planes.data_ptr(), d_raw.data_ptr(),
-                                 spec, stats=st, ctx=ctx, stream=stream.cuda_stream)
+        if not use_dist:
+            cvlg.run_pipeline_device(d_csv.data_ptr(), offs, d_planes.data_ptr(), d_raw.data_ptr(),
+                                     spec, stats=st, ctx=ctx, stream=stream.cuda_stream)
+        else:
+            p, r = run_pipeline_distributed(d_csv, offs, spec, ctx=ctx, stats=dstats)
+            d_planes.copy_(p)
+            d_raw.copy_(r)
+            st.rows_read = dstats["rows_read"]
+            st.parsed = dstats["parsed"]
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -255,7 +272,29 @@ def run_ours(args):
 
     # ---- e2e through the host-buffer C ABI --------------------------------------------------------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and use_dist:
+        host = torch.from_numpy(blob).pin_memory()
+        for _ in range(max(args.warmup, 3)):
+            d_csv.copy_(host, non_blocking=True)
+            p, _r = run_pipeline_distributed(d_csv, offs, spec, ctx=ctx)
+            p.cpu()
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            d_csv.copy_(host, non_blocking=True)
+            p, r = run_pipeline_distributed(d_csv, offs, spec, ctx=ctx)
+            p.cpu()
+            r.cpu()
+        torch.cuda.synchronize()
+        e2e_ms = 1000.0 * (time.perf_counter() - t0) / args.steps
+        e_t = torch.tensor([e2e_ms], device=f"cuda:{local}")
+        dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(e_t.item())
+        e2e = {"value": total_rows / (e2e_ms / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": csv_bytes, "d2h_bytes_per_step": int(p.numel() * 4 + r.numel() * 4),
+               "ms_per_step": e2e_ms, "pinned_host": True, "note": "per-rank H2D + NCCL combine + D2H"}
+    if not args.no_e2e and not use_dist:
         cvlg.pin_host(blob)
         planes = np.empty((T, 8, R, C), dtype=np.uint32)
         raw = np.empty((T, 4, R, C), dtype=np.uint32)
@@ -348,7 +387,7 @@ def run_ours(args):
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 

@@ -129,6 +129,25 @@ int cvlg_run_pipeline_device(cvlg_context* ctx, const uint8_t* d_csv, const uint
                              const cvlg_filter_rules* rules, uint32_t* d_planes,
                              uint32_t* d_raw_count, cvlg_stats* stats, void* stream);
 
+/* ---- multi-GPU building blocks (one process per GPU; journeys sharded by FNV-1a id hash,
+ * ingest.cpp:287-301, so every journey lives on exactly one GPU) ---------------------------
+ * cvlg_partial_device runs the device-resident pipeline up to the per-(cell, journey) subtotals
+ * and keeps them in the context (n_pairs out). cvlg_export_pairs writes them to caller device
+ * buffers as (cell, key0, key1, f64 sum, u64 count) with GLOBAL journey keys (exact,
+ * order-preserving inline keys; ids longer than 15 bytes -> CVLG_E_UNSUPPORTED).
+ * cvlg_finalize_pairs folds any union of such tuples (e.g. after an all-to-all by cell owner)
+ * into a lattice: tuples are ordered by (cell, journey key) and folded exactly like the
+ * reference's finalize (aggregate.cpp:161-204); cells without tuples are zero. */
+int cvlg_partial_device(cvlg_context* ctx, const uint8_t* d_csv, const uint64_t* shard_offsets,
+                        size_t n_shards, const cvlg_grid_spec* spec, const cvlg_filter_rules* rules,
+                        uint64_t* n_pairs, cvlg_stats* stats, void* stream);
+int cvlg_export_pairs(cvlg_context* ctx, uint64_t* d_cell, uint64_t* d_key0, uint64_t* d_key1,
+                      double* d_sum, uint64_t* d_count, void* stream);
+int cvlg_finalize_pairs(cvlg_context* ctx, const uint64_t* d_cell, const uint64_t* d_key0,
+                        const uint64_t* d_key1, const double* d_sum, const uint64_t* d_count,
+                        uint64_t n, const cvlg_grid_spec* spec, uint32_t* d_planes,
+                        uint32_t* d_raw_count, void* stream);
+
 /* .cvl1 container writer (lattice_store.cpp:78-134): 58-byte header then T blocks of
  * (u32 t, planes[t]). Byte-identical to the reference for the same frames. */
 int cvlg_write_container(const uint32_t* planes, const cvlg_grid_spec* spec, int32_t day,

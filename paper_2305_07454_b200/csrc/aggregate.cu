@@ -557,6 +557,47 @@ __global__ void finalize_kernel(const uint64_t* keys, const uint32_t* vals, uint
     if (raw) raw[(t * 4 + d) * RC + rc] = static_cast<uint32_t>(cnt);
 }
 
+// ---- multi-GPU exchange: (cell, local rank) pairs <-> (cell, global journey key) tuples ------
+__global__ void rank_slot_kernel(const uint32_t* uslot, const uint32_t* perm, uint64_t n,
+                                 uint32_t* rank_slot) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) rank_slot[i] = uslot[perm[i]];
+}
+
+// Global journey key = the dictionary's exact inline key (ids <= 15 bytes): (bytes 0..7 BE,
+// bytes 8..14 BE << 8 | len) orders exactly like std::string (SURVEY §7 hard part 2).
+__global__ void export_pairs_kernel(const uint64_t* pkey, const double* psum, const uint32_t* pcnt,
+                                    uint64_t n, int rbits, const uint32_t* rank_slot,
+                                    const unsigned long long* table, uint64_t* cell, uint64_t* k0,
+                                    uint64_t* k1, double* sum, uint64_t* cnt, uint32_t* bad) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t key = pkey[i];
+    const uint64_t r = rbits ? (key & ((1ull << rbits) - 1)) : 0;
+    const uint32_t slot = rank_slot[r];
+    const uint64_t e0 = table[2 * slot], e1 = table[2 * slot + 1];
+    if ((e1 & 0xFF) == 0xFF) *bad = 1u;  // id longer than 15 bytes: no exact inline key
+    cell[i] = key >> rbits;
+    k0[i] = e0;
+    k1[i] = e1;
+    sum[i] = psum[i];
+    cnt[i] = pcnt[i];
+}
+
+__global__ void gather_u64_kernel(const uint64_t* src, const uint32_t* idx, uint64_t n,
+                                  uint64_t* dst) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) dst[i] = src[idx[i]];
+}
+
+__global__ void import_pairs_kernel(const double* sum, const uint64_t* cnt, uint64_t n,
+                                    double* psum, uint32_t* pcnt) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    psum[i] = sum[i];
+    pcnt[i] = static_cast<uint32_t>(cnt[i]);
+}
+
 inline unsigned grid_for(uint64_t n, int bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
 
 }  // namespace
@@ -663,6 +704,37 @@ void launch_fold(const FoldParams& p, bool slow, cudaStream_t s) {
         count_launch();
     }
     spill_drain_kernel<<<grid_for(p.spill_mask + 1, 256), 256, 0, s>>>(p);
+    count_launch();
+}
+
+void launch_rank_slot(const uint32_t* uslot, const uint32_t* perm, uint64_t n, uint32_t* rank_slot,
+                      cudaStream_t s) {
+    if (!n) return;
+    rank_slot_kernel<<<grid_for(n, 256), 256, 0, s>>>(uslot, perm, n, rank_slot);
+    count_launch();
+}
+
+void launch_export_pairs(const uint64_t* pkey, const double* psum, const uint32_t* pcnt, uint64_t n,
+                         int rbits, const uint32_t* rank_slot, const unsigned long long* table,
+                         uint64_t* cell, uint64_t* k0, uint64_t* k1, double* sum, uint64_t* cnt,
+                         uint32_t* bad, cudaStream_t s) {
+    if (!n) return;
+    export_pairs_kernel<<<grid_for(n, 256), 256, 0, s>>>(pkey, psum, pcnt, n, rbits, rank_slot,
+                                                         table, cell, k0, k1, sum, cnt, bad);
+    count_launch();
+}
+
+void launch_gather_u64(const uint64_t* src, const uint32_t* idx, uint64_t n, uint64_t* dst,
+                       cudaStream_t s) {
+    if (!n) return;
+    gather_u64_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, idx, n, dst);
+    count_launch();
+}
+
+void launch_import_pairs(const double* sum, const uint64_t* cnt, uint64_t n, double* psum,
+                         uint32_t* pcnt, cudaStream_t s) {
+    if (!n) return;
+    import_pairs_kernel<<<grid_for(n, 256), 256, 0, s>>>(sum, cnt, n, psum, pcnt);
     count_launch();
 }
 

@@ -201,8 +201,12 @@ struct cvlg_context {
     DevBuf dict, hdict, flags, pos, uslot, rank_of_slot, hrank, scal;
     DevBuf keys, vals, keys_alt, vals_alt, sort_tmp, scan_tmp, srank, jstart;
     DevBuf pair_key, pair_sum, pair_cnt, spill_key, spill_sum, spill_cnt;
-    DevBuf planes, raw;
+    DevBuf planes, raw, rank_slot, x_keys, x_sum, x_cnt;
     HostPinned h_small, h_csv;
+    // last cvlg_partial_device run: pairs kept in pair_key/pair_sum/pair_cnt
+    uint64_t part_pairs = 0, part_J = 0;
+    int part_rbits = 0;
+    bool part_long_ids = false;
     std::vector<cudaEvent_t> chunk_events;
     cudaEvent_t ev[6] = {};
     cudaEvent_t ev_dec0 = nullptr, ev_dec1 = nullptr;
@@ -237,7 +241,8 @@ struct Tracer {
 void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>& shard_off,
               const ColumnMap* h_cmap, const uint8_t* h_good, uint64_t bad_headers,
               const cvlg_grid_spec* spec, const cvlg_filter_rules* rules, uint32_t* d_planes,
-              uint32_t* d_raw, cvlg_stats* out_stats, const std::vector<ChunkMark>& marks) {
+              uint32_t* d_raw, cvlg_stats* out_stats, const std::vector<ChunkMark>& marks,
+              bool partial = false) {
     const Dims dims = validate_grid(spec);
     const GridParams gp = make_params(spec, rules, dims);
     cudaStream_t s = c->stream;
@@ -355,7 +360,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
 
     const uint64_t lattice_words = static_cast<uint64_t>(dims.T) * 8 * dims.RC;
     const uint64_t raw_words = static_cast<uint64_t>(dims.T) * 4 * dims.RC;
-    CK(cudaMemsetAsync(d_planes, 0, lattice_words * 4, s));
+    if (d_planes) CK(cudaMemsetAsync(d_planes, 0, lattice_words * 4, s));
     if (d_raw) CK(cudaMemsetAsync(d_raw, 0, raw_words * 4, s));
 
     bool slow = false;
@@ -433,6 +438,9 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         c->rank_of_slot.ensure(dcap * 4);
         launch_dict_rank(c->uslot.as<uint32_t>(), c->vals.as<uint32_t>(), J,
                          c->rank_of_slot.as<uint32_t>(), s);
+        c->rank_slot.ensure(J * 4 + 4);
+        launch_rank_slot(c->uslot.as<uint32_t>(), c->vals.as<uint32_t>(), J,
+                         c->rank_slot.as<uint32_t>(), s);
         c->hrank.ensure(H * 4);
         launch_head_rank(c->hdict.as<uint32_t>(), c->rank_of_slot.as<uint32_t>(), H,
                          c->hrank.as<uint32_t>(), s);
@@ -555,7 +563,12 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         CK(cudaEventRecord(c->ev[3], s));
         const uint64_t n_pairs = std::min<uint64_t>(static_cast<uint32_t*>(static_cast<void*>(hs))[0], pair_bound);
 
+        c->part_pairs = n_pairs;
+        c->part_rbits = rbits;
+        c->part_J = J;
+        c->part_long_ids = max_len > 15;
         // ---- (cell, journey) subtotals -> canonical per-cell fold ----------------------------------
+        if (!partial) {
         c->keys_alt.ensure(std::max<uint64_t>(n_pairs, sort_n) * 8);
         c->vals.ensure(std::max<uint64_t>(n_pairs, sort_n) * 4);
         c->vals_alt.ensure(std::max<uint64_t>(n_pairs, sort_n) * 4);
@@ -568,7 +581,11 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         launch_finalize(c->pair_key.as<uint64_t>(), c->vals.as<uint32_t>(), n_pairs, rbits,
                         c->pair_sum.as<double>(), c->pair_cnt.as<uint32_t>(), dims.D, dims.RC,
                         d_planes, d_raw, s);
+        }
     } else {
+        c->part_pairs = 0;
+        c->part_J = 0;
+        c->part_long_ids = false;
         CK(cudaEventRecord(c->ev[2], s));
         CK(cudaEventRecord(c->ev[3], s));
     }
@@ -783,7 +800,8 @@ void cvlg_context_destroy(cvlg_context* c) {
                       &c->flags,  &c->pos,       &c->uslot,    &c->rank_of_slot, &c->hrank,
                       &c->scal,   &c->keys,      &c->vals,     &c->keys_alt, &c->vals_alt,
                       &c->sort_tmp, &c->scan_tmp, &c->srank,   &c->jstart,   &c->pair_key,
-                      &c->pair_sum, &c->pair_cnt, &c->planes,  &c->raw};
+                      &c->pair_sum, &c->pair_cnt, &c->planes,  &c->raw, &c->rank_slot,
+                      &c->x_keys, &c->x_sum, &c->x_cnt};
     for (DevBuf* b : bufs) b->release();
     c->h_small.release();
     c->h_csv.release();
@@ -903,6 +921,105 @@ int cvlg_run_pipeline_device(cvlg_context* ctx, const uint8_t* d_csv, const uint
             throw;
         }
         c->stream = saved;
+    });
+}
+
+int cvlg_partial_device(cvlg_context* ctx, const uint8_t* d_csv, const uint64_t* shard_offsets,
+                        size_t n_shards, const cvlg_grid_spec* spec, const cvlg_filter_rules* rules,
+                        uint64_t* n_pairs, cvlg_stats* stats, void* stream) {
+    return guard([&] {
+        validate_grid(spec);
+        if (!shard_offsets || !n_pairs) fail(CVLG_E_INVALID_ARG, "NULL argument");
+        cvlg_context* c = ctx ? ctx : default_context();
+        if (!c) fail(CVLG_E_CUDA, "no CUDA context");
+        CK(cudaSetDevice(c->device));
+        std::vector<uint64_t> off(shard_offsets, shard_offsets + n_shards + 1);
+        if (off[0] != 0) fail(CVLG_E_INVALID_ARG, "shard_offsets[0] must be 0");
+        cudaStream_t saved = c->stream;
+        if (stream) c->stream = static_cast<cudaStream_t>(stream);
+        try {
+            std::vector<ChunkMark> marks{ChunkMark{off.back(), off.back(), nullptr}};
+            run_core(c, d_csv, off, nullptr, nullptr, 0, spec, rules, nullptr, nullptr, stats,
+                     marks, true);
+        } catch (...) {
+            c->stream = saved;
+            throw;
+        }
+        c->stream = saved;
+        *n_pairs = c->part_pairs;
+    });
+}
+
+int cvlg_export_pairs(cvlg_context* ctx, uint64_t* d_cell, uint64_t* d_key0, uint64_t* d_key1,
+                      double* d_sum, uint64_t* d_count, void* stream) {
+    return guard([&] {
+        cvlg_context* c = ctx ? ctx : default_context();
+        if (!c) fail(CVLG_E_CUDA, "no CUDA context");
+        CK(cudaSetDevice(c->device));
+        if (c->part_long_ids)
+            fail(CVLG_E_UNSUPPORTED,
+                 "multi-GPU combine needs journey ids <= 15 bytes (exact inline keys)");
+        const uint64_t n = c->part_pairs;
+        if (!n) return;
+        if (!d_cell || !d_key0 || !d_key1 || !d_sum || !d_count) fail(CVLG_E_INVALID_ARG, "NULL argument");
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+        uint32_t* d_bad = c->scal.as<uint32_t>() + 15;
+        CK(cudaMemsetAsync(d_bad, 0, 4, s));
+        launch_export_pairs(c->pair_key.as<uint64_t>(), c->pair_sum.as<double>(),
+                            c->pair_cnt.as<uint32_t>(), n, c->part_rbits, c->rank_slot.as<uint32_t>(),
+                            c->dict.as<unsigned long long>(), d_cell, d_key0, d_key1, d_sum, d_count,
+                            d_bad, s);
+        CK(cudaStreamSynchronize(s));
+        CK(cudaGetLastError());
+    });
+}
+
+int cvlg_finalize_pairs(cvlg_context* ctx, const uint64_t* d_cell, const uint64_t* d_key0,
+                        const uint64_t* d_key1, const double* d_sum, const uint64_t* d_count,
+                        uint64_t n, const cvlg_grid_spec* spec, uint32_t* d_planes,
+                        uint32_t* d_raw_count, void* stream) {
+    return guard([&] {
+        const Dims dims = validate_grid(spec);
+        cvlg_context* c = ctx ? ctx : default_context();
+        if (!c) fail(CVLG_E_CUDA, "no CUDA context");
+        if (!d_planes) fail(CVLG_E_INVALID_ARG, "NULL planes");
+        CK(cudaSetDevice(c->device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+        const uint64_t lattice_words = static_cast<uint64_t>(dims.T) * 8 * dims.RC;
+        const uint64_t raw_words = static_cast<uint64_t>(dims.T) * 4 * dims.RC;
+        CK(cudaMemsetAsync(d_planes, 0, lattice_words * 4, s));
+        if (d_raw_count) CK(cudaMemsetAsync(d_raw_count, 0, raw_words * 4, s));
+        if (n) {
+            c->h_small.ensure(4096);
+            c->scal.ensure(64);
+            unsigned long long* d_orand = c->scal.as<unsigned long long>() + 4;
+            unsigned long long* h_orand = reinterpret_cast<unsigned long long*>(h_small64(c) + 40);
+            c->x_keys.ensure(n * 8);
+            c->keys_alt.ensure(n * 8);
+            c->vals.ensure(n * 4);
+            c->vals_alt.ensure(n * 4);
+            c->sort_tmp.ensure(radix_temp_bytes(n));
+            c->x_sum.ensure(n * 8);
+            c->x_cnt.ensure(n * 4);
+            uint64_t* keys = c->x_keys.as<uint64_t>();
+            uint32_t* vals = c->vals.as<uint32_t>();
+            // stable LSD over (cell, key0, key1): least significant word first
+            CK(cudaMemcpyAsync(keys, d_key1, n * 8, cudaMemcpyDeviceToDevice, s));
+            launch_pair_vals(vals, n, s);
+            radix_sort_pairs(keys, vals, c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), n,
+                             0, 64, c->sort_tmp.p, s, d_orand, h_orand);
+            launch_gather_u64(d_key0, vals, n, keys, s);
+            radix_sort_pairs(keys, vals, c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), n,
+                             0, 64, c->sort_tmp.p, s, d_orand, h_orand);
+            launch_gather_u64(d_cell, vals, n, keys, s);
+            radix_sort_pairs(keys, vals, c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), n,
+                             0, bits_for(dims.cells - 1), c->sort_tmp.p, s, d_orand, h_orand);
+            launch_import_pairs(d_sum, d_count, n, c->x_sum.as<double>(), c->x_cnt.as<uint32_t>(), s);
+            launch_finalize(keys, vals, n, 0, c->x_sum.as<double>(), c->x_cnt.as<uint32_t>(), dims.D,
+                            dims.RC, d_planes, d_raw_count, s);
+        }
+        CK(cudaStreamSynchronize(s));
+        CK(cudaGetLastError());
     });
 }
 

@@ -142,10 +142,28 @@ extern "C" {
 // the total size in *offsets[n_shards] (generation runs once; results are cached per call pair
 // via the `scratch` handle). Simpler contract used here: the caller passes a capacity; returns
 // -1 if too small (with offsets[n_shards] = required bytes).
+int64_t cvlg_synth_day_owned(uint64_t seed, uint32_t n_journeys, uint32_t n_shards,
+                             double sample_period, double mean_duration, int32_t day_number,
+                             const double* bbox, uint32_t n_threads, uint32_t owner_mod,
+                             uint32_t owner_rem, uint8_t* out, uint64_t capacity,
+                             uint64_t* offsets, uint64_t* total_rows);
+
 int64_t cvlg_synth_day(uint64_t seed, uint32_t n_journeys, uint32_t n_shards, double sample_period,
                        double mean_duration, int32_t day_number, const double* bbox,
                        uint32_t n_threads, uint8_t* out, uint64_t capacity, uint64_t* offsets,
                        uint64_t* total_rows) {
+    return cvlg_synth_day_owned(seed, n_journeys, n_shards, sample_period, mean_duration,
+                                day_number, bbox, n_threads, 1, 0, out, capacity, offsets,
+                                total_rows);
+}
+
+// Same day, restricted to the journeys a multi-GPU rank owns: FNV-1a(id) % owner_mod ==
+// owner_rem (ingest.cpp:287-301). Journey j stays in shard j % n_shards.
+int64_t cvlg_synth_day_owned(uint64_t seed, uint32_t n_journeys, uint32_t n_shards,
+                             double sample_period, double mean_duration, int32_t day_number,
+                             const double* bbox, uint32_t n_threads, uint32_t owner_mod,
+                             uint32_t owner_rem, uint8_t* out, uint64_t capacity,
+                             uint64_t* offsets, uint64_t* total_rows) {
     if (n_shards == 0 || !(sample_period > 0.0) || !offsets) return -2;
     Cfg c;
     c.seed = seed;
@@ -168,6 +186,14 @@ int64_t cvlg_synth_day(uint64_t seed, uint32_t n_journeys, uint32_t n_shards, do
         pool.emplace_back([&] {
             for (uint32_t j = next.fetch_add(64); j < n_journeys; j = next.fetch_add(64))
                 for (uint32_t k = j; k < std::min(n_journeys, j + 64); ++k) {
+                    if (owner_mod > 1) {
+                        char id[24];
+                        const int n = std::snprintf(id, sizeof(id), "j%06u", k);
+                        uint64_t h = 1469598103934665603ull;
+                        for (int i = 0; i < n; ++i)
+                            h = (h ^ static_cast<unsigned char>(id[i])) * 1099511628211ull;
+                        if (h % owner_mod != owner_rem) continue;
+                    }
                     text[k].reserve(static_cast<size_t>(mean_duration / sample_period * 2.0 * 70));
                     rows[k] = gen_journey(k, c, text[k]);
                 }
