@@ -67,6 +67,7 @@ class ClockSampler:
                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, gpu_index: int, interval: float = 0.25):
+        self.disabled = os.environ.get("CVLG_NO_CLOCKS") == "1"  # diagnostics only
         self.gpu = gpu_index
         self.interval = interval
         self.samples: list[tuple[float, float, int]] = []
@@ -83,7 +84,7 @@ class ClockSampler:
             self.nvml = None
 
     def sample(self):
-        if not self.nvml:
+        if not self.nvml or self.disabled:
             return
         n = self.nvml
         try:

@@ -202,7 +202,7 @@ __global__ void head_keys_kernel(const uint32_t* hrank, const uint32_t* hslot, c
                                  uint64_t* keys, uint32_t* vals) {
     const uint64_t h = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (h >= n_heads) return;
-    const uint64_t t = static_cast<uint64_t>(ts[hslot[h]] - ts_min);
+    const uint64_t t = (static_cast<uint64_t>(ts[hslot[h]]) - static_cast<uint64_t>(ts_min));
     // mode 0: (rank << tsbits) | t ; mode 1: t only (then a second pass on rank)
     keys[h] = mode == 0 ? ((static_cast<uint64_t>(hrank[h]) << tsbits) | t) : t;
     vals[h] = static_cast<uint32_t>(h);
@@ -253,7 +253,7 @@ __global__ void slot_keys_kernel(const uint32_t* hslot, const uint32_t* hrank, u
             else hi = mid;
         }
         r = hrank[lo];
-        t = static_cast<uint64_t>(ts[i] - ts_min);
+        t = (static_cast<uint64_t>(ts[i]) - static_cast<uint64_t>(ts_min));
     }
     keys[i] = mode == 0 ? ((static_cast<uint64_t>(r) << tsbits) | t) : t;
     vals[i] = static_cast<uint32_t>(i);

@@ -14,7 +14,7 @@ constexpr int kTile = 16384;  // CSV bytes per decode tile
 constexpr int kHalo = 1024;   // bytes staged past the tile end (lines finishing in the next tile)
 constexpr int kPre = 16;      // bytes staged before the tile (previous-byte '\n' test)
 constexpr int kDecodeThreads = 256;
-constexpr int kLineCap = 512;  // data lines handled per pass over a tile
+constexpr int kLineCap = 384;  // data lines handled per pass over a tile
 
 // Slot word (one per data line): bits 0..30 = cell code (grid.cuh kCode*), bit 31 = run head.
 constexpr uint32_t kHeadBit = 0x80000000u;
@@ -69,6 +69,6 @@ struct DecodeParams {
 
 void launch_parse_headers(const uint8_t* csv, const uint64_t* shard_off, uint32_t n_shards,
                           ColumnMap* cmap, uint8_t* good, uint64_t* stats, cudaStream_t s);
-void launch_decode(const DecodeParams& p, uint32_t n_ctas, cudaStream_t s);
+void launch_decode(const DecodeParams& p, uint32_t tile_begin, uint32_t n_tiles, cudaStream_t s);
 
 }  // namespace cvlg

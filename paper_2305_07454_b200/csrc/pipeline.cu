@@ -204,7 +204,7 @@ struct cvlg_context {
     DevBuf planes, raw, rank_slot, x_keys, x_sum, x_cnt;
     HostPinned h_small, h_csv;
     // last cvlg_partial_device run: pairs kept in pair_key/pair_sum/pair_cnt
-    uint64_t part_pairs = 0, part_J = 0;
+    uint64_t part_pairs = 0, part_J = 0, last_slots = 0;
     int part_rbits = 0;
     bool part_long_ids = false;
     std::vector<cudaEvent_t> chunk_events;
@@ -287,7 +287,6 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
     P.lb.inc = c->lb_val.as<uint64_t>() + 2 * std::max<uint64_t>(n_tiles, 1);
     P.grid = gp;
     P.stats = d_stats;
-    P.ts_minmax = c->tsmm.as<long long>();
     P.aligned16 = (reinterpret_cast<uintptr_t>(d_csv) % 16) == 0;
     // A data line holds >= 30 bytes when it parses; rejects can be shorter, so the first
     // attempt may overflow on pathological inputs and is then re-run with the exact count.
@@ -328,7 +327,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
                 if (t_hi > tiles_done) {
                     P.avail_end = marks[m].avail_end;
                     P.tile_end = static_cast<uint32_t>(t_hi);
-                    launch_decode(P, static_cast<uint32_t>(t_hi - tiles_done), s);
+                    launch_decode(P, static_cast<uint32_t>(tiles_done), static_cast<uint32_t>(t_hi - tiles_done), s);
                     count_launch();
                     tiles_done = t_hi;
                 }
@@ -336,7 +335,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         } else if (n_tiles) {
             P.avail_end = total;
             P.tile_end = static_cast<uint32_t>(n_tiles);
-            launch_decode(P, static_cast<uint32_t>(n_tiles), s);
+            launch_decode(P, 0, static_cast<uint32_t>(n_tiles), s);
             count_launch();
         }
         CK(cudaEventRecord(c->ev_dec1, s));
@@ -352,10 +351,12 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         TRACE("decode done");
     if (hs[kStOverflow]) fail(CVLG_E_INTERNAL, "decode capacity invariant violated");
     const uint64_t n_parsed = hs[kStParsed];
+    c->last_slots = N;
     const uint64_t transitions = hs[kStGTransitions];
     const uint64_t H = hs[kStHeads];
-    const int64_t ts_min = static_cast<int64_t>(hs[32]);
-    const int64_t ts_max = static_cast<int64_t>(hs[33]);
+    // Order keys use the biased epoch (ts - INT64_MIN: signed order as unsigned); the radix sort
+    // skips the digits that are constant across keys, so no ts range reduction is needed.
+    const int64_t ts_min = INT64_MIN;
     if (N >= (1ull << 32) - 1) fail(CVLG_E_UNSUPPORTED, ">= 2^32-1 data lines on one device");
 
     const uint64_t lattice_words = static_cast<uint64_t>(dims.T) * 8 * dims.RC;
@@ -413,7 +414,13 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         const uint64_t max_len = hs[0];
         J = static_cast<uint32_t*>(static_cast<void*>(hs))[4];
         c->uslot.ensure(J * 4);
-        TRACE("dict compacted");
+        if (TRACE.on) {
+            char msg[256];
+            std::snprintf(msg, sizeof(msg), "dict compacted: N=%llu parsed=%llu H=%llu J=%llu trans=%llu maxlen=%llu",
+                          (unsigned long long)N, (unsigned long long)n_parsed, (unsigned long long)H,
+                          (unsigned long long)J, (unsigned long long)transitions, (unsigned long long)max_len);
+            TRACE(msg);
+        }
         launch_dict_compact(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), dcap,
                             c->uslot.as<uint32_t>(), s);
 
@@ -447,14 +454,14 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         TRACE("dict sorted");
 
         // ---- canonical order -----------------------------------------------------------------
-        const int tsbits = bits_for(static_cast<uint64_t>(ts_max - ts_min));
+        const int tsbits = 64;
         TRACE("ranks done");
         c->jstart.ensure((J + 1) * 4);
         c->srank.ensure(sort_n * 4);
         uint32_t* jstart = c->jstart.as<uint32_t>();
         {
             const int rbits = bits_for(J - 1);
-            const int mode = (tsbits + rbits <= 64) ? 0 : 1;
+            const int mode = 1;  // sort by ts, then (stably) by rank
             CK(cudaMemsetAsync(d_invalid, 0, 4, s));
             launch_head_keys(c->hrank.as<uint32_t>(), c->hslot.as<uint32_t>(), c->ts.as<int64_t>(),
                              H, ts_min, tsbits, mode, c->keys.as<uint64_t>(),
@@ -483,7 +490,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             // full (rank, ts) sort of every data line; provenance order breaks ties (stable);
             // rejected lines take rank J and sort after every journey
             const int rbits = bits_for(J);
-            const int mode = (tsbits + rbits <= 64) ? 0 : 1;
+            const int mode = 1;
             launch_slot_keys(c->hslot.as<uint32_t>(), c->hrank.as<uint32_t>(), H,
                              c->ts.as<int64_t>(), c->code.as<uint32_t>(), N, ts_min, tsbits, mode,
                              static_cast<uint32_t>(J), c->keys.as<uint64_t>(),
@@ -504,7 +511,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             set_u32_kernel<<<1, 1, 0, s>>>(jstart + J, static_cast<uint32_t>(n_parsed));
             count_launch();
         }
-        TRACE("order done");
+        TRACE(slow ? "order done (slow path)" : "order done (run-merge fast path)");
         CK(cudaEventRecord(c->ev[2], s));
 
         // ---- per-journey fold ------------------------------------------------------------------
@@ -1020,6 +1027,22 @@ int cvlg_finalize_pairs(cvlg_context* ctx, const uint64_t* d_cell, const uint64_
         }
         CK(cudaStreamSynchronize(s));
         CK(cudaGetLastError());
+    });
+}
+
+int cvlg_debug_slots(cvlg_context* ctx, int64_t* ts, double* speed, uint32_t* code, uint64_t* loff,
+                     uint64_t cap, uint64_t* n) {
+    return guard([&] {
+        cvlg_context* c = ctx ? ctx : default_context();
+        if (!c) fail(CVLG_E_CUDA, "no CUDA context");
+        CK(cudaSetDevice(c->device));
+        const uint64_t m = std::min<uint64_t>(cap, c->last_slots);
+        if (n) *n = c->last_slots;
+        if (!m) return;
+        if (ts) CK(cudaMemcpy(ts, c->ts.p, m * 8, cudaMemcpyDeviceToHost));
+        if (speed) CK(cudaMemcpy(speed, c->speed.p, m * 8, cudaMemcpyDeviceToHost));
+        if (code) CK(cudaMemcpy(code, c->code.p, m * 4, cudaMemcpyDeviceToHost));
+        if (loff) CK(cudaMemcpy(loff, c->loff.p, m * 8, cudaMemcpyDeviceToHost));
     });
 }
 
