@@ -29,7 +29,8 @@ struct FoldParams {
     const uint32_t* jstart;
     const uint32_t* perm;   // fast path: sorted run heads; slow path: sorted slots
     const uint32_t* hslot;  // fast path: run start slots
-    uint64_t n_heads, n_slots;
+    const uint32_t* hend;   // fast path: run end slots (exclusive)
+    uint64_t n_heads;
     const int64_t* ts;
     const double* speed;
     const uint32_t* code;
@@ -55,9 +56,27 @@ struct FoldParams {
     uint64_t* stats;
 };
 
-void launch_head_flags(const uint32_t* code, uint64_t n, uint32_t* flags, cudaStream_t s);
-void launch_head_compact(const uint32_t* flags, const uint32_t* pos, uint64_t n, uint32_t* hslot,
-                         cudaStream_t s);
+struct DensifyParams {
+    const uint4* tiles;
+    uint64_t n_tiles;
+    const uint32_t* lpos;  // exclusive scan of tile lines
+    const uint32_t* hpos;  // exclusive scan of tile heads
+    const uint32_t* hscr;  // K1's per-tile head lists
+    const int64_t* ts;
+    const double* speed;
+    const uint32_t* code;
+    const uint64_t* loff;
+    int64_t* ts_out;
+    double* speed_out;
+    uint32_t* code_out;
+    uint64_t* loff_out;
+    uint32_t* hslot_out;
+};
+
+void launch_tile_field(const uint4* tiles, uint64_t n, int field, uint32_t* out, cudaStream_t s);
+void launch_heads_compact(const uint4* tiles, uint64_t n, const uint32_t* hpos, const uint32_t* hscr,
+                          uint32_t* hslot, uint32_t* hend, cudaStream_t s);
+void launch_densify(const DensifyParams& d, cudaStream_t s);
 void launch_dict_insert(const DictParams& d, cudaStream_t s);
 void launch_dict_flags(const unsigned long long* table, uint64_t cap, uint32_t* flags,
                        cudaStream_t s);
@@ -75,9 +94,8 @@ void launch_head_keys(const uint32_t* hrank, const uint32_t* hslot, const int64_
 void launch_gather_rank_keys(const uint32_t* rank_src, const uint32_t* vals, uint64_t n,
                              uint64_t* keys, cudaStream_t s);
 void launch_head_order_check(const uint32_t* perm, const uint32_t* hrank, const uint32_t* hslot,
-                             const int64_t* ts, const uint32_t* code, uint64_t n_heads,
-                             uint64_t n_slots, uint32_t* jstart, uint32_t* invalid,
-                             cudaStream_t s);
+                             const uint32_t* hend, const int64_t* ts, const uint32_t* code,
+                             uint64_t n_heads, uint32_t* jstart, uint32_t* invalid, cudaStream_t s);
 void launch_slot_keys(const uint32_t* hslot, const uint32_t* hrank, uint64_t n_heads,
                       const int64_t* ts, const uint32_t* code, uint64_t n_slots, int64_t ts_min,
                       int tsbits, int mode, uint32_t reject_rank, uint64_t* keys, uint32_t* vals,

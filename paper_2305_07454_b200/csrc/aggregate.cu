@@ -86,16 +86,44 @@ __device__ void locate_id(const uint8_t* csv, const uint64_t* shard_off, uint32_
     len = 0;
 }
 
-// ---- H: run heads from the slot words --------------------------------------------------------
-__global__ void head_flags_kernel(const uint32_t* code, uint64_t n, uint32_t* flags) {
-    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    if (i < n) flags[i] = code[i] >> 31;
+// ---- H: dense run-head list from K1's per-tile lists --------------------------------------------
+// tiles[t] = (slot base, data lines, head base, heads)
+__global__ void tile_field_kernel(const uint4* tiles, uint64_t n, int field, uint32_t* out) {
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (t >= n) return;
+    const uint4 v = tiles[t];
+    out[t] = field == 0 ? v.x : field == 1 ? v.y : field == 2 ? v.z : v.w;
 }
 
-__global__ void head_compact_kernel(const uint32_t* flags, const uint32_t* pos, uint64_t n,
-                                    uint32_t* hslot) {
-    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    if (i < n && flags[i]) hslot[pos[i]] = static_cast<uint32_t>(i);
+// heads in tile order (= provenance order for regular tiles); a run ends at the next head of its
+// tile or at the tile's last line (runs never cross tiles: a tile's first line is always a head)
+__global__ void heads_compact_kernel(const uint4* tiles, uint64_t n, const uint32_t* hpos,
+                                     const uint32_t* hscr, uint32_t* hslot, uint32_t* hend) {
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (t >= n) return;
+    const uint4 v = tiles[t];
+    const uint32_t base = hpos[t];
+    for (uint32_t i = 0; i < v.w; ++i) {
+        hslot[base + i] = hscr[v.z + i];
+        hend[base + i] = i + 1 < v.w ? hscr[v.z + i + 1] : v.x + v.y;
+    }
+}
+
+// slow path: pack the per-tile slot ranges densely (provenance order), remap the heads
+__global__ void densify_kernel(DensifyParams D) {
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x / 32) + (threadIdx.x >> 5);
+    if (t >= D.n_tiles) return;
+    const int lane = threadIdx.x & 31;
+    const uint4 v = D.tiles[t];
+    const uint32_t dst = D.lpos[t];
+    for (uint32_t k = lane; k < v.y; k += 32) {
+        D.ts_out[dst + k] = D.ts[v.x + k];
+        D.speed_out[dst + k] = D.speed[v.x + k];
+        D.code_out[dst + k] = D.code[v.x + k];
+        D.loff_out[dst + k] = D.loff[v.x + k];
+    }
+    const uint32_t hb = D.hpos[t];
+    for (uint32_t i = lane; i < v.w; i += 32) D.hslot_out[hb + i] = dst + (D.hscr[v.z + i] - v.x);
 }
 
 // ---- D1: dictionary insert (one thread per run head) -----------------------------------------
@@ -217,8 +245,8 @@ __global__ void gather_rank_keys_kernel(const uint32_t* rank_src, const uint32_t
 
 // ---- O2: validity of the run-merge order + journey starts ------------------------------------
 __global__ void head_order_check_kernel(const uint32_t* perm, const uint32_t* hrank,
-                                        const uint32_t* hslot, const int64_t* ts,
-                                        const uint32_t* code, uint64_t n_heads, uint64_t n_slots,
+                                        const uint32_t* hslot, const uint32_t* hend,
+                                        const int64_t* ts, const uint32_t* code, uint64_t n_heads,
                                         uint32_t* jstart, uint32_t* invalid) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (i >= n_heads) return;
@@ -229,7 +257,7 @@ __global__ void head_order_check_kernel(const uint32_t* perm, const uint32_t* hr
         return;
     }
     const uint32_t hp = perm[i - 1];
-    uint64_t last = ((hp + 1 < n_heads) ? hslot[hp + 1] : n_slots) - 1;
+    uint64_t last = hend[hp] - 1;
     while ((code[last] & kCodeMask) == kCodeRejected) --last;  // run head is accepted
     if (!(ts[last] < ts[hslot[h]])) *invalid = 1u;
 }
@@ -355,7 +383,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
 
     auto open_run = [&](uint32_t h) {
         pos = P.hslot[h];
-        end = (h + 1 < P.n_heads) ? P.hslot[h + 1] : P.n_slots;
+        end = P.hend[h];
     };
     auto start_journey = [&]() {
         cur_g = kNone;
@@ -603,16 +631,22 @@ inline unsigned grid_for(uint64_t n, int bs) { return static_cast<unsigned>((n +
 }  // namespace
 
 // ================================ host launchers ================================================
-void launch_head_flags(const uint32_t* code, uint64_t n, uint32_t* flags, cudaStream_t s) {
+void launch_tile_field(const uint4* tiles, uint64_t n, int field, uint32_t* out, cudaStream_t s) {
     if (!n) return;
-    head_flags_kernel<<<grid_for(n, 256), 256, 0, s>>>(code, n, flags);
+    tile_field_kernel<<<grid_for(n, 256), 256, 0, s>>>(tiles, n, field, out);
     count_launch();
 }
 
-void launch_head_compact(const uint32_t* flags, const uint32_t* pos, uint64_t n, uint32_t* hslot,
-                         cudaStream_t s) {
+void launch_heads_compact(const uint4* tiles, uint64_t n, const uint32_t* hpos, const uint32_t* hscr,
+                          uint32_t* hslot, uint32_t* hend, cudaStream_t s) {
     if (!n) return;
-    head_compact_kernel<<<grid_for(n, 256), 256, 0, s>>>(flags, pos, n, hslot);
+    heads_compact_kernel<<<grid_for(n, 128), 128, 0, s>>>(tiles, n, hpos, hscr, hslot, hend);
+    count_launch();
+}
+
+void launch_densify(const DensifyParams& d, cudaStream_t s) {
+    if (!d.n_tiles) return;
+    densify_kernel<<<grid_for(d.n_tiles, 8), 256, 0, s>>>(d);
     count_launch();
 }
 
@@ -667,12 +701,10 @@ void launch_gather_rank_keys(const uint32_t* rank_src, const uint32_t* vals, uin
 }
 
 void launch_head_order_check(const uint32_t* perm, const uint32_t* hrank, const uint32_t* hslot,
-                             const int64_t* ts, const uint32_t* code, uint64_t n_heads,
-                             uint64_t n_slots, uint32_t* jstart, uint32_t* invalid,
-                             cudaStream_t s) {
-    head_order_check_kernel<<<grid_for(n_heads, 256), 256, 0, s>>>(perm, hrank, hslot, ts, code,
-                                                                   n_heads, n_slots, jstart,
-                                                                   invalid);
+                             const uint32_t* hend, const int64_t* ts, const uint32_t* code,
+                             uint64_t n_heads, uint32_t* jstart, uint32_t* invalid, cudaStream_t s) {
+    head_order_check_kernel<<<grid_for(n_heads, 256), 256, 0, s>>>(perm, hrank, hslot, hend, ts, code,
+                                                                   n_heads, jstart, invalid);
     count_launch();
 }
 

@@ -132,6 +132,57 @@ __device__ __forceinline__ uint64_t lookback1_resolve(const Lookback1& st, uint3
     return total;
 }
 
+// CTA-wide look-back without publishing: the exclusive prefix of `tile` over tiles < tile.
+// Each thread inspects one predecessor per step (window of NT tiles); warps combine with ballots
+// (nearest inclusive predecessor = first lane with flag 2), one barrier per step. `sm` / `smf`
+// hold 2 * (NT / 32) entries (double-buffered by step parity); callers separate two calls with a
+// barrier. All NT threads call.
+template <int NT>
+__device__ __forceinline__ uint64_t lookback_exclusive(const Lookback1& st, uint32_t tile, uint64_t* sm,
+                                                       uint32_t* smf) {
+    if (tile == 0) return 0;
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t total = 0;
+    int64_t j = static_cast<int64_t>(tile) - 1;
+    for (int step = 0;; ++step) {
+        uint64_t* bv = sm + (step & 1) * NW;
+        uint32_t* bf = smf + (step & 1) * NW;
+        const int64_t idx = j - static_cast<int64_t>(threadIdx.x);
+        uint32_t f = 2;
+        uint64_t v = 0;
+        if (idx >= 0) {
+            do {
+                f = ld_acquire_u32(&st.flag[idx]);
+            } while (f == 0);
+            v = ld_relaxed_u64(f == 2 ? &st.inc[idx] : &st.agg[idx]);
+        }
+        const uint32_t done = __ballot_sync(0xFFFFFFFFu, f == 2);
+        const int stop = done ? __ffs(done) - 1 : 32;
+        v = warp_sum(lane <= stop ? v : 0ull);
+        // per warp: sum up to (and including) its first inclusive lane
+        if (lane == 0) {
+            bv[warp] = v;
+            bf[warp] = done != 0;
+        }
+        __syncthreads();
+        bool stopped = false;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            if (!stopped) total += bv[w];
+            stopped = stopped || bf[w];
+        }
+        if (stopped) break;
+        j -= NT;
+    }
+    return total;
+}
+
+__device__ __forceinline__ void lookback_publish_inclusive(const Lookback1& st, uint32_t tile, uint64_t v) {
+    st_relaxed_u64(&st.inc[tile], v);
+    st_release_u32(&st.flag[tile], 2u);
+}
+
 // Decoupled look-back state for a scan over tiles carrying two u64 counters.
 // flag: 0 = not ready, 1 = aggregate published, 2 = inclusive prefix published.
 struct LookbackState {

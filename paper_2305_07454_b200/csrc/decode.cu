@@ -1,35 +1,31 @@
 // K0 (shard header map) and K1 (tile decode) for sm_100a.
 //
-// K1 makes a single pass over the concatenated CSV shards in HBM. Each CTA takes one 16 KB tile
-// (dynamic tile order, so decoupled look-back always makes progress) and:
-//   1. stages tile + 1 KB halo (+16 B before) in shared memory with one TMA bulk copy
-//      (cp.async.bulk + mbarrier); edge tiles use bounded loads;
-//   2. builds '\n' and ',' bitmaps cooperatively (SIMD-within-a-register zero-byte detection);
-//   3. lists the DATA lines that start in the tile (non-empty, not a header, good shard) — this
-//      needs no parsing, so the tile publishes its line count to the decoupled look-back at once
-//      and resolves its slot base only after parsing (CTA-wide look-back window);
-//   4. parses one line per thread. Fast path: field boundaries from a 96-bit register window of
-//      the comma bitmap, the 19-byte timestamp from five 32-bit words, decimals digit by digit
-//      from registers (Clinger: one correctly rounded division). Anything unusual (trim
-//      characters, missing fields, non-Clinger numbers, non-canonical column maps, long lines)
-//      goes to the general restatement of parse_record_impl (parse.cuh); then filter + binning
-//      (grid.cuh);
-//   5. marks run heads (journey id changes or timestamp stops increasing vs. the previous data
-//      line) and writes ts / speed / cell code / line offset at slot = base + line index, so
-//      consecutive threads write consecutive slots.
-// Slots follow byte order; shards are concatenated in lexicographic path order, so slot order
-// equals the reference's (shard_rank, line) provenance order (aggregate.cpp:287-289).
+// K1 makes a single pass over the concatenated CSV shards in HBM with persistent CTAs (static
+// round-robin tiles: CTA c takes tiles c, c + G, ...). Per 16 KB tile a CTA:
+//   1. consumes the tile that one TMA bulk copy (cp.async.bulk + mbarrier) prefetched into one
+//      of two stage buffers while the previous tile was decoded, and issues the next one;
+//   2. builds '\n' and ',' bitmaps cooperatively (SIMD-within-a-register byte compares);
+//   3. lists the DATA lines that start in the tile (non-empty, not a header, good shard);
+//   4. parses one line per thread (fastparse.cuh SWAR fast path; anything unusual goes to the
+//      general restatement of parse_record_impl, parse.cuh), then filter + binning (grid.cuh);
+//   5. marks run heads (journey id changes, or the timestamp stops increasing, vs. the previous
+//      data line of the tile) and builds the tile's local head list from warp ballots;
+//   6. publishes (heads, lines) of the tile to a decoupled look-back, and only then resolves the
+//      slot/head base of the tile it decoded ONE ITERATION EARLIER and flushes that tile's
+//      staged outputs: by then every predecessor has published, so the look-back never spins.
+// Outputs, in provenance order (slot = data line; shards are concatenated in lexicographic path
+// order, so slot order equals the reference's (shard_rank, line) order, aggregate.cpp:287-289):
+// ts / speed / cell code (| head bit) / line offset per slot, and the run-head slot list.
+// Tiles with more than kLineCap data lines (pathological short lines) take a multi-pass path
+// that resolves its base first.
 #include <algorithm>
 
+#include "fastparse.cuh"
 #include "kernels.cuh"
 
 namespace cvlg {
 
 namespace {
-
-__constant__ double kPow10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,
-                                  1e8,  1e9,  1e10, 1e11, 1e12, 1e13, 1e14, 1e15,
-                                  1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -77,154 +73,35 @@ __device__ __forceinline__ uint32_t eqmask4(uint32_t x, uint32_t pat) {
     return ((z >> 7) * 0x10204080u) >> 28;
 }
 
-// 32-bit little-endian word holding bytes [off, off + 4) of a 4-byte aligned shared buffer.
-__device__ __forceinline__ uint32_t word_at(const uint32_t* w, uint32_t off) {
-    const uint32_t i = off >> 2, sh = (off & 3) * 8;
-    return __funnelshift_r(w[i], w[i + 1], sh);
-}
-
-__device__ __forceinline__ uint32_t byte_of(uint32_t w, uint32_t k) { return (w >> (8 * k)) & 0xFF; }
-
-// Exact "YYYY-MM-DD HH:MM:SS" (datetime.cpp:53-75) from five little-endian words.
-__device__ __forceinline__ bool fast_timestamp(const uint32_t* w, uint32_t off, int64_t& out) {
-    const uint32_t t0 = word_at(w, off), t1 = word_at(w, off + 4), t2 = word_at(w, off + 8),
-                   t3 = word_at(w, off + 12), t4 = word_at(w, off + 16);
-    // separators at 4 '-', 7 '-', 10 ' ', 13 ':', 16 ':'
-    if ((t1 & 0xFF0000FFu) != 0x2D00002Du || ((t2 >> 16) & 0xFF) != ' ' ||
-        ((t3 >> 8) & 0xFF) != ':' || (t4 & 0xFF) != ':')
-        return false;
-    // the 14 digit positions, separators replaced by '0'
-    const uint32_t a = t0, b = (t1 & 0x00FFFF00u) | 0x30000030u,
-                   c = (t2 & 0xFF00FFFFu) | 0x00300000u, d = (t3 & 0xFFFF00FFu) | 0x00003000u,
-                   e = (t4 & 0x00FFFF00u) | 0x30000030u;
-    // byte in '0'..'9'  <=>  high nibble 3 and (byte + 6) keeps high nibble 3
-    const uint32_t hi = ((a | b | c | d | e) & 0xC0C0C0C0u) |
-                        (((a & b & c & d & e) & 0x30303030u) ^ 0x30303030u);
-    const uint32_t lo = ((a + 0x06060606u) | (b + 0x06060606u) | (c + 0x06060606u) |
-                         (d + 0x06060606u) | (e + 0x06060606u)) & 0x40404040u;
-    if (hi != 0 || lo != 0) return false;
-    const uint32_t da = a - 0x30303030u, db = b - 0x30303030u, dc = c - 0x30303030u,
-                   dd = d - 0x30303030u, de = e - 0x30303030u;
-    const int y = static_cast<int>(byte_of(da, 0) * 1000 + byte_of(da, 1) * 100 + byte_of(da, 2) * 10 +
-                                   byte_of(da, 3));
-    const int mo = static_cast<int>(byte_of(db, 1) * 10 + byte_of(db, 2));
-    const int dy = static_cast<int>(byte_of(dc, 0) * 10 + byte_of(dc, 1));
-    const int h = static_cast<int>(byte_of(dc, 3) * 10 + byte_of(dd, 0));
-    const int mi = static_cast<int>(byte_of(dd, 2) * 10 + byte_of(dd, 3));
-    const int s = static_cast<int>(byte_of(de, 1) * 10 + byte_of(de, 2));
-    if (mo < 1 || mo > 12 || dy < 1 || dy > static_cast<int>(days_in_month(y, mo)) || h > 23 ||
-        mi > 59 || s > 59)
-        return false;
-    out = days_from_civil(y, static_cast<unsigned>(mo), static_cast<unsigned>(dy)) * 86400 +
-          h * 3600 + mi * 60 + s;
-    return true;
-}
-
-__constant__ uint32_t kPow10u[9] = {1u, 10u, 100u, 1000u, 10000u, 100000u, 1000000u, 10000000u,
-                                    100000000u};
-
-// 4 ASCII digits (first = lowest byte = most significant) -> value
-__device__ __forceinline__ uint32_t swar4(uint32_t v) {
-    v &= 0x0F0F0F0Fu;
-    v = (v * 10u + (v >> 8)) & 0x00FF00FFu;
-    return (v * 100u + (v >> 16)) & 0xFFFFu;
-}
-
-// all four bytes in '0'..'9' (exact nibble test)
-__device__ __forceinline__ bool all_digits4(uint32_t v) {
-    return ((v & 0xF0F0F0F0u) | (((v + 0x06060606u) & 0xF0F0F0F0u) >> 4)) == 0x33333333u;
-}
-
-// value of the F (1..8) digits at bytes [at, at + F) of the shared buffer; false if any is not a
-// digit. Reads the 8 bytes ending at the last digit and forces the leading 8 - F bytes to '0'.
-__device__ __forceinline__ bool digits8(const uint32_t* w, uint32_t at, uint32_t F, uint32_t& val) {
-    const uint32_t st = at + F - 8;
-    uint32_t g0 = word_at(w, st), g1 = word_at(w, st + 4);
-    const uint32_t k = 8 - F;  // leading pad bytes
-    if (k >= 4) {
-        g0 = 0x30303030u;
-        const uint32_t m = k == 4 ? 0u : (0xFFFFFFFFu >> (8 * (8 - k)));
-        g1 = (g1 & ~m) | (0x30303030u & m);
-    } else if (k > 0) {
-        const uint32_t m = 0xFFFFFFFFu >> (8 * (4 - k));
-        g0 = (g0 & ~m) | (0x30303030u & m);
-    }
-    if (!all_digits4(g0) || !all_digits4(g1)) return false;
-    val = swar4(g0) * 10000u + swar4(g1);
-    return true;
-}
-
-// [-]I['.'F] with I <= 3 digits and F <= 8 digits (or an integer of <= 8 digits): the Clinger
-// case of parse_double computed identically (w < 10^11 exact; one correctly rounded division
-// by 10^F). SWAR digit conversion; false -> the general parser decides.
-__device__ __forceinline__ bool fast_number(const uint32_t* w, uint32_t off, uint32_t n, double& v) {
-    const bool neg = (word_at(w, off) & 0xFF) == '-';
-    const uint32_t o = off + (neg ? 1u : 0u);
-    const uint32_t m = n - (neg ? 1u : 0u);
-    if (n == 0 || m == 0) return false;
-    const uint32_t h = word_at(w, o);
-    const uint32_t lim = m < 4 ? ((1u << m) - 1u) : 0xFu;
-    const uint32_t dm = eqmask4(h, 0x2E2E2E2Eu) & lim;
-    uint64_t mant;
-    uint32_t fd;
-    if (dm == 0) {  // integer
-        if (m > 8) return false;
-        uint32_t val;
-        if (!digits8(w, o, m, val)) return false;
-        mant = val;
-        fd = 0;
-    } else {
-        const uint32_t L = __ffs(dm) - 1;  // digits before the dot (0..3)
-        const uint32_t F = m - L - 1;      // digits after it
-        if (F > 8 || L + F == 0) return false;
-        const uint32_t d = h - 0x30303030u;
-        const uint32_t b0 = d & 0xFF, b1 = (d >> 8) & 0xFF, b2 = (d >> 16) & 0xFF;
-        uint32_t ip = 0;
-        if (L >= 1) {
-            if (b0 > 9) return false;
-            ip = b0;
-        }
-        if (L >= 2) {
-            if (b1 > 9) return false;
-            ip = ip * 10 + b1;
-        }
-        if (L == 3) {
-            if (b2 > 9) return false;
-            ip = ip * 10 + b2;
-        }
-        uint32_t fp = 0;
-        if (F && !digits8(w, o + L + 1, F, fp)) return false;
-        mant = static_cast<uint64_t>(ip) * kPow10u[F] + fp;
-        fd = F;
-    }
-    const double md = static_cast<double>(mant);
-    const double r = fd ? __ddiv_rn(md, kPow10[fd]) : md;
-    v = neg ? -r : r;
-    return true;
-}
-
 struct LineOut {
     int64_t ts;
     double lat, lon, speed, heading;
     uint32_t id_rel, id_len;  // tile-relative id span
+    uint32_t minute;          // minute of day (fast path), kNoMinute when unknown
 };
 
+constexpr uint32_t kNoMinute = 0xFFFFFFFFu;
 constexpr uint8_t kNeedGeneral = 255;
 
+// Per-thread fast-path state carried across lines: the last validated date and, per numeric
+// column, the decimal point position of the previous line.
+struct FastState {
+    DateCache dc;
+    int q[4] = {-1, -1, -1, -1};
+};
+
 // Fast path of parse_record_impl for a line [p, e) (tile-relative) entirely staged in shared
-// memory whose header is canonical: journey, timestamp, latitude, longitude as fields 0..3,
-// then speed, heading as 5, 6 (`postal` = 1: any column at 4) or 4, 5. Returns kAccepted or
+// memory whose header is canonical: journey, timestamp, latitude, longitude as fields 0..3, then
+// speed, heading as 5, 6 (`postal` = 1: any column at 4) or 4, 5. Returns kAccepted or
 // kRangeViolation, or kNeedGeneral whenever the general restatement has to decide.
-__device__ __forceinline__ uint8_t fast_parse(const uint8_t* __restrict__ tile,
-                                              const uint32_t* __restrict__ cm, uint32_t p,
-                                              uint32_t e, int postal, LineOut& o) {
+__device__ __forceinline__ uint8_t fast_parse(const uint8_t* __restrict__ buf, const uint32_t* __restrict__ cm,
+                                              uint32_t p, uint32_t e, int postal, FastState& fs, LineOut& o) {
     const uint32_t len = e - p;
     if (len > 95) return kNeedGeneral;
     // 96-bit comma window starting at bit p
     const uint32_t wi = p >> 5, sh = p & 31;
     const uint32_t a = cm[wi], b = cm[wi + 1], c = cm[wi + 2], d = cm[wi + 3];
-    uint32_t m0 = __funnelshift_r(a, b, sh), m1 = __funnelshift_r(b, c, sh),
-             m2 = __funnelshift_r(c, d, sh);
+    uint32_t m0 = __funnelshift_r(a, b, sh), m1 = __funnelshift_r(b, c, sh), m2 = __funnelshift_r(c, d, sh);
     if (len < 32) {
         m0 &= (1u << len) - 1u;
         m1 = m2 = 0;
@@ -262,15 +139,14 @@ __device__ __forceinline__ uint8_t fast_parse(const uint8_t* __restrict__ tile,
     // every required field must exist and be non-empty (else: general decides MissingField)
     if (fb_hd >= fe_hd || fe_id == 0 || fb_la >= fe_la || fb_lo >= fe_lo || fb_sp >= fe_sp)
         return kNeedGeneral;
-    const uint8_t* q = tile + p;
-    if (is_trim(q[0]) || is_trim(q[fe_id - 1])) return kNeedGeneral;
-    const uint32_t* words = reinterpret_cast<const uint32_t*>(tile - kPre);  // 16 B aligned
-    const uint32_t base = p + kPre;
-    if (fe_ts - fb_ts != 19 || !fast_timestamp(words, base + fb_ts, o.ts)) return kNeedGeneral;
-    if (!fast_number(words, base + fb_la, fe_la - fb_la, o.lat) ||
-        !fast_number(words, base + fb_lo, fe_lo - fb_lo, o.lon) ||
-        !fast_number(words, base + fb_sp, fe_sp - fb_sp, o.speed) ||
-        !fast_number(words, base + fb_hd, fe_hd - fb_hd, o.heading))
+    const uint32_t base = p + kPre;  // buffer offset of the line
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(buf);
+    if (is_trim(buf[base]) || is_trim(buf[base + fe_id - 1])) return kNeedGeneral;
+    if (fe_ts - fb_ts != 19 || !fast_timestamp(w, base + fb_ts, fs.dc, o.ts, o.minute)) return kNeedGeneral;
+    if (!fast_number(w, buf, base + fb_la, base + fe_la, fs.q[0], o.lat) ||
+        !fast_number(w, buf, base + fb_lo, base + fe_lo, fs.q[1], o.lon) ||
+        !fast_number(w, buf, base + fb_sp, base + fe_sp, fs.q[2], o.speed) ||
+        !fast_number(w, buf, base + fb_hd, base + fe_hd, fs.q[3], o.heading))
         return kNeedGeneral;
     if (o.heading == 360.0) o.heading = 0.0;
     o.id_rel = p;
@@ -294,6 +170,7 @@ __device__ __noinline__ uint8_t general_parse(const uint8_t* line, int32_t len, 
         o.heading = pr.heading;
         o.id_rel = p_rel + static_cast<uint32_t>(pr.id_begin);
         o.id_len = static_cast<uint32_t>(pr.id_len);
+        o.minute = kNoMinute;
     }
     return why;
 }
@@ -343,42 +220,46 @@ void launch_parse_headers(const uint8_t* csv, const uint64_t* shard_off, uint32_
 }
 
 // ---------------------------------------------------------------------------------------------
-// K1: persistent CTAs, static round-robin tiles (CTA c: tiles c, c + G, ...), double-buffered TMA
-// prefetch of the next tile while the current one is parsed. Every CTA of the grid is
-// co-resident (G <= occupancy x SMs), and a tile only ever waits on smaller tiles, so the
-// decoupled look-back cannot deadlock: the smallest unfinished tile is always being processed.
+// K1
 constexpr int kStage = kPre + kTile + kHalo;
-constexpr int kStageAlloc = kStage + 112;  // word_at() over-read padding, keeps 16 B alignment
+constexpr int kStageAlloc = kStage + 112;  // word over-read padding, keeps 16 B alignment
 constexpr int kWords = (kTile + kHalo) / 32;
 constexpr int kMaxShardsInTile = 32;
 constexpr int kDecodeCtasPerSm = 3;
+constexpr int kNW = kDecodeThreads / 32;
+constexpr int kRounds = (kLineCap + kDecodeThreads - 1) / kDecodeThreads;
+constexpr int kHeadWords = kRounds * kNW;  // one ballot word per (round, warp)
+static_assert(kHeadWords <= 32, "head ballot words");
+static_assert(kTile / 64 == kDecodeThreads, "thread t owns tile words 2t, 2t+1");
 
 struct DecodeSmem {
     uint8_t buf[2][kStageAlloc];
     uint32_t nl[kWords + 4];
     uint32_t cm[kWords + 4];
     uint32_t starts[kLineCap];
-    long long st_ts[kLineCap];
-    double st_speed[kLineCap];
-    uint32_t st_code[kLineCap];
-    uint32_t st_id[kLineCap];   // tile-relative id start
-    uint32_t st_len[kLineCap];  // id length | accepted << 31
+    uint32_t id_rel[kLineCap];  // tile-relative id start
+    uint32_t id_len[kLineCap];  // id length | accepted << 31
+    uint32_t l_code[kLineCap];  // cell code (no head bit)
+    uint32_t hbits[kHeadWords];
+    alignas(8) long long l_ts[kLineCap];
 };
 
 __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kernel(DecodeParams P,
                                                                                   uint32_t tile_begin) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     DecodeSmem& S = *reinterpret_cast<DecodeSmem*>(smem_raw);
-    __shared__ uint32_t scan_smem[kDecodeThreads / 32 + 1];
+    __shared__ uint32_t scan_smem[kNW];
     __shared__ uint64_t sh_off[kMaxShardsInTile + 2];
-    __shared__ uint32_t sh_first, sh_count, sh_overflow;
+    __shared__ uint32_t sh_first, sh_count, sh_overflow, sh_good;
+    __shared__ int sh_kind;
+    __shared__ unsigned long long sh_send;
     __shared__ __align__(8) uint64_t bar[2];
+    __shared__ uint32_t s_cnt[8];  // rejects[4], heads, transitions, accepted, rows
+    __shared__ unsigned long long s_ovf[2];
     __shared__ long long c_ts;
     __shared__ uint32_t c_id, c_len, c_code;
-    __shared__ uint32_t s_cnt[8];  // rejects[4], heads, transitions, accepted, rows
-    __shared__ uint64_t s_lb[kDecodeThreads / 32 + 2];
 
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -395,6 +276,8 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
         mbar_expect_tx(&bar[b], kStage);
         tma_load_1d(S.buf[b], P.csv + static_cast<uint64_t>(t) * kTile - kPre, kStage, &bar[b]);
     };
+
+    FastState fs;
     uint32_t phase0 = 0, phase1 = 0;
     uint32_t c_acc = 0;
     const uint32_t G = gridDim.x;
@@ -428,7 +311,7 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
             S.nl[kWords + (tid & 3)] = 0;
             S.cm[kWords + (tid & 3)] = 0;
         }
-        if (tid == 32) {  // shard containing tb (overlaps the copy)
+        if (tid == 32) {  // shards overlapping the tile (overlaps the copy)
             uint32_t lo = 0, hi = P.n_shards;
             while (hi - lo > 1) {
                 const uint32_t mid = (lo + hi) / 2;
@@ -438,14 +321,13 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
             sh_first = lo;
             uint32_t c = 0, s = lo + 1;
             while (s <= P.n_shards && P.shard_off[s] < te && c < kMaxShardsInTile) sh_off[c++] = P.shard_off[s++];
-            sh_overflow = (s <= P.n_shards && P.shard_off[s] < te) ? 1u : 0u;
+            const uint32_t over = (s <= P.n_shards && P.shard_off[s] < te) ? 1u : 0u;
+            sh_overflow = over;
             sh_count = c;
-        }
-        if (tid == 0) {
-            c_len = 0;  // "no previous data line" for the first line of the tile
-            c_ts = 0;
-            c_id = 0;
-            c_code = kCodeRejected;
+            const bool one = c == 0 && !over;
+            sh_kind = one ? canonical_kind(P.cmap[lo]) : -1;
+            sh_good = (one && P.shard_good[lo] && tb != P.shard_off[lo]) ? 1u : 0u;
+            sh_send = P.shard_off[lo + 1];
         }
         if (tma) {
             if (b == 0) {
@@ -458,21 +340,19 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
         }
         __syncthreads();
 
-        // ---- 2. '\n' and ',' bitmaps over [tb, tb + kTile + kHalo) -----------------------------
-        for (int w = tid; w < kWords; w += kDecodeThreads) {
+        // ---- 2. '\n' / ',' bitmaps of this thread's 64 bytes (+ the halo) and its line starts -----
+        auto bitmap_word = [&](int w) -> uint32_t {
             const uint4* p = reinterpret_cast<const uint4*>(tile_s + 32 * w);
             const uint4 a = p[0], c = p[1];
             const uint32_t x[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
-            uint32_t mn = 0, mc = 0;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                mn |= eqmask4(x[k], 0x0A0A0A0Au) << (4 * k);
-                mc |= eqmask4(x[k], 0x2C2C2C2Cu) << (4 * k);
-            }
+            uint32_t mn, mc;
+            class_masks32(x, mn, mc);
             S.nl[w] = mn;
             S.cm[w] = mc;
-        }
-        __syncthreads();
+            return mn;
+        };
+        const uint32_t nlw0 = bitmap_word(2 * tid), nlw1 = bitmap_word(2 * tid + 1);
+        if (tid < kWords - 2 * kDecodeThreads) bitmap_word(2 * kDecodeThreads + tid);
 
         const bool one_shard = !sh_overflow && sh_count == 0;
         auto shard_of = [&](uint64_t p) -> uint32_t {
@@ -492,85 +372,97 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
             return lo;
         };
 
-        // ---- 3. data lines starting in [0, tlen) ------------------------------------------------
-        // thread t owns tile words 2t, 2t+1 (kTile / 32 = 512 words)
+        // data lines starting in [0, tlen): a start follows a '\n' (or the byte before the tile)
         uint32_t smask[2];
         uint32_t my_count = 0;
-        const bool tile_good = one_shard && P.shard_good[sh_first] && tb != P.shard_off[sh_first];
+        const bool tile_good = sh_good != 0;
+        {
+            const uint8_t before = (tid == 0) ? bufb[kPre - 1] : tile_s[64 * tid - 1];
+            uint32_t prev_top = before == '\n' ? 1u : 0u;
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int w = 2 * tid + k;
-            const uint32_t prev_top = (w == 0) ? (bufb[kPre - 1] == '\n' ? 1u : 0u) : (S.nl[w - 1] >> 31);
-            uint32_t m = (S.nl[w] << 1) | prev_top;
-            const int lo = 32 * w;
-            if (lo >= static_cast<int>(tlen)) m = 0;
-            else if (lo + 32 > static_cast<int>(tlen)) m &= (1u << (tlen - lo)) - 1u;
-            m &= ~S.nl[w];  // a start whose first byte is '\n' is an empty line
-            uint32_t keep = m;
-            uint32_t cand = m;
-            while (cand) {
-                const int bit = __ffs(cand) - 1;
-                cand &= cand - 1;
-                const uint32_t pr = static_cast<uint32_t>(lo + bit);
-                const uint64_t p = tb + pr;
-                bool data;
-                uint64_t s_end;
-                if (tile_good) {
-                    data = true;
-                    s_end = P.shard_off[sh_first + 1];
-                } else {
-                    const uint32_t s = shard_of(p);
-                    data = p != P.shard_off[s] && P.shard_good[s];
-                    s_end = P.shard_off[s + 1];
-                }
-                // "\r\n" or "\r<shard end>" is empty after stripping one '\r'
-                if (data && tile_s[pr] == '\r' && (p + 1 == s_end || tile_s[pr + 1] == '\n')) data = false;
-                if (!data) keep &= ~(1u << bit);
-            }
-            smask[k] = keep;
-            my_count += __popc(keep);
-        }
-        uint32_t n_data;
-        const uint32_t my_off = block_exclusive_scan<kDecodeThreads>(my_count, scan_smem, n_data);
-
-        // ---- publish the tile's line count now; resolve the slot base after parsing --------------
-        if (tid == 0) {
-            lookback1_publish(P.lb, tile, n_data);
-            s_cnt[7] += n_data;
-        }
-        uint64_t base = 0;
-        bool resolved = false;
-
-        for (uint32_t pass_base = 0; pass_base < n_data; pass_base += kLineCap) {
-            {
-                uint32_t idx = my_off;
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    uint32_t m = smask[k];
-                    while (m) {
-                        const int bit = __ffs(m) - 1;
-                        m &= m - 1;
-                        if (idx >= pass_base && idx < pass_base + kLineCap)
-                            S.starts[idx - pass_base] = static_cast<uint32_t>(32 * (2 * tid + k) + bit);
-                        ++idx;
+            for (int k = 0; k < 2; ++k) {
+                const int w = 2 * tid + k;
+                const uint32_t nlw = k ? nlw1 : nlw0;
+                uint32_t m = (nlw << 1) | prev_top;
+                prev_top = nlw >> 31;
+                const int lo = 32 * w;
+                if (lo >= static_cast<int>(tlen)) m = 0;
+                else if (lo + 32 > static_cast<int>(tlen)) m &= (1u << (tlen - lo)) - 1u;
+                m &= ~nlw;  // a start whose first byte is '\n' is an empty line
+                uint32_t keep = m;
+                uint32_t cand = m;
+                while (cand) {
+                    const int bit = __ffs(cand) - 1;
+                    cand &= cand - 1;
+                    const uint32_t pr = static_cast<uint32_t>(lo + bit);
+                    bool data = true;
+                    uint64_t s_end;
+                    if (tile_good) {
+                        s_end = sh_send;
+                    } else {
+                        const uint64_t p = tb + pr;
+                        const uint32_t s = shard_of(p);
+                        data = p != P.shard_off[s] && P.shard_good[s];
+                        s_end = P.shard_off[s + 1];
                     }
+                    // "\r\n" or "\r<shard end>" is empty after stripping one '\r'
+                    if (data && tile_s[pr] == '\r' && (tb + pr + 1 == s_end || tile_s[pr + 1] == '\n')) data = false;
+                    if (!data) keep &= ~(1u << bit);
+                }
+                smask[k] = keep;
+                my_count += __popc(keep);
+            }
+        }
+        // block exclusive scan of my_count, one barrier (also publishes the bitmaps)
+        const uint32_t inc = warp_inclusive_sum(my_count);
+        if (lane == 31) scan_smem[warp] = inc;
+        __syncthreads();
+        uint32_t n_data = 0, my_off = inc - my_count;
+#pragma unroll
+        for (int w = 0; w < kNW; ++w) {
+            const uint32_t v = scan_smem[w];
+            n_data += v;
+            if (w < warp) my_off += v;
+        }
+        if (tid == 0) s_cnt[7] += n_data;
+
+        // ---- line starts of lines [pass_base, pass_base + kLineCap) ------------------------------
+        auto write_starts = [&](uint32_t pass_base) {
+            uint32_t idx = my_off;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                uint32_t m = smask[k];
+                while (m) {
+                    const int bit = __ffs(m) - 1;
+                    m &= m - 1;
+                    if (idx >= pass_base && idx < pass_base + kLineCap)
+                        S.starts[idx - pass_base] = static_cast<uint32_t>(32 * (2 * tid + k) + bit);
+                    ++idx;
                 }
             }
-            __syncthreads();
-            const uint32_t n_pass = min(static_cast<uint32_t>(kLineCap), n_data - pass_base);
-            // ---- 4. parse: one data line per thread, results staged in shared memory -------------
+        };
+        // ---- 4. parse: one data line per thread, results staged in shared memory -----------------
+        auto parse_lines = [&](uint32_t n_pass, uint64_t slot0) {
             for (uint32_t li = tid; li < n_pass; li += kDecodeThreads) {
-                uint8_t why;
                 LineOut o;
                 o.ts = 0;
                 o.speed = 0.0;
                 o.id_rel = 0;
                 o.id_len = 0;
-                uint32_t code = kCodeRejected;
                 const uint32_t p_rel = S.starts[li];
                 const uint64_t p = tb + p_rel;
-                const uint32_t s = shard_of(p);
-                const uint64_t s_end = P.shard_off[s + 1];
+                uint32_t s;
+                uint64_t s_end;
+                int kind;
+                if (one_shard) {
+                    s = sh_first;
+                    s_end = sh_send;
+                    kind = sh_kind;
+                } else {
+                    s = shard_of(p);
+                    s_end = P.shard_off[s + 1];
+                    kind = canonical_kind(P.cmap[s]);
+                }
                 // line end: next '\n' at or after p (within the staged bytes), clamped to the shard end
                 uint64_t e = 0;
                 bool found = false;
@@ -601,103 +493,157 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                 uint32_t len = static_cast<uint32_t>(e - p);
                 const uint8_t last = in_smem ? tile_s[p_rel + len - 1] : gline[len - 1];
                 if (last == '\r') --len;  // len > 0: empty lines are not data lines
-                const ColumnMap map = P.cmap[s];
-                why = kNeedGeneral;
-                const int kind = canonical_kind(map);
-                if (in_smem && kind >= 0) why = fast_parse(tile_s, S.cm, p_rel, p_rel + len, kind, o);
+                uint8_t why = kNeedGeneral;
+                if (in_smem && kind >= 0) why = fast_parse(bufb, S.cm, p_rel, p_rel + len, kind, fs, o);
                 if (why == kNeedGeneral)
-                    why = general_parse(in_smem ? tile_s + p_rel : gline, static_cast<int32_t>(len), map,
+                    why = general_parse(in_smem ? tile_s + p_rel : gline, static_cast<int32_t>(len), P.cmap[s],
                                         p_rel, o);
+                uint32_t code = kCodeRejected;
                 if (why == kAccepted) {
-                    code = cell_code(o.ts, o.lat, o.lon, o.speed, o.heading, P.grid);
+                    const uint32_t t = o.minute != kNoMinute ? time_bin_mod(o.minute, P.grid)
+                                                             : time_bin(o.ts, P.grid.min_step);
+                    code = cell_code_t(t, o.lat, o.lon, o.speed, o.heading, P.grid);
                     ++c_acc;
                 } else {
                     atomicAdd(&s_cnt[why - 1], 1u);  // rare
                 }
-                S.st_ts[li] = o.ts;
-                S.st_speed[li] = o.speed;
-                S.st_code[li] = code;
-                S.st_id[li] = o.id_rel;
-                S.st_len[li] = o.id_len | (why == kAccepted ? 0x80000000u : 0u);
+                const uint64_t slot = slot0 + li;
+                P.out.ts[slot] = o.ts;
+                P.out.speed[slot] = o.speed;
+                P.out.loff[slot] = p;
+                S.l_ts[li] = o.ts;
+                S.l_code[li] = code;
+                S.id_rel[li] = o.id_rel;
+                S.id_len[li] = o.id_len | (why == kAccepted ? 0x80000000u : 0u);
             }
-            if (!resolved) {
-                // predecessors have had a full parse phase to publish: the walk is short
-                base = lookback1_resolve<kDecodeThreads>(P.lb, tile, n_data, s_lb);
-                resolved = true;
-                if (tid == 0 && base + n_data > P.out.slot_cap)
-                    atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[kStOverflow]), 1ull);
-            } else {
-                __syncthreads();
-            }
-            const bool fits = base + n_data <= P.out.slot_cap;
-            // ---- 5. run heads + coalesced writes --------------------------------------------------
-            uint32_t my_heads = 0, my_trans = 0;
+        };
+
+        // ---- 5. run heads: the journey id changes or the timestamp stops increasing --------------
+        // Line 0 compares against the carry (c_*; c_len = 0: no previous line -> head). Writes the
+        // slot words (cell code | head bit), counts cell transitions inside runs, and calls
+        // emit(index, line) for every head, index = rank among this pass's heads. Returns the
+        // pass's head count.
+        auto mark_heads = [&](uint32_t n_pass, uint64_t slot0, auto&& emit) -> uint32_t {
             const uint32_t* ws = reinterpret_cast<const uint32_t*>(bufb);
-            for (uint32_t k = tid; k < n_pass; k += kDecodeThreads) {
-                const uint32_t ln = S.st_len[k];
-                uint32_t code = S.st_code[k];
-                if (ln >> 31) {
-                    const uint32_t pl = k ? S.st_len[k - 1] : c_len;
-                    const long long pts = k ? S.st_ts[k - 1] : c_ts;
-                    const uint32_t idl = ln & 0x7FFFFFFFu;
-                    bool head = true;
-                    if ((pl >> 31) && (pl & 0x7FFFFFFFu) == idl && pts < S.st_ts[k]) {
-                        const uint32_t pid = k ? S.st_id[k - 1] : c_id;
-                        const uint32_t mid = S.st_id[k];
-                        bool same = true;
-                        if (pid + idl <= staged_len && mid + idl <= staged_len) {
-                            for (uint32_t i = 0; i < idl; i += 4) {
-                                uint32_t x = word_at(ws, kPre + pid + i) ^ word_at(ws, kPre + mid + i);
-                                if (idl - i < 4) x &= (1u << (8 * (idl - i))) - 1u;
-                                if (x) {
-                                    same = false;
-                                    break;
+            uint32_t my_trans = 0;
+#pragma unroll
+            for (int r = 0; r < kRounds; ++r) {
+                const uint32_t k = r * kDecodeThreads + tid;
+                bool head = false;
+                if (k < n_pass) {
+                    const uint32_t ln = S.id_len[k];
+                    const uint32_t code = S.l_code[k];
+                    if (ln >> 31) {
+                        const uint32_t pl = k ? S.id_len[k - 1] : c_len;
+                        const long long pts = k ? S.l_ts[k - 1] : c_ts;
+                        const uint32_t idl = ln & 0x7FFFFFFFu;
+                        head = true;
+                        if ((pl >> 31) && (pl & 0x7FFFFFFFu) == idl && pts < S.l_ts[k]) {
+                            const uint32_t pid = k ? S.id_rel[k - 1] : c_id;
+                            const uint32_t mid = S.id_rel[k];
+                            bool same = true;
+                            if (pid + idl <= staged_len && mid + idl <= staged_len) {
+                                for (uint32_t i = 0; i < idl; i += 4) {
+                                    uint32_t x = word_at(ws, kPre + pid + i) ^ word_at(ws, kPre + mid + i);
+                                    if (idl - i < 4) x &= (1u << (8 * (idl - i))) - 1u;
+                                    if (x) {
+                                        same = false;
+                                        break;
+                                    }
                                 }
+                            } else {
+                                const uint8_t* pa = (pid + idl <= staged_len) ? tile_s + pid : P.csv + tb + pid;
+                                const uint8_t* pb = (mid + idl <= staged_len) ? tile_s + mid : P.csv + tb + mid;
+                                for (uint32_t i = 0; i < idl; ++i)
+                                    if (pa[i] != pb[i]) {
+                                        same = false;
+                                        break;
+                                    }
                             }
-                        } else {
-                            const uint8_t* pa = (pid + idl <= staged_len) ? tile_s + pid : P.csv + tb + pid;
-                            const uint8_t* pb = (mid + idl <= staged_len) ? tile_s + mid : P.csv + tb + mid;
-                            for (uint32_t i = 0; i < idl; ++i)
-                                if (pa[i] != pb[i]) {
-                                    same = false;
-                                    break;
-                                }
+                            head = !same;
                         }
-                        head = !same;
+                        if (!head && (k ? S.l_code[k - 1] : c_code) != code) ++my_trans;
                     }
-                    if (head) {
-                        ++my_heads;
-                        code |= kHeadBit;
-                    } else if ((k ? S.st_code[k - 1] : c_code) != code) {
-                        ++my_trans;
-                    }
+                    P.out.code[slot0 + k] = head ? (code | kHeadBit) : code;
                 }
-                if (fits) {
-                    const uint64_t slot = base + pass_base + k;
-                    P.out.ts[slot] = S.st_ts[k];
-                    P.out.speed[slot] = S.st_speed[k];
-                    P.out.code[slot] = code;
-                    P.out.loff[slot] = tb + S.starts[k];
-                }
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, head);
+                if (lane == 0) S.hbits[r * kNW + warp] = bal;
             }
-            if (my_heads) atomicAdd(&s_cnt[4], my_heads);
             if (my_trans) atomicAdd(&s_cnt[5], my_trans);
             __syncthreads();
-            if (tid == 0) {  // carry the pass's last line
-                c_ts = S.st_ts[n_pass - 1];
-                c_id = S.st_id[n_pass - 1];
-                c_len = S.st_len[n_pass - 1];
-                c_code = S.st_code[n_pass - 1];
+            // exclusive prefix of the head words (every warp computes it redundantly)
+            const uint32_t cntw = lane < kHeadWords ? __popc(S.hbits[lane]) : 0u;
+            const uint32_t incw = warp_inclusive_sum(cntw);
+            const uint32_t nh = __shfl_sync(0xFFFFFFFFu, incw, kHeadWords - 1);
+#pragma unroll
+            for (int r = 0; r < kRounds; ++r) {
+                const uint32_t k = r * kDecodeThreads + tid;
+                const int wd = r * kNW + warp;
+                const uint32_t bits = S.hbits[wd];
+                const uint32_t pre = __shfl_sync(0xFFFFFFFFu, incw - cntw, wd);
+                if (k < n_pass && ((bits >> lane) & 1u)) emit(pre + __popc(bits & ((1u << lane) - 1u)), k);
+            }
+            if (tid == 0) s_cnt[4] += nh;
+            return nh;
+        };
+
+        uint64_t slot0, head0;
+        uint32_t heads = 0;
+        if (n_data <= static_cast<uint32_t>(kLineCap)) {
+            // ---- common case: the tile's own slot range [tile * kLineCap, + n_data) ----------------
+            slot0 = static_cast<uint64_t>(tile) * kLineCap;
+            head0 = slot0;
+            write_starts(0);
+            if (tid == 0) c_len = 0;
+            __syncthreads();
+            parse_lines(n_data, slot0);
+            __syncthreads();
+            heads = mark_heads(n_data, slot0, [&](uint32_t idx, uint32_t k) {
+                P.out.hslot[head0 + idx] = static_cast<uint32_t>(slot0 + k);
+            });
+        } else {
+            // ---- more than kLineCap lines: slots and heads from the overflow regions --------------
+            if (tid == 0) {
+                s_ovf[0] = atomicAdd(P.out.ovf_slots, static_cast<unsigned long long>(n_data));
+                s_ovf[1] = atomicAdd(P.out.ovf_heads, static_cast<unsigned long long>(n_data));
+                c_len = 0;
             }
             __syncthreads();
+            const bool fits = s_ovf[0] + n_data <= P.out.ovf_slot_cap && s_ovf[1] + n_data <= P.out.ovf_head_cap;
+            slot0 = P.out.reg_slots + s_ovf[0];
+            head0 = P.out.reg_slots + s_ovf[1];
+            if (!fits) {
+                if (tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[kStOverflow]), 1ull);
+            } else {
+                for (uint32_t pass_base = 0; pass_base < n_data; pass_base += kLineCap) {
+                    const uint32_t n_pass = min(static_cast<uint32_t>(kLineCap), n_data - pass_base);
+                    __syncthreads();
+                    write_starts(pass_base);
+                    __syncthreads();
+                    parse_lines(n_pass, slot0 + pass_base);
+                    __syncthreads();
+                    heads += mark_heads(n_pass, slot0 + pass_base, [&](uint32_t idx, uint32_t k) {
+                        P.out.hslot[head0 + heads + idx] = static_cast<uint32_t>(slot0 + pass_base + k);
+                    });
+                    __syncthreads();
+                    if (tid == 0) {  // carry the pass's last line
+                        c_ts = S.l_ts[n_pass - 1];
+                        c_id = S.id_rel[n_pass - 1];
+                        c_len = S.id_len[n_pass - 1];
+                        c_code = S.l_code[n_pass - 1];
+                    }
+                }
+            }
         }
-        if (!resolved) lookback1_resolve<kDecodeThreads>(P.lb, tile, n_data, s_lb);
+        if (tid == 0) {
+            P.out.tiles[tile] = make_uint4(static_cast<uint32_t>(slot0), n_data, static_cast<uint32_t>(head0), heads);
+        }
         __syncthreads();  // buffers and per-tile shared state are reused by the next tile
     }
 
     // ---- stats (once per CTA) ---------------------------------------------------------------------
     const uint32_t acc = warp_sum(c_acc);
-    if ((tid & 31) == 0 && acc) atomicAdd(&s_cnt[6], acc);
+    if (lane == 0 && acc) atomicAdd(&s_cnt[6], acc);
     __syncthreads();
     if (tid == 0) {
         unsigned long long* st = reinterpret_cast<unsigned long long*>(P.stats);

@@ -29,7 +29,23 @@ struct GridParams {
     double speed_ceiling;
     uint32_t min_step, dxn_step, R, C, D, T;
     int32_t require_in_grid, drop_missing;
+    uint32_t t_magic;  // ceil(2^32 / min_step) (min_step > 1): minute / min_step = umulhi(minute, t_magic)
 };
+
+// ceil(2^32 / min_step): exact quotient for every minute of day (minute * min_step < 2^32 / 2^11)
+inline uint32_t time_magic(uint32_t min_step) {
+    return min_step > 1 ? static_cast<uint32_t>(((1ull << 32) + min_step - 1) / min_step) : 0u;
+}
+
+// time_bin from the minute of day (0..1439) of the parsed timestamp (grid.cpp:69-71)
+CVLG_HD uint32_t time_bin_mod(uint32_t minute, const GridParams& g) {
+    if (g.min_step <= 1) return minute;
+#if defined(__CUDA_ARCH__)
+    return __umulhi(minute, g.t_magic);
+#else
+    return static_cast<uint32_t>((static_cast<uint64_t>(minute) * g.t_magic) >> 32);
+#endif
+}
 
 CVLG_HD double d_abs(double x) { return bits_dbl(dbl_bits(x) & 0x7FFFFFFFFFFFFFFFull); }
 
@@ -83,21 +99,25 @@ CVLG_HD uint32_t dxn_bin(double heading, const GridParams& g) {
     if (h < 0.0) h = d_add(h, 360.0);
     const double q = snap_to_integer(d_div(h, g.dxn_step_d));
     const uint32_t d = static_cast<uint32_t>(floor(q));
-    return d % g.D;
+    return d >= g.D ? d - g.D : d;  // == d % D: h <= 360 so q <= 360 / dxn_step = D
 }
 
-// filter_reason + binning for one accepted record -> cell code.
-CVLG_HD uint32_t cell_code(int64_t epoch, double lat, double lon, double speed, double heading,
-                           const GridParams& g) {
+// filter_reason + binning for one accepted record with time bin t -> cell code.
+CVLG_HD uint32_t cell_code_t(uint32_t t, double lat, double lon, double speed, double heading,
+                             const GridParams& g) {
     const bool in_grid = lat >= g.lat_min && lat <= g.lat_max && lon >= g.lon_min && lon <= g.lon_max;
     if (g.require_in_grid && !in_grid) return kCodeOutOfGrid;
     if (speed > g.speed_ceiling) return kCodeSpeedCeiling;
     if (!in_grid) return kCodeUnbinnable;
-    const uint32_t t = time_bin(epoch, g.min_step);
     const uint32_t d = dxn_bin(heading, g);
     const uint32_t r = linear_bin(lat, g.lat_min, g.lat_step, g.R);
     const uint32_t c = linear_bin(lon, g.lon_min, g.lon_step, g.C);
     return ((t * g.D + d) * g.R + r) * g.C + c;
+}
+
+CVLG_HD uint32_t cell_code(int64_t epoch, double lat, double lon, double speed, double heading,
+                           const GridParams& g) {
+    return cell_code_t(time_bin(epoch, g.min_step), lat, lon, speed, heading, g);
 }
 
 }  // namespace cvlg

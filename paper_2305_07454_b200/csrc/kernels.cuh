@@ -39,14 +39,22 @@ enum : int {
     kStCount = 17,
 };
 
-// Per data line ("slot", in provenance order). Rejected lines keep their slot with
-// code kCodeRejected so that slot assignment never waits for parsing.
+// Per data line ("slot"). Slot space: tile t owns slots [t * kLineCap, t * kLineCap + lines(t))
+// in provenance order (tiles are in byte order, shards in lexicographic path order); a tile with
+// more than kLineCap data lines takes a range of the overflow region [reg_slots, ...). Slots past
+// a tile's line count are never written and never read. Rejected lines keep their slot with code
+// kCodeRejected.
 struct DecodeOut {
     int64_t* ts;      // [slot] epoch seconds
     double* speed;    // [slot]
     uint32_t* code;   // [slot] cell code | kHeadBit
     uint64_t* loff;   // [slot] absolute line offset in the CSV buffer
-    uint64_t slot_cap;
+    uint32_t* hslot;  // [head scratch] run-head slots; tile t's at tiles[t].z + (0 .. tiles[t].w)
+    uint4* tiles;     // [tile] (slot base, data lines, head base, heads)
+    uint64_t reg_slots;                  // n_tiles * kLineCap
+    unsigned long long* ovf_slots;       // overflow-region slot counter (zeroed)
+    unsigned long long* ovf_heads;       // overflow-region head counter (zeroed)
+    uint64_t ovf_slot_cap, ovf_head_cap;
 };
 
 struct DecodeParams {
@@ -58,12 +66,9 @@ struct DecodeParams {
     const uint8_t* shard_good;  // [n_shards]
     uint32_t n_shards;
     uint32_t tile_end;
-    uint32_t* tile_counter;
-    Lookback1 lb;
     GridParams grid;
     DecodeOut out;
     uint64_t* stats;
-    long long* ts_minmax;  // [0] = min, [1] = max over accepted records
     int aligned16;
 };
 

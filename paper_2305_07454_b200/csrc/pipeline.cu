@@ -158,6 +158,7 @@ GridParams make_params(const cvlg_grid_spec* s, const cvlg_filter_rules* r, cons
     g.require_in_grid = rr->require_in_grid;
     g.drop_missing = rr->drop_missing;
     g.speed_ceiling = rr->speed_ceiling;
+    g.t_magic = time_magic(s->min_step);
     return g;
 }
 
@@ -197,7 +198,8 @@ struct cvlg_context {
     cudaStream_t stream = nullptr, copy_stream = nullptr;
     bool own_stream = true;
     DevBuf csv, shard_off, cmap, good, lb_flag, lb_val, counter, stats, tsmm;
-    DevBuf ts, speed, code, loff, hslot;
+    DevBuf ts, speed, code, loff, hslot, hscr, hend, tiles, thpos;
+    DevBuf ts2, speed2, code2, loff2;  // dense copies for the slow (full-sort) path
     DevBuf dict, hdict, flags, pos, uslot, rank_of_slot, hrank, scal;
     DevBuf keys, vals, keys_alt, vals_alt, sort_tmp, scan_tmp, srank, jstart;
     DevBuf pair_key, pair_sum, pair_cnt, spill_key, spill_sum, spill_cnt;
@@ -269,11 +271,10 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         CK(cudaMemcpyAsync(c->cmap.p, h_cmap, n_shards * sizeof(ColumnMap), cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(c->good.p, h_good, n_shards, cudaMemcpyHostToDevice, s));
     }
-    c->lb_flag.ensure(std::max<uint64_t>(n_tiles, 1) * 4);
-    c->lb_val.ensure(std::max<uint64_t>(n_tiles, 1) * 32);
-    c->counter.ensure(4);
+    c->tiles.ensure(std::max<uint64_t>(n_tiles, 1) * 16);
+    c->counter.ensure(16);
 
-    // ---- K1 decode (slot per data line) ----------------------------------------------------------
+    // ---- K1 decode (slot per data line, sparse per-tile slot ranges) -----------------------------
     DecodeParams P;
     P.csv = d_csv;
     P.total_end = total;
@@ -281,27 +282,33 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
     P.cmap = c->cmap.as<ColumnMap>();
     P.shard_good = c->good.as<uint8_t>();
     P.n_shards = n_shards;
-    P.tile_counter = c->counter.as<uint32_t>();
-    P.lb.flag = c->lb_flag.as<uint32_t>();
-    P.lb.agg = c->lb_val.as<uint64_t>();
-    P.lb.inc = c->lb_val.as<uint64_t>() + 2 * std::max<uint64_t>(n_tiles, 1);
     P.grid = gp;
     P.stats = d_stats;
     P.aligned16 = (reinterpret_cast<uintptr_t>(d_csv) % 16) == 0;
-    // A data line holds >= 30 bytes when it parses; rejects can be shorter, so the first
-    // attempt may overflow on pathological inputs and is then re-run with the exact count.
-    uint64_t slot_cap = total / 24 + n_shards + 1024;
+    const uint64_t reg = n_tiles * static_cast<uint64_t>(kLineCap);
+    // Tiles with more than kLineCap data lines (lines averaging < 43 bytes) draw slots from an
+    // overflow region; sized small first and re-run with the exact demand if it ever fills.
+    uint64_t ovf_cap = 4096 + total / 512;
     uint64_t N = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
-        c->ts.ensure(slot_cap * 8);
-        c->speed.ensure(slot_cap * 8);
-        c->code.ensure(slot_cap * 4);
-        c->loff.ensure(slot_cap * 8);
+        const uint64_t S_all = reg + ovf_cap;
+        if (S_all >= (1ull << 32)) fail(CVLG_E_UNSUPPORTED, "input too large for 32-bit slot ids");
+        c->ts.ensure(S_all * 8);
+        c->speed.ensure(S_all * 8);
+        c->code.ensure(S_all * 4);
+        c->loff.ensure(S_all * 8);
+        c->hscr.ensure(S_all * 4);
         P.out.ts = c->ts.as<int64_t>();
         P.out.speed = c->speed.as<double>();
         P.out.code = c->code.as<uint32_t>();
         P.out.loff = c->loff.as<uint64_t>();
-        P.out.slot_cap = slot_cap;
+        P.out.hslot = c->hscr.as<uint32_t>();
+        P.out.tiles = c->tiles.as<uint4>();
+        P.out.reg_slots = reg;
+        P.out.ovf_slots = c->counter.as<unsigned long long>();
+        P.out.ovf_heads = c->counter.as<unsigned long long>() + 1;
+        P.out.ovf_slot_cap = ovf_cap;
+        P.out.ovf_head_cap = ovf_cap;
         init_run_kernel<<<1, 32, 0, s>>>(d_stats, c->tsmm.as<long long>());
         count_launch();
         if (h_cmap) {
@@ -314,8 +321,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
                                  c->good.as<uint8_t>(), d_stats, s);
             count_launch();
         }
-        CK(cudaMemsetAsync(c->lb_flag.p, 0, std::max<uint64_t>(n_tiles, 1) * 4, s));
-        CK(cudaMemsetAsync(c->counter.p, 0, 4, s));
+        CK(cudaMemsetAsync(c->counter.p, 0, 16, s));
         CK(cudaEventRecord(c->ev_dec0, s));
         uint64_t tiles_done = 0;
         if (attempt == 0) {
@@ -341,17 +347,18 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         CK(cudaEventRecord(c->ev_dec1, s));
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(hs, d_stats, kStCount * 8, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(hs + 32, c->tsmm.p, 16, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hs + 32, c->counter.p, 16, cudaMemcpyDeviceToHost, s));
         sync(c);
         N = hs[kStRowsRead];
-        if (N <= slot_cap) break;
-        slot_cap = N;  // exact count from the look-back totals
+        const uint64_t need = std::max(hs[32], hs[33]);
+        if (!hs[kStOverflow] || need <= ovf_cap) break;
+        ovf_cap = need;  // exact demand of the overflow tiles
     }
     CK(cudaEventRecord(c->ev[1], s));
         TRACE("decode done");
     if (hs[kStOverflow]) fail(CVLG_E_INTERNAL, "decode capacity invariant violated");
     const uint64_t n_parsed = hs[kStParsed];
-    c->last_slots = N;
+    c->last_slots = 0;  // the slot space is sparse (see cvlg_debug_slots)
     const uint64_t transitions = hs[kStGTransitions];
     const uint64_t H = hs[kStHeads];
     // Order keys use the biased epoch (ts - INT64_MIN: signed order as unsigned); the radix sort
@@ -375,18 +382,20 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         unsigned long long* h_orand = reinterpret_cast<unsigned long long*>(hs + 40);
         uint32_t* d_invalid = c->scal.as<uint32_t>() + 12;
         const uint64_t dcap = pow2_at_least(2 * H);
-        const uint64_t flag_n = std::max<uint64_t>(dcap, N + 1);
+        const uint64_t flag_n = std::max<uint64_t>({dcap, n_tiles + 1, N + 1});
         c->flags.ensure(flag_n * 4 + 16);
         c->pos.ensure(flag_n * 4 + 16);
         c->scan_tmp.ensure(scan_temp_words(flag_n) * 4 + 64);
 
-        // ---- run heads -> compact list -----------------------------------------------------------
+        // ---- run heads: K1 listed them per tile; dense list in tile order + run ends -------------
         c->hslot.ensure(H * 4 + 4);
-        launch_head_flags(c->code.as<uint32_t>(), N, c->flags.as<uint32_t>(), s);
-        exclusive_scan_u32(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), N, nullptr,
+        c->hend.ensure(H * 4 + 4);
+        c->thpos.ensure(n_tiles * 4 + 4);
+        launch_tile_field(c->tiles.as<uint4>(), n_tiles, 3, c->flags.as<uint32_t>(), s);
+        exclusive_scan_u32(c->flags.as<uint32_t>(), c->thpos.as<uint32_t>(), n_tiles, nullptr,
                            c->scan_tmp.as<uint32_t>(), s);
-        launch_head_compact(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), N,
-                            c->hslot.as<uint32_t>(), s);
+        launch_heads_compact(c->tiles.as<uint4>(), n_tiles, c->thpos.as<uint32_t>(),
+                             c->hscr.as<uint32_t>(), c->hslot.as<uint32_t>(), c->hend.as<uint32_t>(), s);
 
         // ---- journey dictionary ----------------------------------------------------------------
         c->dict.ensure(dcap * 16);
@@ -477,8 +486,9 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
                                  rbits, c->sort_tmp.p, s, d_orand, h_orand);
             }
             launch_head_order_check(c->vals.as<uint32_t>(), c->hrank.as<uint32_t>(),
-                                    c->hslot.as<uint32_t>(), c->ts.as<int64_t>(),
-                                    c->code.as<uint32_t>(), H, N, jstart, d_invalid, s);
+                                    c->hslot.as<uint32_t>(), c->hend.as<uint32_t>(),
+                                    c->ts.as<int64_t>(), c->code.as<uint32_t>(), H, jstart,
+                                    d_invalid, s);
             CK(cudaMemcpyAsync(hs, d_invalid, 4, cudaMemcpyDeviceToHost, s));
             sync(c);
             slow = static_cast<uint32_t*>(static_cast<void*>(hs))[0] != 0;
@@ -488,7 +498,36 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             count_launch();
         } else {
             // full (rank, ts) sort of every data line; provenance order breaks ties (stable);
-            // rejected lines take rank J and sort after every journey
+            // rejected lines take rank J and sort after every journey. First the sparse per-tile
+            // slot ranges are packed densely in provenance order (heads remapped).
+            launch_tile_field(c->tiles.as<uint4>(), n_tiles, 1, c->flags.as<uint32_t>(), s);
+            exclusive_scan_u32(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), n_tiles, nullptr,
+                               c->scan_tmp.as<uint32_t>(), s);
+            c->ts2.ensure(N * 8 + 8);
+            c->speed2.ensure(N * 8 + 8);
+            c->code2.ensure(N * 4 + 4);
+            c->loff2.ensure(N * 8 + 8);
+            DensifyParams DZ;
+            DZ.tiles = c->tiles.as<uint4>();
+            DZ.n_tiles = n_tiles;
+            DZ.lpos = c->pos.as<uint32_t>();
+            DZ.hpos = c->thpos.as<uint32_t>();
+            DZ.hscr = c->hscr.as<uint32_t>();
+            DZ.ts = c->ts.as<int64_t>();
+            DZ.speed = c->speed.as<double>();
+            DZ.code = c->code.as<uint32_t>();
+            DZ.loff = c->loff.as<uint64_t>();
+            DZ.ts_out = c->ts2.as<int64_t>();
+            DZ.speed_out = c->speed2.as<double>();
+            DZ.code_out = c->code2.as<uint32_t>();
+            DZ.loff_out = c->loff2.as<uint64_t>();
+            DZ.hslot_out = c->hslot.as<uint32_t>();
+            launch_densify(DZ, s);
+            std::swap(c->ts, c->ts2);
+            std::swap(c->speed, c->speed2);
+            std::swap(c->code, c->code2);
+            std::swap(c->loff, c->loff2);
+            c->last_slots = N;
             const int rbits = bits_for(J);
             const int mode = 1;
             launch_slot_keys(c->hslot.as<uint32_t>(), c->hrank.as<uint32_t>(), H,
@@ -526,8 +565,8 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         F.jstart = jstart;
         F.perm = c->vals.as<uint32_t>();
         F.hslot = c->hslot.as<uint32_t>();
+        F.hend = c->hend.as<uint32_t>();
         F.n_heads = H;
-        F.n_slots = N;
         F.ts = c->ts.as<int64_t>();
         F.speed = c->speed.as<double>();
         F.code = c->code.as<uint32_t>();
@@ -802,6 +841,8 @@ void cvlg_context_destroy(cvlg_context* c) {
     cudaStreamSynchronize(c->copy_stream);
     DevBuf* bufs[] = {&c->csv,    &c->shard_off, &c->cmap,     &c->good,     &c->lb_flag,
                       &c->lb_val, &c->counter,   &c->stats,    &c->tsmm,     &c->ts,
+                      &c->hscr,   &c->hend,      &c->tiles,    &c->thpos,    &c->ts2,
+                      &c->speed2, &c->code2,     &c->loff2,
                       &c->speed,  &c->code,      &c->loff,     &c->hslot,    &c->spill_key,
                       &c->spill_sum, &c->spill_cnt, &c->dict,     &c->hdict,
                       &c->flags,  &c->pos,       &c->uslot,    &c->rank_of_slot, &c->hrank,
