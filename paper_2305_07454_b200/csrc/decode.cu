@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
 
     FastState fs;
     uint32_t phase0 = 0, phase1 = 0;
-    uint32_t c_acc = 0;
+    uint32_t c_acc = 0, c_inert = 0;
     const uint32_t G = gridDim.x;
     uint32_t tile = tile_begin + blockIdx.x;
     if (tid == 0 && tile < P.tile_end && can_tma(tile)) issue(tile, 0);
@@ -389,25 +389,17 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                 if (lo >= static_cast<int>(tlen)) m = 0;
                 else if (lo + 32 > static_cast<int>(tlen)) m &= (1u << (tlen - lo)) - 1u;
                 m &= ~nlw;  // a start whose first byte is '\n' is an empty line
+                // ("\r\n" lines are empty too: they keep a slot but are made inert in parse_lines)
                 uint32_t keep = m;
-                uint32_t cand = m;
-                while (cand) {
-                    const int bit = __ffs(cand) - 1;
-                    cand &= cand - 1;
-                    const uint32_t pr = static_cast<uint32_t>(lo + bit);
-                    bool data = true;
-                    uint64_t s_end;
-                    if (tile_good) {
-                        s_end = sh_send;
-                    } else {
-                        const uint64_t p = tb + pr;
+                if (!tile_good) {
+                    uint32_t cand = m;
+                    while (cand) {
+                        const int bit = __ffs(cand) - 1;
+                        cand &= cand - 1;
+                        const uint64_t p = tb + static_cast<uint32_t>(lo + bit);
                         const uint32_t s = shard_of(p);
-                        data = p != P.shard_off[s] && P.shard_good[s];
-                        s_end = P.shard_off[s + 1];
+                        if (p == P.shard_off[s] || !P.shard_good[s]) keep &= ~(1u << bit);
                     }
-                    // "\r\n" or "\r<shard end>" is empty after stripping one '\r'
-                    if (data && tile_s[pr] == '\r' && (tb + pr + 1 == s_end || tile_s[pr + 1] == '\n')) data = false;
-                    if (!data) keep &= ~(1u << bit);
                 }
                 smask[k] = keep;
                 my_count += __popc(keep);
@@ -417,12 +409,17 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
         const uint32_t inc = warp_inclusive_sum(my_count);
         if (lane == 31) scan_smem[warp] = inc;
         __syncthreads();
-        uint32_t n_data = 0, my_off = inc - my_count;
+        uint32_t n_data, my_off;
+        {
+            const uint32_t wv = lane < kNW ? scan_smem[lane] : 0u;
+            uint32_t wi = wv;
 #pragma unroll
-        for (int w = 0; w < kNW; ++w) {
-            const uint32_t v = scan_smem[w];
-            n_data += v;
-            if (w < warp) my_off += v;
+            for (int o = 1; o < kNW; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+                if (lane >= o) wi += t;
+            }
+            n_data = __shfl_sync(0xFFFFFFFFu, wi, kNW - 1);
+            my_off = inc - my_count + __shfl_sync(0xFFFFFFFFu, wi - wv, warp);
         }
         if (tid == 0) s_cnt[7] += n_data;
 
@@ -463,23 +460,36 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                     s_end = P.shard_off[s + 1];
                     kind = canonical_kind(P.cmap[s]);
                 }
-                // line end: next '\n' at or after p (within the staged bytes), clamped to the shard end
+                // line end: next '\n' at or after p (within the staged bytes), clamped to the shard end;
+                // a 96-bit window of the newline bitmap covers every line of <= 95 bytes
                 uint64_t e = 0;
                 bool found = false;
                 {
-                    uint32_t w = p_rel >> 5;
-                    uint32_t m = S.nl[w] & (0xFFFFFFFFu << (p_rel & 31));
-                    while (true) {
-                        if (m) {
-                            const uint32_t x = 32 * w + (__ffs(m) - 1);
-                            if (x < staged_len) {
-                                e = tb + x;
-                                found = true;
-                            }
-                            break;
+                    const uint32_t w = p_rel >> 5, sh = p_rel & 31;
+                    const uint32_t n0 = S.nl[w], n1 = S.nl[w + 1], n2 = S.nl[w + 2], n3 = S.nl[w + 3];
+                    const uint32_t m0 = __funnelshift_r(n0, n1, sh), m1 = __funnelshift_r(n1, n2, sh),
+                                   m2 = __funnelshift_r(n2, n3, sh);
+                    uint32_t x = 0xFFFFFFFFu;
+                    if (m0) x = p_rel + __ffs(m0) - 1;
+                    else if (m1) x = p_rel + 31 + __ffs(m1);
+                    else if (m2) x = p_rel + 63 + __ffs(m2);
+                    if (x != 0xFFFFFFFFu) {
+                        if (x < staged_len) {
+                            e = tb + x;
+                            found = true;
                         }
-                        if (++w >= static_cast<uint32_t>(kWords) || 32 * w >= staged_len) break;
-                        m = S.nl[w];
+                    } else {
+                        for (uint32_t v = w + 3; v < static_cast<uint32_t>(kWords) && 32 * v < staged_len; ++v) {
+                            const uint32_t mm = S.nl[v];
+                            if (mm) {
+                                const uint32_t y = 32 * v + (__ffs(mm) - 1);
+                                if (y < staged_len) {
+                                    e = tb + y;
+                                    found = true;
+                                }
+                                break;
+                            }
+                        }
                     }
                 }
                 if (!found) {
@@ -492,7 +502,19 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                 const uint8_t* gline = P.csv + p;
                 uint32_t len = static_cast<uint32_t>(e - p);
                 const uint8_t last = in_smem ? tile_s[p_rel + len - 1] : gline[len - 1];
-                if (last == '\r') --len;  // len > 0: empty lines are not data lines
+                if (last == '\r') --len;
+                if (len == 0) {  // "\r\n" / "\r<shard end>": empty, not a data line (inert slot)
+                    ++c_inert;
+                    const uint64_t slot = slot0 + li;
+                    P.out.ts[slot] = 0;
+                    P.out.speed[slot] = 0.0;
+                    P.out.loff[slot] = p;
+                    S.l_ts[li] = 0;
+                    S.l_code[li] = kCodeRejected;
+                    S.id_rel[li] = 0;
+                    S.id_len[li] = 0;
+                    continue;
+                }
                 uint8_t why = kNeedGeneral;
                 if (in_smem && kind >= 0) why = fast_parse(bufb, S.cm, p_rel, p_rel + len, kind, fs, o);
                 if (why == kNeedGeneral)
@@ -642,8 +664,11 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
     }
 
     // ---- stats (once per CTA) ---------------------------------------------------------------------
-    const uint32_t acc = warp_sum(c_acc);
+    const uint32_t acc = warp_sum(c_acc), inert = warp_sum(c_inert);
     if (lane == 0 && acc) atomicAdd(&s_cnt[6], acc);
+    if (lane == 0 && inert) atomicSub(&s_cnt[7], inert);
+    if (lane == 0 && inert)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[kStInert]), static_cast<unsigned long long>(inert));
     __syncthreads();
     if (tid == 0) {
         unsigned long long* st = reinterpret_cast<unsigned long long*>(P.stats);

@@ -36,6 +36,14 @@ CVLG_HD uint32_t fs_rc(uint32_t lo, uint32_t hi, uint32_t sh) {  // (hi:lo >> mi
     return static_cast<uint32_t>(((static_cast<uint64_t>(hi) << 32) | lo) >> sh);
 #endif
 }
+CVLG_HD uint32_t fs_l(uint32_t lo, uint32_t hi, uint32_t sh) {  // high word of (hi:lo << (sh & 31))
+#if defined(__CUDA_ARCH__)
+    return __funnelshift_l(lo, hi, sh);
+#else
+    sh &= 31;
+    return static_cast<uint32_t>((((static_cast<uint64_t>(hi) << 32) | lo) << sh) >> 32);
+#endif
+}
 CVLG_HD int clz32(uint32_t x) {
 #if defined(__CUDA_ARCH__)
     return __clz(x);
@@ -127,12 +135,13 @@ CVLG_HD double div_pow10(double x, int k) {
 }
 
 // std::from_chars(double) on field [b, e) (buffer offsets, kPre bytes of readable padding before
-// the first field). `qguess` carries the point position of this column from the previous line.
-// Branch-free after the checks: a 12-byte window right-aligned at e, bytes before the digits
-// forced to '0'; the point at window position q is dropped by moving the bytes after it down one
-// position ('0' enters at 11), so the 12 digits read V = 10 * M for the decimal M * 10^-F
-// (F = 11 - q) and the value is V / 10^(12 - q), correctly rounded (Markstein, div_pow10).
-// Without a point q is taken as 12: nothing moves and V is divided by 10^0 = 1.
+// the first field) for [-]digits[.digits] of at most 12 bytes. `qguess` carries the point
+// position (in the 12-byte window right-aligned at e) of this column from the previous line.
+//   short path (<= 8 digits, point in the last 8 bytes): bytes up to the point move up one
+//     position over it, so the last two words hold the digits M right-aligned; x = M / 10^F.
+//   long path (<= 11 digits): bytes after the point move down one position ('0' enters at 11),
+//     so the three words read V = 10 M; x = V / 10^(F+1). Without a point nothing moves.
+// Both divide an exact integer by an exact power of ten with correct rounding (div_pow10).
 CVLG_HD bool fast_number(const uint32_t* w, const uint8_t* buf, uint32_t b, uint32_t e, int& qguess,
                          double& v) {
     const uint32_t n = e - b;
@@ -140,28 +149,45 @@ CVLG_HD bool fast_number(const uint32_t* w, const uint8_t* buf, uint32_t b, uint
     const bool neg = buf[b] == '-';
     const uint32_t o = e - 12, i = o >> 2, sh = (o & 3) * 8;
     const uint32_t x0 = w[i], x1 = w[i + 1], x2 = w[i + 2], x3 = w[i + 3];
-    const int s = 12 - static_cast<int>(n) + (neg ? 1 : 0);  // first digit position
-    uint32_t r0 = keep_from(fs_r(x0, x1, sh), s);
-    uint32_t r1 = keep_from(fs_r(x1, x2, sh), s - 4);
-    uint32_t r2 = keep_from(fs_r(x2, x3, sh), s - 8);
+    const uint32_t a0 = fs_r(x0, x1, sh), a1 = fs_r(x1, x2, sh), a2 = fs_r(x2, x3, sh);
+    const int s = 12 - static_cast<int>(n) + (neg ? 1 : 0);  // first byte after the sign
     int q = qguess;
-    const bool hit = q >= 4 && (((q < 8 ? r1 : r2) >> (8 * (q & 3))) & 0xFF) == '.';
-    if (!hit) {
-        const uint32_t z1 = eqflags(r1, 0x2E2E2E2Eu), z2 = eqflags(r2, 0x2E2E2E2Eu);
+    const bool hit = q >= s && q >= 4 && (((q < 8 ? a1 : a2) >> (8 * (q & 3))) & 0xFF) == '.';
+    if (!hit) {  // rightmost point among the field's bytes in the last 8 (else -1)
+        const uint32_t z1 = eqflags(a1, 0x2E2E2E2Eu) & bytes_from_rt(s - 4);
+        const uint32_t z2 = eqflags(a2, 0x2E2E2E2Eu) & bytes_from_rt(s - 8);
         q = z2 ? 8 + ((31 - clz32(z2)) >> 3) : (z1 ? 4 + ((31 - clz32(z1)) >> 3) : -1);
         qguess = q;
     }
-    if (static_cast<int>(n) - (neg ? 1 : 0) - (q >= 0 ? 1 : 0) <= 0) return false;  // no digit
+    const int D = static_cast<int>(n) - (neg ? 1 : 0) - (q >= 0 ? 1 : 0);  // digits (if one point)
+    if (D <= 0) return false;
+    if (D <= 8) {
+        uint32_t r1 = a1, r2 = a2;
+        if (q >= 0) {  // bytes at positions <= q take the byte below them
+            const uint32_t s1 = fs_l(a0, a1, 8), s2 = fs_l(a1, a2, 8);
+            const uint32_t m1 = bytes_from_rt(q - 3), m2 = bytes_from_rt(q - 7);  // positions > q
+            r1 = (a1 & m1) | (s1 & ~m1);
+            r2 = (a2 & m2) | (s2 & ~m2);
+        }
+        r1 = keep_from(r1, 8 - D);  // digits occupy [12 - D, 12)
+        r2 = keep_from(r2, 4 - D);
+        if (!digits3(r1, r2, 0x30303030u)) return false;
+        const double x = div_pow10(static_cast<double>(swar4(r1) * 10000u + swar4(r2)), q >= 0 ? 11 - q : 0);
+        v = neg ? -x : x;
+        return true;
+    }
+    const uint32_t r0 = keep_from(a0, s);
+    uint32_t r1 = keep_from(a1, s - 4);
+    uint32_t r2 = keep_from(a2, s - 8);
     const int qe = q < 0 ? 12 : q;  // (a point before byte 4 stays in place and fails below)
     const uint32_t s0 = fs_r(r0, r1, 8), s1 = fs_r(r1, r2, 8), s2 = (r2 >> 8) | 0x30000000u;
     const uint32_t m0 = bytes_from_rt(qe), m1 = bytes_from_rt(qe - 4), m2 = bytes_from_rt(qe - 8);
-    r0 = (s0 & m0) | (r0 & ~m0);
+    const uint32_t t0 = (s0 & m0) | (r0 & ~m0);
     r1 = (s1 & m1) | (r1 & ~m1);
     r2 = (s2 & m2) | (r2 & ~m2);
-    if (!digits3(r0, r1, r2)) return false;
-    const uint64_t V = static_cast<uint64_t>(swar4(r0)) * 100000000ull + (swar4(r1) * 10000u + swar4(r2));
-    const double d = static_cast<double>(V);  // exact: V < 10^12
-    const double x = div_pow10(d, 12 - qe);
+    if (!digits3(t0, r1, r2)) return false;
+    const uint64_t V = static_cast<uint64_t>(swar4(t0)) * 100000000ull + (swar4(r1) * 10000u + swar4(r2));
+    const double x = div_pow10(static_cast<double>(V), 12 - qe);  // V exact: < 10^12
     v = neg ? -x : x;
     return true;
 }

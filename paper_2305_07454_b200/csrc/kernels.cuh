@@ -36,7 +36,8 @@ enum : int {
     kStUnbinnable = 14,    // kept records that would throw OutOfBounds
     kStOverflow = 15,      // capacity overflow (hash tables / slot arrays)
     kStHeads = 16,
-    kStCount = 17,
+    kStInert = 17,         // "\r\n" lines: hold a slot, are not data lines
+    kStCount = 18,
 };
 
 // Per data line ("slot"). Slot space: tile t owns slots [t * kLineCap, t * kLineCap + lines(t))

@@ -358,6 +358,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         TRACE("decode done");
     if (hs[kStOverflow]) fail(CVLG_E_INTERNAL, "decode capacity invariant violated");
     const uint64_t n_parsed = hs[kStParsed];
+    const uint64_t hs_inert = hs[kStInert];
     c->last_slots = 0;  // the slot space is sparse (see cvlg_debug_slots)
     const uint64_t transitions = hs[kStGTransitions];
     const uint64_t H = hs[kStHeads];
@@ -434,7 +435,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
                             c->uslot.as<uint32_t>(), s);
 
         // ---- lexicographic rank: LSD over (length, then 8-byte chunks last..first) ----------------
-        const uint64_t sort_n = std::max<uint64_t>({J, H, N});
+        const uint64_t sort_n = std::max<uint64_t>({J, H, N + hs_inert});
         c->keys.ensure(sort_n * 8);
         c->keys_alt.ensure(sort_n * 8);
         c->vals.ensure(sort_n * 4);
@@ -503,10 +504,12 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             launch_tile_field(c->tiles.as<uint4>(), n_tiles, 1, c->flags.as<uint32_t>(), s);
             exclusive_scan_u32(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), n_tiles, nullptr,
                                c->scan_tmp.as<uint32_t>(), s);
-            c->ts2.ensure(N * 8 + 8);
-            c->speed2.ensure(N * 8 + 8);
-            c->code2.ensure(N * 4 + 4);
-            c->loff2.ensure(N * 8 + 8);
+            // dense slot count: data lines plus the inert "\r\n" lines that hold slots
+            const uint64_t NS = N + hs[kStInert];
+            c->ts2.ensure(NS * 8 + 8);
+            c->speed2.ensure(NS * 8 + 8);
+            c->code2.ensure(NS * 4 + 4);
+            c->loff2.ensure(NS * 8 + 8);
             DensifyParams DZ;
             DZ.tiles = c->tiles.as<uint4>();
             DZ.n_tiles = n_tiles;
@@ -527,25 +530,25 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             std::swap(c->speed, c->speed2);
             std::swap(c->code, c->code2);
             std::swap(c->loff, c->loff2);
-            c->last_slots = N;
+            c->last_slots = NS;
             const int rbits = bits_for(J);
             const int mode = 1;
             launch_slot_keys(c->hslot.as<uint32_t>(), c->hrank.as<uint32_t>(), H,
-                             c->ts.as<int64_t>(), c->code.as<uint32_t>(), N, ts_min, tsbits, mode,
+                             c->ts.as<int64_t>(), c->code.as<uint32_t>(), NS, ts_min, tsbits, mode,
                              static_cast<uint32_t>(J), c->keys.as<uint64_t>(),
                              c->vals.as<uint32_t>(), c->srank.as<uint32_t>(), s);
             radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(),
-                             c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), N, 0,
+                             c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), NS, 0,
                              mode == 0 ? tsbits + rbits : tsbits, c->sort_tmp.p, s, d_orand,
                              h_orand);
             if (mode == 1) {
-                launch_gather_rank_keys(c->srank.as<uint32_t>(), c->vals.as<uint32_t>(), N,
+                launch_gather_rank_keys(c->srank.as<uint32_t>(), c->vals.as<uint32_t>(), NS,
                                         c->keys.as<uint64_t>(), s);
                 radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(),
-                                 c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), N, 0,
+                                 c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), NS, 0,
                                  rbits, c->sort_tmp.p, s, d_orand, h_orand);
             }
-            launch_slot_jstart(c->vals.as<uint32_t>(), c->srank.as<uint32_t>(), N,
+            launch_slot_jstart(c->vals.as<uint32_t>(), c->srank.as<uint32_t>(), NS,
                                static_cast<uint32_t>(J), jstart, s);
             set_u32_kernel<<<1, 1, 0, s>>>(jstart + J, static_cast<uint32_t>(n_parsed));
             count_launch();
