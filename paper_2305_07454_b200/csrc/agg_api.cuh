@@ -14,8 +14,8 @@ struct DictParams {
     const uint64_t* shard_off;
     const ColumnMap* cmap;
     uint32_t n_shards;
-    const uint32_t* hslot;
-    const uint64_t* loff;
+    uint64_t csv_len;
+    const uint64_t* hid;  // [head] id byte offset | length << 40 (from K1)
     uint64_t n_heads;
     unsigned long long* table;  // [2 * (mask + 1)]
     uint64_t mask;
@@ -75,7 +75,8 @@ struct DensifyParams {
 
 void launch_tile_field(const uint4* tiles, uint64_t n, int field, uint32_t* out, cudaStream_t s);
 void launch_heads_compact(const uint4* tiles, uint64_t n, const uint32_t* hpos, const uint32_t* hscr,
-                          uint32_t* hslot, uint32_t* hend, cudaStream_t s);
+                          const uint64_t* hid_scr, uint32_t* hslot, uint32_t* hend, uint64_t* hid,
+                          cudaStream_t s);
 void launch_densify(const DensifyParams& d, cudaStream_t s);
 void launch_dict_insert(const DictParams& d, cudaStream_t s);
 void launch_dict_flags(const unsigned long long* table, uint64_t cap, uint32_t* flags,

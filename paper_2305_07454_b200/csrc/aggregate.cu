@@ -57,35 +57,6 @@ __device__ __forceinline__ uint32_t shard_of(const uint64_t* shard_off, uint32_t
     return lo;
 }
 
-// Journey id span of the (accepted) line at `loff`: field cmap.journey_id, trimmed
-// (ingest.cpp:31-53, 128).
-__device__ void locate_id(const uint8_t* csv, const uint64_t* shard_off, uint32_t n_shards,
-                          const ColumnMap* cmap, uint64_t loff, uint64_t& off, uint32_t& len) {
-    const uint32_t s = shard_of(shard_off, n_shards, loff);
-    const uint64_t end = shard_off[s + 1];
-    const int32_t col = cmap[s].journey_id;
-    int32_t field = 0;
-    uint64_t start = loff;
-    for (uint64_t x = loff;; ++x) {
-        const uint8_t c = x < end ? csv[x] : uint8_t('\n');
-        if (c == ',' || c == '\n') {
-            if (field == col) {
-                uint64_t b = start, e = x;
-                while (b < e && is_trim(csv[b])) ++b;
-                while (e > b && is_trim(csv[e - 1])) --e;
-                off = b;
-                len = static_cast<uint32_t>(e - b);
-                return;
-            }
-            if (c == '\n') break;
-            ++field;
-            start = x + 1;
-        }
-    }
-    off = loff;
-    len = 0;
-}
-
 // ---- H: dense run-head list from K1's per-tile lists --------------------------------------------
 // tiles[t] = (slot base, data lines, head base, heads)
 __global__ void tile_field_kernel(const uint4* tiles, uint64_t n, int field, uint32_t* out) {
@@ -98,7 +69,8 @@ __global__ void tile_field_kernel(const uint4* tiles, uint64_t n, int field, uin
 // heads in tile order (= provenance order for regular tiles); a run ends at the next head of its
 // tile or at the tile's last line (runs never cross tiles: a tile's first line is always a head)
 __global__ void heads_compact_kernel(const uint4* tiles, uint64_t n, const uint32_t* hpos,
-                                     const uint32_t* hscr, uint32_t* hslot, uint32_t* hend) {
+                                     const uint32_t* hscr, const uint64_t* hid_scr, uint32_t* hslot,
+                                     uint32_t* hend, uint64_t* hid) {
     const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (t >= n) return;
     const uint4 v = tiles[t];
@@ -106,6 +78,7 @@ __global__ void heads_compact_kernel(const uint4* tiles, uint64_t n, const uint3
     for (uint32_t i = 0; i < v.w; ++i) {
         hslot[base + i] = hscr[v.z + i];
         hend[base + i] = i + 1 < v.w ? hscr[v.z + i + 1] : v.x + v.y;
+        hid[base + i] = hid_scr[v.z + i];
     }
 }
 
@@ -129,19 +102,36 @@ __global__ void densify_kernel(DensifyParams D) {
 // ---- D1: dictionary insert (one thread per run head) -----------------------------------------
 // Short ids (<= 15 bytes) are keyed exactly by (bytes 0..7 BE, bytes 8..14 BE << 8 | len);
 // longer ids by (FNV-1a high 40 bits | len, offset << 8 | 0xFF) with a byte comparison.
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0u, 0x0123u); }
+
 __global__ void dict_insert_kernel(DictParams D) {
     const uint64_t h = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (h >= D.n_heads) return;
-    uint64_t off;
-    uint32_t len;
-    locate_id(D.csv, D.shard_off, D.n_shards, D.cmap, D.loff[D.hslot[h]], off, len);
+    const uint64_t id = D.hid[h];
+    const uint64_t off = id & ((1ull << 40) - 1);
+    const uint32_t len = static_cast<uint32_t>(id >> 40);
     const uint8_t* p = D.csv + off;
     uint64_t e0, e1, slot;
     const bool is_long = len > 15;
     if (!is_long) {
         uint64_t k0 = 0, k1 = 0;
-        for (uint32_t i = 0; i < 8; ++i) k0 = (k0 << 8) | (i < len ? p[i] : 0u);
-        for (uint32_t i = 8; i < 15; ++i) k1 = (k1 << 8) | (i < len ? p[i] : 0u);
+        if (off + 20 <= D.csv_len) {  // 5 aligned words cover bytes [off, off + 16)
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(D.csv + (off & ~3ull));
+            const uint32_t sh = static_cast<uint32_t>(off & 3) * 8;
+            const uint32_t a0 = w[0], a1 = w[1], a2 = w[2], a3 = w[3], a4 = w[4];
+            uint32_t b[4] = {__funnelshift_r(a0, a1, sh), __funnelshift_r(a1, a2, sh),
+                             __funnelshift_r(a2, a3, sh), __funnelshift_r(a3, a4, sh)};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // zero the bytes at index >= len
+                const int keep = static_cast<int>(len) - 4 * q;
+                b[q] = keep >= 4 ? b[q] : (keep <= 0 ? 0u : (b[q] & (0xFFFFFFFFu >> (8 * (4 - keep)))));
+            }
+            k0 = (static_cast<uint64_t>(bswap32(b[0])) << 32) | bswap32(b[1]);
+            k1 = ((static_cast<uint64_t>(bswap32(b[2])) << 32) | bswap32(b[3])) >> 8;
+        } else {
+            for (uint32_t i = 0; i < 8; ++i) k0 = (k0 << 8) | (i < len ? p[i] : 0u);
+            for (uint32_t i = 8; i < 15; ++i) k1 = (k1 << 8) | (i < len ? p[i] : 0u);
+        }
         e0 = k0;
         e1 = (k1 << 8) | len;
         slot = mix64(e0 ^ mix64(e1)) & D.mask;
@@ -152,7 +142,11 @@ __global__ void dict_insert_kernel(DictParams D) {
         e1 = (off << 8) | 0xFF;
         slot = mix64(fnv) & D.mask;
     }
-    atomicMax(D.max_len, static_cast<unsigned long long>(len));
+    const uint32_t wmax = __reduce_max_sync(__activemask(), len);
+    if (len == wmax) {  // one atomic per warp (ties: all equal lanes, harmless)
+        const uint32_t lanes = __match_any_sync(__activemask(), len);
+        if ((threadIdx.x & 31) == __ffs(lanes) - 1) atomicMax(D.max_len, static_cast<unsigned long long>(len));
+    }
     for (uint64_t probe = 0; probe <= D.mask; ++probe) {
         uint64_t o0, o1;
         cas128(&D.table[2 * slot], kEmpty, kEmpty, e0, e1, o0, o1);
@@ -329,7 +323,10 @@ __device__ bool payload_equal(const FoldParams& P, uint64_t la, uint64_t lb) {
 // (re-entries continue the same fold), so per-(cell, journey) subtotals are exact.
 constexpr int kFoldWarps = 4;
 constexpr int kChunk = 8;
-constexpr int kLaneCellsFast = 16;  // per-lane cell table; a journey visits ~9 cells
+#ifndef CVLG_LANE_CELLS
+#define CVLG_LANE_CELLS 16
+#endif
+constexpr int kLaneCellsFast = CVLG_LANE_CELLS;  // per-lane cell table; a journey visits ~9 cells
 constexpr int kLaneCellsSlow = 12;  // (slow path also stages slot ids: less shared memory left)
 
 __device__ __forceinline__ uint64_t table_find(const FoldParams& P, uint64_t key, bool insert,
@@ -439,19 +436,34 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
         const uint64_t left = end - pos;
         const uint32_t avail = !active ? 0u : (left < kChunk ? static_cast<uint32_t>(left) : kChunk);
         // ---- stage every lane's next chunk: 32/kChunk lane chunks per coalesced load ----------
+        // (all loads first, then the shared stores: every load of the window is in flight at once)
         constexpr int kPer = 32 / kChunk;
+        constexpr int kIt = 32 / kPer;
+        uint32_t slv[kIt], cv[kIt];
+        double sv[kIt];
+        const int k = lane % kChunk;
 #pragma unroll
-        for (int l = 0; l < 32; l += kPer) {
-            const int src = l + lane / kChunk;
+        for (int it = 0; it < kIt; ++it) {
+            const int src = it * kPer + lane / kChunk;
             const uint64_t p0 = __shfl_sync(0xFFFFFFFFu, pos, src);
             const uint32_t a = __shfl_sync(0xFFFFFFFFu, avail, src);
-            const int k = lane % kChunk;
-            if (static_cast<uint32_t>(k) < a) {
-                const uint64_t slot = kSlow ? P.perm[p0 + k] : p0 + k;
-                s_code[warp][src][k] = P.code[slot];
-                s_speed[warp][src][k] = P.speed[slot];
-                if (kSlow) s_slot[warp][src][k] = static_cast<uint32_t>(slot);
-            }
+            const bool in = static_cast<uint32_t>(k) < a;
+            slv[it] = in ? (kSlow ? __ldg(&P.perm[p0 + k]) : static_cast<uint32_t>(p0 + k)) : 0u;
+        }
+#pragma unroll
+        for (int it = 0; it < kIt; ++it) {
+            const int src = it * kPer + lane / kChunk;
+            const uint32_t a = __shfl_sync(0xFFFFFFFFu, avail, src);
+            const bool in = static_cast<uint32_t>(k) < a;
+            cv[it] = in ? __ldg(&P.code[slv[it]]) : 0u;
+            sv[it] = in ? __ldg(&P.speed[slv[it]]) : 0.0;
+        }
+#pragma unroll
+        for (int it = 0; it < kIt; ++it) {
+            const int src = it * kPer + lane / kChunk;
+            s_code[warp][src][k] = cv[it];
+            s_speed[warp][src][k] = sv[it];
+            if (kSlow) s_slot[warp][src][k] = slv[it];
         }
         __syncwarp();
         // ---- sequential walk of this lane's chunk ---------------------------------------------
@@ -638,9 +650,10 @@ void launch_tile_field(const uint4* tiles, uint64_t n, int field, uint32_t* out,
 }
 
 void launch_heads_compact(const uint4* tiles, uint64_t n, const uint32_t* hpos, const uint32_t* hscr,
-                          uint32_t* hslot, uint32_t* hend, cudaStream_t s) {
+                          const uint64_t* hid_scr, uint32_t* hslot, uint32_t* hend, uint64_t* hid,
+                          cudaStream_t s) {
     if (!n) return;
-    heads_compact_kernel<<<grid_for(n, 128), 128, 0, s>>>(tiles, n, hpos, hscr, hslot, hend);
+    heads_compact_kernel<<<grid_for(n, 128), 128, 0, s>>>(tiles, n, hpos, hscr, hid_scr, hslot, hend, hid);
     count_launch();
 }
 

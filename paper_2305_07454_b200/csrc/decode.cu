@@ -622,6 +622,7 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
             __syncthreads();
             heads = mark_heads(n_data, slot0, [&](uint32_t idx, uint32_t k) {
                 P.out.hslot[head0 + idx] = static_cast<uint32_t>(slot0 + k);
+                P.out.hid[head0 + idx] = (tb + S.id_rel[k]) | (static_cast<uint64_t>(S.id_len[k] & 0x7FFFFFFFu) << 40);
             });
         } else {
             // ---- more than kLineCap lines: slots and heads from the overflow regions --------------
@@ -646,6 +647,8 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                     __syncthreads();
                     heads += mark_heads(n_pass, slot0 + pass_base, [&](uint32_t idx, uint32_t k) {
                         P.out.hslot[head0 + heads + idx] = static_cast<uint32_t>(slot0 + pass_base + k);
+                        P.out.hid[head0 + heads + idx] =
+                            (tb + S.id_rel[k]) | (static_cast<uint64_t>(S.id_len[k] & 0x7FFFFFFFu) << 40);
                     });
                     __syncthreads();
                     if (tid == 0) {  // carry the pass's last line

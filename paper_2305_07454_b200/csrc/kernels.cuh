@@ -51,6 +51,7 @@ struct DecodeOut {
     uint32_t* code;   // [slot] cell code | kHeadBit
     uint64_t* loff;   // [slot] absolute line offset in the CSV buffer
     uint32_t* hslot;  // [head scratch] run-head slots; tile t's at tiles[t].z + (0 .. tiles[t].w)
+    uint64_t* hid;    // [head scratch] journey id span of the head: byte offset | length << 40
     uint4* tiles;     // [tile] (slot base, data lines, head base, heads)
     uint64_t reg_slots;                  // n_tiles * kLineCap
     unsigned long long* ovf_slots;       // overflow-region slot counter (zeroed)

@@ -198,7 +198,7 @@ struct cvlg_context {
     cudaStream_t stream = nullptr, copy_stream = nullptr;
     bool own_stream = true;
     DevBuf csv, shard_off, cmap, good, lb_flag, lb_val, counter, stats, tsmm;
-    DevBuf ts, speed, code, loff, hslot, hscr, hend, tiles, thpos;
+    DevBuf ts, speed, code, loff, hslot, hscr, hend, tiles, thpos, hid_scr, hid, runs;
     DevBuf ts2, speed2, code2, loff2;  // dense copies for the slow (full-sort) path
     DevBuf dict, hdict, flags, pos, uslot, rank_of_slot, hrank, scal;
     DevBuf keys, vals, keys_alt, vals_alt, sort_tmp, scan_tmp, srank, jstart;
@@ -298,11 +298,13 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         c->code.ensure(S_all * 4);
         c->loff.ensure(S_all * 8);
         c->hscr.ensure(S_all * 4);
+        c->hid_scr.ensure(S_all * 8);
         P.out.ts = c->ts.as<int64_t>();
         P.out.speed = c->speed.as<double>();
         P.out.code = c->code.as<uint32_t>();
         P.out.loff = c->loff.as<uint64_t>();
         P.out.hslot = c->hscr.as<uint32_t>();
+        P.out.hid = c->hid_scr.as<uint64_t>();
         P.out.tiles = c->tiles.as<uint4>();
         P.out.reg_slots = reg;
         P.out.ovf_slots = c->counter.as<unsigned long long>();
@@ -395,8 +397,10 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         launch_tile_field(c->tiles.as<uint4>(), n_tiles, 3, c->flags.as<uint32_t>(), s);
         exclusive_scan_u32(c->flags.as<uint32_t>(), c->thpos.as<uint32_t>(), n_tiles, nullptr,
                            c->scan_tmp.as<uint32_t>(), s);
+        c->hid.ensure(H * 8 + 8);
         launch_heads_compact(c->tiles.as<uint4>(), n_tiles, c->thpos.as<uint32_t>(),
-                             c->hscr.as<uint32_t>(), c->hslot.as<uint32_t>(), c->hend.as<uint32_t>(), s);
+                             c->hscr.as<uint32_t>(), c->hid_scr.as<uint64_t>(), c->hslot.as<uint32_t>(),
+                             c->hend.as<uint32_t>(), c->hid.as<uint64_t>(), s);
 
         // ---- journey dictionary ----------------------------------------------------------------
         c->dict.ensure(dcap * 16);
@@ -407,8 +411,8 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         DP.shard_off = P.shard_off;
         DP.cmap = P.cmap;
         DP.n_shards = n_shards;
-        DP.hslot = c->hslot.as<uint32_t>();
-        DP.loff = c->loff.as<uint64_t>();
+        DP.csv_len = total;
+        DP.hid = c->hid.as<uint64_t>();
         DP.n_heads = H;
         DP.table = c->dict.as<unsigned long long>();
         DP.mask = dcap - 1;
@@ -569,6 +573,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         F.perm = c->vals.as<uint32_t>();
         F.hslot = c->hslot.as<uint32_t>();
         F.hend = c->hend.as<uint32_t>();
+
         F.n_heads = H;
         F.ts = c->ts.as<int64_t>();
         F.speed = c->speed.as<double>();
@@ -845,6 +850,7 @@ void cvlg_context_destroy(cvlg_context* c) {
     DevBuf* bufs[] = {&c->csv,    &c->shard_off, &c->cmap,     &c->good,     &c->lb_flag,
                       &c->lb_val, &c->counter,   &c->stats,    &c->tsmm,     &c->ts,
                       &c->hscr,   &c->hend,      &c->tiles,    &c->thpos,    &c->ts2,
+                      &c->hid_scr, &c->hid,      &c->runs,
                       &c->speed2, &c->code2,     &c->loff2,
                       &c->speed,  &c->code,      &c->loff,     &c->hslot,    &c->spill_key,
                       &c->spill_sum, &c->spill_cnt, &c->dict,     &c->hdict,
