@@ -160,6 +160,121 @@ __global__ void __launch_bounds__(kRThreads) radix_scatter_kernel(
     }
 }
 
+// ---- one-sweep LSD passes ------------------------------------------------------------------------
+// (1) radix_hist8_kernel: global 256-bin histograms of all 8 byte digits in one read of the keys;
+// (2) radix_digit_base_kernel: per pass, exclusive digit offsets + "digit constant" flags (a digit
+//     is constant iff one bin holds every key: the pass is skipped, order unchanged);
+// (3) radix_onesweep_kernel per remaining pass: tiles taken in order from an atomic counter rank
+//     their keys (stable, as radix_scatter_kernel), publish per-digit counts, and resolve their
+//     per-digit offsets by a decoupled look-back over previous tiles (one 32-bit word per
+//     (tile, digit): 2-bit flag | 30-bit count), then scatter. One launch per pass.
+constexpr uint32_t kOsAgg = 1u << 30, kOsInc = 2u << 30, kOsMask = (1u << 30) - 1;
+
+__global__ void __launch_bounds__(256) radix_hist8_kernel(const uint64_t* keys, uint64_t n, uint32_t* hist) {
+    __shared__ uint32_t h[8][256];
+    for (int i = threadIdx.x; i < 8 * 256; i += 256) (&h[0][0])[i] = 0;
+    __syncthreads();
+    for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < n; i += static_cast<uint64_t>(gridDim.x) * 256) {
+        const uint64_t k = keys[i];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xFF], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 8 * 256; i += 256) {
+        const uint32_t v = (&h[0][0])[i];
+        if (v) atomicAdd(&hist[i], v);
+    }
+}
+
+__global__ void __launch_bounds__(256) radix_digit_base_kernel(const uint32_t* hist, uint64_t n, uint32_t* base,
+                                                               unsigned long long* constant_mask) {
+    __shared__ uint32_t sm[256 / 32 + 1];
+    for (int p = 0; p < 8; ++p) {
+        const uint32_t v = hist[p * 256 + threadIdx.x];
+        uint32_t tot;
+        base[p * 256 + threadIdx.x] = block_exclusive_scan<256>(v, sm, tot);
+        if (v == n) atomicOr(constant_mask, 1ull << p);
+    }
+}
+
+__global__ void __launch_bounds__(kRThreads) radix_onesweep_kernel(
+    const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_out, uint32_t* vals_out, uint64_t n,
+    int shift, const uint32_t* digit_base, uint32_t* status, uint32_t* tile_counter) {
+    __shared__ uint32_t wc[kRWarps][256];
+    __shared__ uint32_t tile_off[256];
+    __shared__ uint32_t s_tile;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+    for (int i = threadIdx.x; i < kRWarps * 256; i += kRThreads) (&wc[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t base = static_cast<uint64_t>(tile) * kRTile + static_cast<uint64_t>(warp) * kRWarpKeys;
+    uint64_t k[kRItems];
+    uint32_t v[kRItems];
+    uint32_t rank[kRItems];
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < kRItems; ++i) {
+        const uint64_t idx = base + static_cast<uint64_t>(i) * 32 + lane;
+        const bool valid = idx < n;
+        k[i] = valid ? keys_in[idx] : 0ull;
+        v[i] = valid ? vals_in[idx] : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < kRItems; ++i) {
+        const uint64_t idx = base + static_cast<uint64_t>(i) * 32 + lane;
+        const bool valid = idx < n;
+        const uint32_t d = valid ? (static_cast<uint32_t>(k[i] >> shift) & 0xFFu) : 256u;
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+        uint32_t r = 0;
+        if (valid) r = wc[warp][d] + __popc(peers & lt);
+        __syncwarp();
+        if (valid && (peers & lt) == 0) wc[warp][d] += __popc(peers);
+        __syncwarp();
+        rank[i] = r;
+    }
+    __syncthreads();
+    {
+        const int d = threadIdx.x;
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < kRWarps; ++w) {
+            const uint32_t t = wc[w][d];
+            wc[w][d] = run;
+            run += t;
+        }
+        volatile uint32_t* st = status;
+        const uint64_t me = static_cast<uint64_t>(tile) * 256 + d;
+        uint32_t excl = 0;
+        if (tile == 0) {
+            st[me] = kOsInc | run;
+        } else {
+            st[me] = kOsAgg | run;
+            for (int64_t t = static_cast<int64_t>(tile) - 1; t >= 0; --t) {
+                uint32_t w;
+                do {
+                    w = st[static_cast<uint64_t>(t) * 256 + d];
+                } while ((w & ~kOsMask) == 0);
+                excl += w & kOsMask;
+                if ((w & ~kOsMask) == kOsInc) break;
+            }
+            st[me] = kOsInc | (excl + run);
+        }
+        tile_off[d] = digit_base[d] + excl;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kRItems; ++i) {
+        const uint64_t idx = base + static_cast<uint64_t>(i) * 32 + lane;
+        if (idx < n) {
+            const uint32_t d = static_cast<uint32_t>(k[i] >> shift) & 0xFFu;
+            const uint64_t pos = static_cast<uint64_t>(tile_off[d]) + wc[warp][d] + rank[i];
+            keys_out[pos] = k[i];
+            vals_out[pos] = v[i];
+        }
+    }
+}
+
 __global__ void key_or_and_kernel(const uint64_t* keys, uint64_t n, unsigned long long* acc) {
     uint64_t o = 0, a = ~0ull;
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -200,13 +315,56 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t*
 uint64_t radix_temp_bytes(uint64_t n) {
     const uint64_t tiles = (n + kRTile - 1) / kRTile;
     const uint64_t counts = 256 * tiles;
-    return (counts + scan_temp_words(counts) + 16) * 4 + 64;
+    const uint64_t legacy = (counts + scan_temp_words(counts) + 16) * 4 + 64;
+    const uint64_t onesweep = (2 * 8 * 256 + 16 + 8 * counts) * 4 + 64;  // hist, base, flags, status
+    return std::max(legacy, onesweep);
 }
 
 void radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,
                       uint64_t n, int begin_bit, int end_bit, void* d_tmp, cudaStream_t s,
                       unsigned long long* d_orand, unsigned long long* h_orand) {
     if (n <= 1 || end_bit <= begin_bit) return;
+    if (n < (1ull << 30) && d_orand && h_orand) {  // one-sweep passes
+        const uint32_t n_tiles = static_cast<uint32_t>((n + kRTile - 1) / kRTile);
+        uint32_t* hist = static_cast<uint32_t*>(d_tmp);
+        uint32_t* dbase = hist + 8 * 256;
+        unsigned long long* cmask = reinterpret_cast<unsigned long long*>(dbase + 8 * 256);
+        uint32_t* counters = reinterpret_cast<uint32_t*>(cmask + 1);  // 8
+        uint32_t* status = counters + 8;                              // [8][n_tiles][256]
+        cudaMemsetAsync(hist, 0, (2 * 8 * 256 + 16) * 4, s);
+        const unsigned hb = static_cast<unsigned>(std::min<uint64_t>((n + 4095) / 4096, 148 * 4));
+        radix_hist8_kernel<<<hb, 256, 0, s>>>(keys, n, hist);
+        count_launch();
+        radix_digit_base_kernel<<<1, 256, 0, s>>>(hist, n, dbase, cmask);
+        count_launch();
+        cudaMemcpyAsync(h_orand, cmask, 8, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        const uint64_t constant = h_orand[0];
+        int n_pass = 0;
+        for (int shift = begin_bit; shift < end_bit; shift += 8)
+            if (!((constant >> (shift / 8)) & 1)) ++n_pass;
+        if (n_pass) cudaMemsetAsync(status, 0, static_cast<uint64_t>(n_pass) * n_tiles * 256 * 4, s);
+        uint64_t* ki = keys;
+        uint32_t* vi = vals;
+        uint64_t* ko = keys_alt;
+        uint32_t* vo = vals_alt;
+        int p = 0;
+        for (int shift = begin_bit; shift < end_bit; shift += 8) {
+            if ((constant >> (shift / 8)) & 1) continue;  // digit constant: order unchanged
+            radix_onesweep_kernel<<<n_tiles, kRThreads, 0, s>>>(
+                ki, vi, ko, vo, n, shift, dbase + (shift / 8) * 256,
+                status + static_cast<uint64_t>(p) * n_tiles * 256, counters + p);
+            count_launch();
+            ++p;
+            std::swap(ki, ko);
+            std::swap(vi, vo);
+        }
+        if (ki != keys) {
+            cudaMemcpyAsync(keys, ki, n * 8, cudaMemcpyDeviceToDevice, s);
+            cudaMemcpyAsync(vals, vi, n * 4, cudaMemcpyDeviceToDevice, s);
+        }
+        return;
+    }
     // constant-digit detection
     uint64_t diff = ~0ull;
     if (d_orand && h_orand) {
