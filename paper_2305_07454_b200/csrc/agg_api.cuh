@@ -30,6 +30,7 @@ struct FoldParams {
     const uint32_t* perm;   // fast path: sorted run heads; slow path: sorted slots
     const uint32_t* hslot;  // fast path: run start slots
     const uint32_t* hend;   // fast path: run end slots (exclusive)
+    const uint2* runs;      // fast path scratch [H]: (start, end) of the runs in perm order
     uint64_t n_heads;
     const int64_t* ts;
     const double* speed;

@@ -366,8 +366,17 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
     uint64_t j = atomicAdd(reinterpret_cast<unsigned long long*>(P.journey_counter), 1ull);
     bool active = j < P.n_journeys;
     uint32_t ri = 0, re = 0;    // fast path: remaining runs of the journey, [ri, re) in perm
+    // fast path prefetch: the next run of this journey (runs[ri]) and the next journey (its run
+    // range and first run), loaded one or more windows before they are needed, so switching runs
+    // or journeys never stalls the warp on a dependent global load
+    uint2 nrun = make_uint2(0u, 0u);
+    uint64_t jn = ~0ull;
+    uint32_t jn_ri = 0, jn_re = 0;
+    uint2 jn_run = make_uint2(0u, 0u);
+    int jstage = 0;  // 0: jn's run range not loaded, 1: first run not loaded, 2: ready
     uint64_t pos = 0, end = 0;  // current stream window: slots (fast) / perm positions (slow)
     uint32_t n_cells = 0;       // entries used in this lane's table
+    uint64_t seen = 0;          // bloom filter of the cells this journey visited (new cells skip the search)
     uint32_t cur = 0;           // table entry of the current cell (valid when n_cells > 0)
     uint32_t cur_g = kNone;
     double cur_sum = 0.0;
@@ -378,13 +387,10 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
     uint64_t surv = 0;
     bool have_prev = false;
 
-    auto open_run = [&](uint32_t h) {
-        pos = P.hslot[h];
-        end = P.hend[h];
-    };
     auto start_journey = [&]() {
         cur_g = kNone;
         n_cells = 0;
+        seen = 0;
         evict = 0;
         spilled = false;
         have_prev = false;
@@ -392,9 +398,27 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
             pos = P.jstart[j];
             end = P.jstart[j + 1];
         } else {
-            ri = P.jstart[j];
-            re = P.jstart[j + 1];
-            open_run(P.perm[ri++]);
+            // (ri, re, first run) come from the prefetch when ready, else are loaded here
+            if (jstage == 2) {
+                ri = jn_ri;
+                re = jn_re;
+                pos = jn_run.x;
+                end = jn_run.y;
+            } else {
+                ri = P.jstart[j];
+                re = P.jstart[j + 1];
+                const uint2 r0 = P.runs[ri];
+                pos = r0.x;
+                end = r0.y;
+            }
+            ++ri;
+            jstage = 0;
+            if (ri < re) {
+                nrun = P.runs[ri];
+                jn = ~0ull;
+            } else {  // last run open: take the next journey now (not earlier: no hoarding)
+                jn = atomicAdd(reinterpret_cast<unsigned long long*>(P.journey_counter), 1ull);
+            }
         }
     };
     auto spill_store = [&](uint32_t g, double s, uint32_t c) {
@@ -494,8 +518,14 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
                     t_s[warp][cur][lane] = cur_sum;
                     t_c[warp][cur][lane] = cur_cnt;
                 }
-                uint32_t e = 0;
-                while (e < n_cells && t_g[warp][e][lane] != code) ++e;
+                const uint64_t bit = 1ull << ((code * 0x9E3779B1u) >> 26);
+                const bool maybe_seen = (seen & bit) != 0;
+                seen |= bit;
+                uint32_t e = n_cells;
+                if (maybe_seen) {
+                    e = 0;
+                    while (e < n_cells && t_g[warp][e][lane] != code) ++e;
+                }
                 if (e < n_cells) {
                     cur_sum = t_s[warp][e][lane];
                     cur_cnt = t_c[warp][e][lane];
@@ -510,7 +540,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
                     }
                     cur_sum = 0.0;
                     cur_cnt = 0;
-                    if (spilled) {  // the cell may have been evicted earlier: continue its fold
+                    if (spilled && maybe_seen) {  // the cell may have been evicted earlier: continue its fold
                         bool fresh;
                         const uint64_t t = table_find(P, (static_cast<uint64_t>(code) << 32) | j,
                                                       false, fresh);
@@ -529,13 +559,35 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
         }
         __syncwarp();
         // ---- advance the stream ----------------------------------------------------------------
+        if (!kSlow && active && jn < P.n_journeys) {  // advance the next-journey prefetch
+            if (jstage == 0) {
+                jn_ri = P.jstart[jn];
+                jn_re = P.jstart[jn + 1];
+                jstage = 1;
+            } else if (jstage == 1) {
+                jn_run = P.runs[jn_ri];
+                jstage = 2;
+            }
+        }
         pos += avail;
         if (active && pos >= end) {
             if (!kSlow && ri < re) {
-                open_run(P.perm[ri++]);
+                pos = nrun.x;
+                end = nrun.y;
+                ++ri;
+                if (ri < re) nrun = P.runs[ri];
+                else jn = atomicAdd(reinterpret_cast<unsigned long long*>(P.journey_counter), 1ull);
             } else {
                 flush_journey();
-                j = atomicAdd(reinterpret_cast<unsigned long long*>(P.journey_counter), 1ull);
+                if (kSlow) {
+                    j = atomicAdd(reinterpret_cast<unsigned long long*>(P.journey_counter), 1ull);
+                } else {
+                    if (jstage == 1) {  // first run of the prefetched journey not in yet
+                        jn_run = P.runs[jn_ri];
+                        jstage = 2;
+                    }
+                    j = jn;
+                }
                 active = j < P.n_journeys;
                 if (active) start_journey();
             }
@@ -549,6 +601,15 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
         const unsigned long long s = warp_sum(vals[k]);
         if (lane == 0 && s) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[idx[k]]), s);
     }
+}
+
+// fast path: the runs in perm order as (start, end) slot pairs (one load per run switch)
+__global__ void run_list_kernel(const uint32_t* perm, const uint32_t* hslot, const uint32_t* hend,
+                                uint64_t n, uint2* runs) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t h = perm[i];
+    runs[i] = make_uint2(hslot[h], hend[h]);
 }
 
 // spilled journeys' subtotals -> pair list
@@ -738,6 +799,11 @@ void launch_slot_jstart(const uint32_t* perm, const uint32_t* srank, uint64_t n,
 }
 
 void launch_fold(const FoldParams& p, bool slow, cudaStream_t s) {
+    if (!slow && p.n_heads) {
+        run_list_kernel<<<grid_for(p.n_heads, 256), 256, 0, s>>>(p.perm, p.hslot, p.hend, p.n_heads,
+                                                                 const_cast<uint2*>(p.runs));
+        count_launch();
+    }
     if (p.n_journeys) {
         const uint64_t warps = p.n_journeys;
         const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((warps + 7) / 8, 148ull * 64));

@@ -573,6 +573,8 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         F.perm = c->vals.as<uint32_t>();
         F.hslot = c->hslot.as<uint32_t>();
         F.hend = c->hend.as<uint32_t>();
+        c->runs.ensure(H * 8 + 8);
+        F.runs = c->runs.as<uint2>();
 
         F.n_heads = H;
         F.ts = c->ts.as<int64_t>();
