@@ -148,6 +148,42 @@ int cvlg_finalize_pairs(cvlg_context* ctx, const uint64_t* d_cell, const uint64_
                         uint64_t n, const cvlg_grid_spec* spec, uint32_t* d_planes,
                         uint32_t* d_raw_count, void* stream);
 
+/* ---- per-journey feature table (north_star extension) -----------------
+ * NOT IN THE REFERENCE (proj/ has no such function): parity is against this repository's CPU
+ * restatement (tests/test_features.py), never against cvl::run_pipeline. Runs the pipeline (the
+ * lattice outputs are as cvlg_run_pipeline_host / _device) and, per journey in lexicographic id
+ * order, over the records the lattice aggregates in timestamp order: record count, first/last
+ * epoch second, haversine trip length and largest step (mean Earth radius 6,371,008.8 m), largest
+ * speed, largest |d speed / d t|, dwell seconds (steps with both ends at speed <= stop_speed) and
+ * stop episodes; per cell, min / max speed (f32) in [T][4][R][C] (0 where no record). The
+ * results stay in the context until cvlg_features_copy. */
+typedef struct cvlg_features {
+    uint64_t n_journeys;   /* out */
+    uint32_t* points;      /* each array: n_journeys entries, host memory; NULL = skip */
+    int64_t* t_first;
+    int64_t* t_last;
+    double* length_m;
+    double* max_step_m;
+    double* max_speed;
+    double* max_abs_accel;
+    double* dwell_s;
+    uint32_t* stops;
+    uint64_t* id_span;     /* journey id bytes in the concatenated shards: offset | length << 40 */
+    float* cell_speed_min; /* T * 4 * R * C */
+    float* cell_speed_max;
+} cvlg_features;
+
+int cvlg_journey_features_host(cvlg_context* ctx, const uint8_t* const* shard_bufs,
+                               const uint64_t* shard_lens, size_t n_shards, const cvlg_grid_spec* spec,
+                               const cvlg_filter_rules* rules, double stop_speed, uint32_t* planes,
+                               uint32_t* raw_count, cvlg_stats* stats, uint64_t* n_journeys);
+int cvlg_journey_features_device(cvlg_context* ctx, const uint8_t* d_csv, const uint64_t* shard_offsets,
+                                 size_t n_shards, const cvlg_grid_spec* spec,
+                                 const cvlg_filter_rules* rules, double stop_speed, uint32_t* d_planes,
+                                 uint32_t* d_raw_count, cvlg_stats* stats, uint64_t* n_journeys,
+                                 void* stream);
+int cvlg_features_copy(cvlg_context* ctx, cvlg_features* out);
+
 /* .cvl1 container writer (lattice_store.cpp:78-134): 58-byte header then T blocks of
  * (u32 t, planes[t]). Byte-identical to the reference for the same frames. */
 int cvlg_write_container(const uint32_t* planes, const cvlg_grid_spec* spec, int32_t day,

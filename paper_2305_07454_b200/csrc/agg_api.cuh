@@ -57,6 +57,36 @@ struct FoldParams {
     uint64_t* stats;
 };
 
+// per-journey features (features.cu)
+struct FeatureParams {
+    uint64_t n_journeys;
+    const uint32_t* jstart;
+    const uint32_t* perm;  // slow path: sorted dense slots
+    const uint2* runs;     // fast path: (start, end) runs in perm order
+    int slow;
+    const int64_t* ts;
+    const double* speed;
+    const double* lat;
+    const double* lon;
+    const uint32_t* code;
+    double stop_speed;
+    uint64_t D, RC;
+    uint32_t* points;
+    int64_t* t_first;
+    int64_t* t_last;
+    double* length_m;
+    double* max_step_m;
+    double* max_speed;
+    double* max_abs_accel;
+    double* dwell_s;
+    uint32_t* stops;
+    uint32_t* cell_min;  // f32 bits [T][4][R][C] (nullable)
+    uint32_t* cell_max;
+};
+void launch_journey_features(const FeatureParams& f, const uint32_t* hrank, uint64_t n_heads,
+                             const uint64_t* hid, uint32_t* first_scratch, uint64_t* id_span,
+                             uint64_t n_cells_planes, cudaStream_t s);
+
 struct DensifyParams {
     const uint4* tiles;
     uint64_t n_tiles;
@@ -67,6 +97,10 @@ struct DensifyParams {
     const double* speed;
     const uint32_t* code;
     const uint64_t* loff;
+    const double* lat;  // nullable (features only)
+    const double* lon;
+    double* lat_out;
+    double* lon_out;
     int64_t* ts_out;
     double* speed_out;
     uint32_t* code_out;

@@ -94,6 +94,10 @@ __global__ void densify_kernel(DensifyParams D) {
         D.speed_out[dst + k] = D.speed[v.x + k];
         D.code_out[dst + k] = D.code[v.x + k];
         D.loff_out[dst + k] = D.loff[v.x + k];
+        if (D.lat) {
+            D.lat_out[dst + k] = D.lat[v.x + k];
+            D.lon_out[dst + k] = D.lon[v.x + k];
+        }
     }
     const uint32_t hb = D.hpos[t];
     for (uint32_t i = lane; i < v.w; i += 32) D.hslot_out[hb + i] = dst + (D.hscr[v.z + i] - v.x);

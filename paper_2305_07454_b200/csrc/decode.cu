@@ -533,6 +533,10 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                 P.out.ts[slot] = o.ts;
                 P.out.speed[slot] = o.speed;
                 P.out.loff[slot] = p;
+                if (P.out.lat) {
+                    P.out.lat[slot] = why == kAccepted ? o.lat : 0.0;
+                    P.out.lon[slot] = why == kAccepted ? o.lon : 0.0;
+                }
                 S.l_ts[li] = o.ts;
                 S.l_code[li] = code;
                 S.id_rel[li] = o.id_rel;

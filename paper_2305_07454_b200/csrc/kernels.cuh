@@ -50,6 +50,8 @@ struct DecodeOut {
     double* speed;    // [slot]
     uint32_t* code;   // [slot] cell code | kHeadBit
     uint64_t* loff;   // [slot] absolute line offset in the CSV buffer
+    double* lat;      // [slot] (nullable: only written when per-journey features are requested)
+    double* lon;
     uint32_t* hslot;  // [head scratch] run-head slots; tile t's at tiles[t].z + (0 .. tiles[t].w)
     uint64_t* hid;    // [head scratch] journey id span of the head: byte offset | length << 40
     uint4* tiles;     // [tile] (slot base, data lines, head base, heads)

@@ -200,6 +200,10 @@ struct cvlg_context {
     DevBuf csv, shard_off, cmap, good, lb_flag, lb_val, counter, stats, tsmm;
     DevBuf ts, speed, code, loff, hslot, hscr, hend, tiles, thpos, hid_scr, hid, runs;
     DevBuf ts2, speed2, code2, loff2;  // dense copies for the slow (full-sort) path
+    // per-journey features (cvlg_journey_features_*): lat/lon per slot, outputs per journey / cell
+    DevBuf lat, lon, lat2, lon2, f_points, f_tfirst, f_tlast, f_len, f_step, f_vmax, f_acc, f_dwell,
+        f_stops, f_id, f_first, f_cmin, f_cmax;
+    uint64_t f_J = 0, f_cells = 0;
     DevBuf dict, hdict, flags, pos, uslot, rank_of_slot, hrank, scal;
     DevBuf keys, vals, keys_alt, vals_alt, sort_tmp, scan_tmp, srank, jstart;
     DevBuf pair_key, pair_sum, pair_cnt, spill_key, spill_sum, spill_cnt;
@@ -244,7 +248,8 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
               const ColumnMap* h_cmap, const uint8_t* h_good, uint64_t bad_headers,
               const cvlg_grid_spec* spec, const cvlg_filter_rules* rules, uint32_t* d_planes,
               uint32_t* d_raw, cvlg_stats* out_stats, const std::vector<ChunkMark>& marks,
-              bool partial = false) {
+              bool partial = false, const double* feat_stop_speed = nullptr) {
+    const bool feat = feat_stop_speed != nullptr;
     const Dims dims = validate_grid(spec);
     const GridParams gp = make_params(spec, rules, dims);
     cudaStream_t s = c->stream;
@@ -303,6 +308,14 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         P.out.speed = c->speed.as<double>();
         P.out.code = c->code.as<uint32_t>();
         P.out.loff = c->loff.as<uint64_t>();
+        P.out.lat = nullptr;
+        P.out.lon = nullptr;
+        if (feat) {
+            c->lat.ensure(S_all * 8);
+            c->lon.ensure(S_all * 8);
+            P.out.lat = c->lat.as<double>();
+            P.out.lon = c->lon.as<double>();
+        }
         P.out.hslot = c->hscr.as<uint32_t>();
         P.out.hid = c->hid_scr.as<uint64_t>();
         P.out.tiles = c->tiles.as<uint4>();
@@ -524,6 +537,18 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             DZ.speed = c->speed.as<double>();
             DZ.code = c->code.as<uint32_t>();
             DZ.loff = c->loff.as<uint64_t>();
+            DZ.lat = nullptr;
+            DZ.lon = nullptr;
+            DZ.lat_out = nullptr;
+            DZ.lon_out = nullptr;
+            if (feat) {
+                c->lat2.ensure(NS * 8 + 8);
+                c->lon2.ensure(NS * 8 + 8);
+                DZ.lat = c->lat.as<double>();
+                DZ.lon = c->lon.as<double>();
+                DZ.lat_out = c->lat2.as<double>();
+                DZ.lon_out = c->lon2.as<double>();
+            }
             DZ.ts_out = c->ts2.as<int64_t>();
             DZ.speed_out = c->speed2.as<double>();
             DZ.code_out = c->code2.as<uint32_t>();
@@ -534,6 +559,10 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             std::swap(c->speed, c->speed2);
             std::swap(c->code, c->code2);
             std::swap(c->loff, c->loff2);
+            if (feat) {
+                std::swap(c->lat, c->lat2);
+                std::swap(c->lon, c->lon2);
+            }
             c->last_slots = NS;
             const int rbits = bits_for(J);
             const int mode = 1;
@@ -619,6 +648,50 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         CK(cudaEventRecord(c->ev[3], s));
         const uint64_t n_pairs = std::min<uint64_t>(static_cast<uint32_t*>(static_cast<void*>(hs))[0], pair_bound);
 
+        if (feat) {  // per-journey features over the fold's record order (features.cu)
+            c->f_J = J;
+            c->f_cells = static_cast<uint64_t>(dims.T) * 4 * dims.RC;
+            c->f_points.ensure(J * 4 + 4);
+            c->f_tfirst.ensure(J * 8 + 8);
+            c->f_tlast.ensure(J * 8 + 8);
+            c->f_len.ensure(J * 8 + 8);
+            c->f_step.ensure(J * 8 + 8);
+            c->f_vmax.ensure(J * 8 + 8);
+            c->f_acc.ensure(J * 8 + 8);
+            c->f_dwell.ensure(J * 8 + 8);
+            c->f_stops.ensure(J * 4 + 4);
+            c->f_id.ensure(J * 8 + 8);
+            c->f_first.ensure(J * 4 + 4);
+            c->f_cmin.ensure(c->f_cells * 4);
+            c->f_cmax.ensure(c->f_cells * 4);
+            FeatureParams FP;
+            FP.n_journeys = J;
+            FP.jstart = jstart;
+            FP.perm = c->vals.as<uint32_t>();
+            FP.runs = c->runs.as<uint2>();
+            FP.slow = slow ? 1 : 0;
+            FP.ts = c->ts.as<int64_t>();
+            FP.speed = c->speed.as<double>();
+            FP.lat = c->lat.as<double>();
+            FP.lon = c->lon.as<double>();
+            FP.code = c->code.as<uint32_t>();
+            FP.stop_speed = *feat_stop_speed;
+            FP.D = dims.D;
+            FP.RC = dims.RC;
+            FP.points = c->f_points.as<uint32_t>();
+            FP.t_first = c->f_tfirst.as<int64_t>();
+            FP.t_last = c->f_tlast.as<int64_t>();
+            FP.length_m = c->f_len.as<double>();
+            FP.max_step_m = c->f_step.as<double>();
+            FP.max_speed = c->f_vmax.as<double>();
+            FP.max_abs_accel = c->f_acc.as<double>();
+            FP.dwell_s = c->f_dwell.as<double>();
+            FP.stops = c->f_stops.as<uint32_t>();
+            FP.cell_min = c->f_cmin.as<uint32_t>();
+            FP.cell_max = c->f_cmax.as<uint32_t>();
+            launch_journey_features(FP, c->hrank.as<uint32_t>(), H, c->hid.as<uint64_t>(),
+                                    c->f_first.as<uint32_t>(), c->f_id.as<uint64_t>(), c->f_cells, s);
+        }
         c->part_pairs = n_pairs;
         c->part_rbits = rbits;
         c->part_J = J;
@@ -639,6 +712,14 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
                         d_planes, d_raw, s);
         }
     } else {
+        if (feat) {
+            c->f_J = 0;
+            c->f_cells = static_cast<uint64_t>(dims.T) * 4 * dims.RC;
+            c->f_cmin.ensure(c->f_cells * 4);
+            c->f_cmax.ensure(c->f_cells * 4);
+            CK(cudaMemsetAsync(c->f_cmin.p, 0, c->f_cells * 4, s));
+            CK(cudaMemsetAsync(c->f_cmax.p, 0, c->f_cells * 4, s));
+        }
         c->part_pairs = 0;
         c->part_J = 0;
         c->part_long_ids = false;
@@ -705,7 +786,7 @@ void host_headers(const uint8_t* const* bufs, const uint64_t* lens, size_t n,
 
 void run_host(cvlg_context* c, const uint8_t* const* bufs, const uint64_t* lens, size_t n,
               const cvlg_grid_spec* spec, const cvlg_filter_rules* rules, uint32_t* planes,
-              uint32_t* raw, cvlg_stats* stats) {
+              uint32_t* raw, cvlg_stats* stats, const double* feat_stop_speed = nullptr) {
     const Dims dims = validate_grid(spec);
     std::vector<uint64_t> off(n + 1, 0);
     for (size_t i = 0; i < n; ++i) off[i + 1] = off[i] + lens[i];
@@ -765,7 +846,7 @@ void run_host(cvlg_context* c, const uint8_t* const* bufs, const uint64_t* lens,
         d_raw = c->raw.as<uint32_t>();
     }
     run_core(c, d_csv, off, cmap.data(), good.data(), bad, spec, rules, d_planes, d_raw, stats,
-             marks);
+             marks, false, feat_stop_speed);
     if (planes)
         CK(cudaMemcpyAsync(planes, d_planes, lattice_words * 4, cudaMemcpyDeviceToHost, c->stream));
     if (raw) CK(cudaMemcpyAsync(raw, d_raw, raw_words * 4, cudaMemcpyDeviceToHost, c->stream));
@@ -852,7 +933,10 @@ void cvlg_context_destroy(cvlg_context* c) {
     DevBuf* bufs[] = {&c->csv,    &c->shard_off, &c->cmap,     &c->good,     &c->lb_flag,
                       &c->lb_val, &c->counter,   &c->stats,    &c->tsmm,     &c->ts,
                       &c->hscr,   &c->hend,      &c->tiles,    &c->thpos,    &c->ts2,
-                      &c->hid_scr, &c->hid,      &c->runs,
+                      &c->hid_scr, &c->hid,      &c->runs,     &c->lat,      &c->lon,
+                      &c->lat2,    &c->lon2,     &c->f_points, &c->f_tfirst, &c->f_tlast,
+                      &c->f_len,   &c->f_step,   &c->f_vmax,   &c->f_acc,    &c->f_dwell,
+                      &c->f_stops, &c->f_id,     &c->f_first,  &c->f_cmin,   &c->f_cmax,
                       &c->speed2, &c->code2,     &c->loff2,
                       &c->speed,  &c->code,      &c->loff,     &c->hslot,    &c->spill_key,
                       &c->spill_sum, &c->spill_cnt, &c->dict,     &c->hdict,
@@ -980,6 +1064,79 @@ int cvlg_run_pipeline_device(cvlg_context* ctx, const uint8_t* d_csv, const uint
             throw;
         }
         c->stream = saved;
+    });
+}
+
+int cvlg_journey_features_host(cvlg_context* ctx, const uint8_t* const* shard_bufs,
+                               const uint64_t* shard_lens, size_t n_shards, const cvlg_grid_spec* spec,
+                               const cvlg_filter_rules* rules, double stop_speed, uint32_t* planes,
+                               uint32_t* raw_count, cvlg_stats* stats, uint64_t* n_journeys) {
+    return guard([&] {
+        validate_grid(spec);
+        if (n_shards && (!shard_bufs || !shard_lens)) fail(CVLG_E_INVALID_ARG, "NULL shard arrays");
+        if (!(stop_speed == stop_speed)) fail(CVLG_E_INVALID_ARG, "stop_speed is NaN");
+        cvlg_context* c = ctx ? ctx : default_context();
+        if (!c) fail(CVLG_E_CUDA, "no CUDA context");
+        CK(cudaSetDevice(c->device));
+        run_host(c, shard_bufs, shard_lens, n_shards, spec, rules, planes, raw_count, stats, &stop_speed);
+        if (n_journeys) *n_journeys = c->f_J;
+    });
+}
+
+int cvlg_journey_features_device(cvlg_context* ctx, const uint8_t* d_csv, const uint64_t* shard_offsets,
+                                 size_t n_shards, const cvlg_grid_spec* spec,
+                                 const cvlg_filter_rules* rules, double stop_speed, uint32_t* d_planes,
+                                 uint32_t* d_raw_count, cvlg_stats* stats, uint64_t* n_journeys,
+                                 void* stream) {
+    return guard([&] {
+        validate_grid(spec);
+        if (!shard_offsets || !d_planes) fail(CVLG_E_INVALID_ARG, "NULL argument");
+        if (!(stop_speed == stop_speed)) fail(CVLG_E_INVALID_ARG, "stop_speed is NaN");
+        cvlg_context* c = ctx ? ctx : default_context();
+        if (!c) fail(CVLG_E_CUDA, "no CUDA context");
+        CK(cudaSetDevice(c->device));
+        std::vector<uint64_t> off(shard_offsets, shard_offsets + n_shards + 1);
+        if (off[0] != 0) fail(CVLG_E_INVALID_ARG, "shard_offsets[0] must be 0");
+        for (size_t i = 0; i < n_shards; ++i)
+            if (off[i + 1] < off[i]) fail(CVLG_E_INVALID_ARG, "shard_offsets must be non-decreasing");
+        cudaStream_t saved = c->stream;
+        if (stream) c->stream = static_cast<cudaStream_t>(stream);
+        try {
+            std::vector<ChunkMark> marks{ChunkMark{off.back(), off.back(), nullptr}};
+            run_core(c, d_csv, off, nullptr, nullptr, 0, spec, rules, d_planes, d_raw_count, stats,
+                     marks, false, &stop_speed);
+        } catch (...) {
+            c->stream = saved;
+            throw;
+        }
+        c->stream = saved;
+        if (n_journeys) *n_journeys = c->f_J;
+    });
+}
+
+int cvlg_features_copy(cvlg_context* ctx, cvlg_features* out) {
+    return guard([&] {
+        if (!out) fail(CVLG_E_INVALID_ARG, "NULL argument");
+        cvlg_context* c = ctx ? ctx : default_context();
+        if (!c) fail(CVLG_E_CUDA, "no CUDA context");
+        CK(cudaSetDevice(c->device));
+        const uint64_t J = c->f_J;
+        out->n_journeys = J;
+        auto cp = [&](void* dst, const DevBuf& src, uint64_t bytes) {
+            if (dst && bytes) CK(cudaMemcpy(dst, src.p, bytes, cudaMemcpyDeviceToHost));
+        };
+        cp(out->points, c->f_points, J * 4);
+        cp(out->t_first, c->f_tfirst, J * 8);
+        cp(out->t_last, c->f_tlast, J * 8);
+        cp(out->length_m, c->f_len, J * 8);
+        cp(out->max_step_m, c->f_step, J * 8);
+        cp(out->max_speed, c->f_vmax, J * 8);
+        cp(out->max_abs_accel, c->f_acc, J * 8);
+        cp(out->dwell_s, c->f_dwell, J * 8);
+        cp(out->stops, c->f_stops, J * 4);
+        cp(out->id_span, c->f_id, J * 8);
+        cp(out->cell_speed_min, c->f_cmin, c->f_cells * 4);
+        cp(out->cell_speed_max, c->f_cmax, c->f_cells * 4);
     });
 }
 

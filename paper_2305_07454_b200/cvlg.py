@@ -69,6 +69,13 @@ class _Stats(ctypes.Structure):
                 ("stage_seconds", ctypes.c_double * 4)]
 
 
+class _Features(ctypes.Structure):
+    _fields_ = [("n_journeys", ctypes.c_uint64)] + [
+        (n, ctypes.c_void_p) for n in ("points", "t_first", "t_last", "length_m", "max_step_m",
+                                       "max_speed", "max_abs_accel", "dwell_s", "stops", "id_span",
+                                       "cell_speed_min", "cell_speed_max")]
+
+
 def _load() -> ctypes.CDLL:
     if not LIB_PATH.exists():
         raise ImportError(
@@ -99,6 +106,15 @@ def _load() -> ctypes.CDLL:
     lib.cvlg_unpin_host.argtypes = [vp]
     lib.cvlg_launch_count.restype = ctypes.c_uint64
     lib.cvlg_last_error.argtypes = [ctypes.c_char_p, ctypes.c_size_t]
+    lib.cvlg_journey_features_host.argtypes = [vp, ctypes.POINTER(vp), u64p, ctypes.c_size_t,
+                                               ctypes.POINTER(_Grid), ctypes.POINTER(_Rules),
+                                               ctypes.c_double, vp, vp, ctypes.POINTER(_Stats),
+                                               u64p]
+    lib.cvlg_journey_features_device.argtypes = [vp, vp, u64p, ctypes.c_size_t,
+                                                 ctypes.POINTER(_Grid), ctypes.POINTER(_Rules),
+                                                 ctypes.c_double, vp, vp, ctypes.POINTER(_Stats),
+                                                 u64p, vp]
+    lib.cvlg_features_copy.argtypes = [vp, ctypes.POINTER(_Features)]
     return lib
 
 
@@ -108,7 +124,8 @@ EXPORTED_SYMBOLS = [
     "cvlg_default_grid", "cvlg_default_rules", "cvlg_grid_dims", "cvlg_context_create",
     "cvlg_context_destroy", "cvlg_run_pipeline", "cvlg_run_pipeline_host",
     "cvlg_run_pipeline_device", "cvlg_write_container", "cvlg_last_stage_ms", "cvlg_pin_host",
-    "cvlg_unpin_host", "cvlg_launch_count", "cvlg_last_error",
+    "cvlg_unpin_host", "cvlg_launch_count", "cvlg_last_error", "cvlg_journey_features_host",
+    "cvlg_journey_features_device", "cvlg_features_copy",
 ]
 
 
@@ -375,6 +392,63 @@ def run_pipeline_device(d_csv_ptr: int, shard_offsets: Sequence[int], d_planes_p
                                          ctypes.c_void_p(stream) if stream else None))
     if stats is not None:
         stats._fill(st)
+
+
+FEATURE_COLUMNS = {
+    "points": np.uint32, "t_first": np.int64, "t_last": np.int64, "length_m": np.float64,
+    "max_step_m": np.float64, "max_speed": np.float64, "max_abs_accel": np.float64,
+    "dwell_s": np.float64, "stops": np.uint32, "id_span": np.uint64,
+}
+
+
+def _features_fetch(ctx: Context, spec: GridSpec, n: int) -> dict:
+    out = {k: np.empty(n, dtype=t) for k, t in FEATURE_COLUMNS.items()}
+    t, _, r, c = spec.dims()
+    out["cell_speed_min"] = np.empty((t, 4, r, c), dtype=np.float32)
+    out["cell_speed_max"] = np.empty((t, 4, r, c), dtype=np.float32)
+    f = _Features()
+    for k, a in out.items():
+        setattr(f, k, a.ctypes.data if a.size else None)
+    _check(_lib.cvlg_features_copy(ctx.handle, ctypes.byref(f)))
+    return out
+
+
+def journey_features_host(buffers: Iterable, spec: GridSpec | None = None,
+                          rules: FilterRules | None = None, stop_speed: float = 5.0,
+                          stats: PipelineStats | None = None, ctx: Context | None = None):
+    """Pipeline + per-journey feature table (north_star extension, NOT in the reference; see
+    include/cvlg.h cvlg_journey_features_host). Returns (Lattice, features dict): one row per
+    journey in lexicographic id order; ``id_span`` = byte offset | length << 40 into the
+    concatenated shard bytes; ``journey_ids(buffers, features)`` decodes them."""
+    spec = spec or GridSpec()
+    rules = rules or FilterRules()
+    ctx = ctx or default_context()
+    keep, ptrs, lens = [], [], []
+    for b in buffers:
+        a = np.frombuffer(b, dtype=np.uint8) if isinstance(b, (bytes, bytearray, memoryview)) else b
+        keep.append(a)
+        ptrs.append(a.ctypes.data if a.size else 0)
+        lens.append(a.size)
+    n = len(ptrs)
+    parr = (ctypes.c_void_p * max(n, 1))(*ptrs)
+    larr = (ctypes.c_uint64 * max(n, 1))(*lens)
+    planes, rawa = _alloc(spec, True)
+    st = _Stats()
+    nj = ctypes.c_uint64()
+    _check(_lib.cvlg_journey_features_host(ctx.handle, parr, larr, n, ctypes.byref(spec._c()),
+                                           ctypes.byref(rules._c()), float(stop_speed),
+                                           _ptr(planes), _ptr(rawa), ctypes.byref(st),
+                                           ctypes.byref(nj)))
+    if stats is not None:
+        stats._fill(st)
+    return Lattice(planes, rawa), _features_fetch(ctx, spec, nj.value)
+
+
+def journey_ids(buffers: Iterable, features: dict) -> list[bytes]:
+    """Journey id bytes of each feature row (id_span into the concatenated shard bytes)."""
+    blob = b"".join(bytes(b) for b in buffers)
+    spans = features["id_span"]
+    return [blob[int(s) & ((1 << 40) - 1):(int(s) & ((1 << 40) - 1)) + (int(s) >> 40)] for s in spans]
 
 
 def write_container(frames: Lattice | np.ndarray, spec: GridSpec, day: int, path: str | os.PathLike) -> int:
