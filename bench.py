@@ -48,6 +48,8 @@ def parse_args():
                     help="bounded CPU sample for cpu_baseline / --impl reference")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-features", action="store_true",
+                    help="skip the per-journey feature-table timing (extra key, not the metric)")
     return ap.parse_args()
 
 
@@ -323,6 +325,29 @@ def run_ours(args):
         cvlg.unpin_host(raw)
         cvlg.unpin_host(blob)
 
+    # ---- per-journey feature table (north_star extension; extra key, not the headline metric) ---
+    features = None
+    if not args.no_features and not use_dist and rank == 0:
+        for _ in range(2):
+            cvlg.journey_features_device(d_csv.data_ptr(), offs, d_planes.data_ptr(), d_raw.data_ptr(),
+                                         spec, stop_speed=5.0, ctx=ctx, stream=stream.cuda_stream,
+                                         fetch=False)
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        fsteps = max(3, min(args.steps, 10))
+        f0.record(stream)
+        for _ in range(fsteps):
+            nj = cvlg.journey_features_device(d_csv.data_ptr(), offs, d_planes.data_ptr(),
+                                              d_raw.data_ptr(), spec, stop_speed=5.0, ctx=ctx,
+                                              stream=stream.cuda_stream, fetch=False)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        fms = f0.elapsed_time(f1) / fsteps
+        features = {"ms_per_step": fms, "records_per_s": rows / (fms / 1000.0), "journeys": int(nj),
+                    "note": "pipeline + per-journey feature table + per-cell speed min/max "
+                            "(not in the reference: parity vs tests/features_oracle.py)"}
+
     # ---- roofline of the dominant kernel (K1 decode) ---------------------------------------------
     peak, peak_kind = measured_peak_hbm()
     dec_ms = sum(decode_ms) / len(decode_ms)
@@ -384,6 +409,7 @@ def run_ours(args):
             "stage_ms": dict(zip(["decode", "dictionary+order", "fold", "finalize"], stage_avg)),
             "pipeline_hbm_frac": value * (csv_bytes / rows) / 1e9 / peak,
             "cpu_baseline": cpu,
+            "features": features,
             "clocks": clocks.summary(),
             "gpu_launches": launches,
         }

@@ -444,6 +444,29 @@ def journey_features_host(buffers: Iterable, spec: GridSpec | None = None,
     return Lattice(planes, rawa), _features_fetch(ctx, spec, nj.value)
 
 
+def journey_features_device(d_csv_ptr: int, shard_offsets: Sequence[int], d_planes_ptr: int,
+                            d_raw_ptr: int | None = None, spec: GridSpec | None = None,
+                            rules: FilterRules | None = None, stop_speed: float = 5.0,
+                            stats: PipelineStats | None = None, ctx: Context | None = None,
+                            stream: int | None = None, fetch: bool = True):
+    """Device-resident pipeline + per-journey features (see journey_features_host). Returns the
+    features dict (host copies) when ``fetch``, else the number of journeys."""
+    spec = spec or GridSpec()
+    rules = rules or FilterRules()
+    ctx = ctx or default_context()
+    offs = (ctypes.c_uint64 * len(shard_offsets))(*shard_offsets)
+    st = _Stats()
+    nj = ctypes.c_uint64()
+    _check(_lib.cvlg_journey_features_device(
+        ctx.handle, ctypes.c_void_p(d_csv_ptr), offs, len(shard_offsets) - 1,
+        ctypes.byref(spec._c()), ctypes.byref(rules._c()), float(stop_speed),
+        ctypes.c_void_p(d_planes_ptr), ctypes.c_void_p(d_raw_ptr) if d_raw_ptr else None,
+        ctypes.byref(st), ctypes.byref(nj), ctypes.c_void_p(stream) if stream else None))
+    if stats is not None:
+        stats._fill(st)
+    return _features_fetch(ctx, spec, nj.value) if fetch else nj.value
+
+
 def journey_ids(buffers: Iterable, features: dict) -> list[bytes]:
     """Journey id bytes of each feature row (id_span into the concatenated shard bytes)."""
     blob = b"".join(bytes(b) for b in buffers)
