@@ -264,8 +264,8 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
-    ms_t = torch.tensor([ms], device=f"cuda:{local}")
-    rows_t = torch.tensor([float(rows)], device=f"cuda:{local}")
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    rows_t = torch.tensor([float(rows)], dtype=torch.float64, device=f"cuda:{local}")
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
         dist.all_reduce(rows_t, op=dist.ReduceOp.SUM)
@@ -291,7 +291,7 @@ def run_ours(args):
             r.cpu()
         torch.cuda.synchronize()
         e2e_ms = 1000.0 * (time.perf_counter() - t0) / args.steps
-        e_t = torch.tensor([e2e_ms], device=f"cuda:{local}")
+        e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
         dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
         e2e_ms = float(e_t.item())
         e2e = {"value": total_rows / (e2e_ms / 1000.0), "unit": UNIT,
@@ -311,7 +311,7 @@ def run_ours(args):
         for _ in range(args.steps):
             cvlg.run_pipeline_host(bufs, spec, ctx=ctx, out=(planes, raw))
         e2e_ms = 1000.0 * (time.perf_counter() - t0) / args.steps
-        e_t = torch.tensor([e2e_ms], device=f"cuda:{local}")
+        e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
         if world > 1:
             dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
         e2e_ms = float(e_t.item())
@@ -393,7 +393,10 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generator algorithm, byte-identical; seed 1)",
             "config": {
-                "workload": "c2: synthetic 50M-point trace, 100k journeys per GPU, device-resident",
+                "workload": ("c2: synthetic 50M-point trace, 100k journeys per GPU, device-resident"
+                             if args.journeys == 100_000 else
+                             f"synthetic trace, {args.journeys} journeys per GPU "
+                             f"(c3 = 1,000,000: full-day statewide shape), device-resident"),
                 "journeys_per_gpu": args.journeys, "rows_per_gpu": rows, "rows_total": total_rows,
                 "csv_bytes_per_gpu": csv_bytes, "shards": args.shards,
                 "grid": "default GridSpec 46x67x288x4 (3,550,464 cells)",

@@ -30,7 +30,15 @@ struct GridParams {
     uint32_t min_step, dxn_step, R, C, D, T;
     int32_t require_in_grid, drop_missing;
     uint32_t t_magic;  // ceil(2^32 / min_step) (min_step > 1): minute / min_step = umulhi(minute, t_magic)
+    double inv_lat_step, inv_lon_step, inv_dxn_step;  // RN(1 / step): the binning fast path
 };
+
+// RN(1 / step) for the binning fast path (host side, once per run)
+inline void set_inverse_steps(GridParams& g) {
+    g.inv_lat_step = 1.0 / g.lat_step;
+    g.inv_lon_step = 1.0 / g.lon_step;
+    g.inv_dxn_step = 1.0 / g.dxn_step_d;
+}
 
 // ceil(2^32 / min_step): exact quotient for every minute of day (minute * min_step < 2^32 / 2^11)
 inline uint32_t time_magic(uint32_t min_step) {
@@ -71,10 +79,33 @@ CVLG_HD uint32_t extent_bins(double lo, double hi, double step) {
     return n < 1.0 ? 1u : static_cast<uint32_t>(n);
 }
 
+// floor(snap_to_integer(d / step)) for d >= 0, computed first as qa = RN(d * RN(1/step)).
+// |qa - RN(d / step)| <= 3 * 2^-53 * (d / step) (< 3.4e-10 for quotients below 1e6), so when qa is
+// more than 4e-9 * max(1, |rint(qa)|) from every integer, no integer lies between qa and the
+// exact quotient and snap_to_integer (tolerance 1e-9 * max(1, |r|)) leaves the quotient alone:
+// floor(qa) is the exact bin. Otherwise (near a bin edge, or huge quotients) the exact division
+// and snap of grid.cpp decide.
+CVLG_HD double snapped_floor(double d, double step, double inv) {
+    const double qa = d_mul(d, inv);
+    const double r = d_rint(qa);
+    const double ar = d_abs(r);
+    const double m = ar > 1.0 ? ar : 1.0;
+    if (qa < 1e6 && d_abs(d_sub(qa, r)) > d_mul(4e-9, m)) return floor(qa);
+    return floor(snap_to_integer(d_div(d, step)));
+}
+
 // precondition: lo <= x <= hi (checked by the caller)
 CVLG_HD uint32_t linear_bin(double x, double lo, double step, uint32_t n) {
     const double q = snap_to_integer(d_div(d_sub(x, lo), step));
     double b = floor(q);
+    if (b < 0.0) b = 0.0;
+    const double last = static_cast<double>(n - 1);
+    if (b > last) b = last;
+    return static_cast<uint32_t>(b);
+}
+
+CVLG_HD uint32_t linear_bin_fast(double x, double lo, double step, double inv, uint32_t n) {
+    double b = snapped_floor(d_sub(x, lo), step, inv);
     if (b < 0.0) b = 0.0;
     const double last = static_cast<double>(n - 1);
     if (b > last) b = last;
@@ -97,8 +128,7 @@ CVLG_HD uint32_t dxn_bin(double heading, const GridParams& g) {
     double h = d_add(heading, g.dxn_offset);
     h = d_fmod360(h);
     if (h < 0.0) h = d_add(h, 360.0);
-    const double q = snap_to_integer(d_div(h, g.dxn_step_d));
-    const uint32_t d = static_cast<uint32_t>(floor(q));
+    const uint32_t d = static_cast<uint32_t>(snapped_floor(h, g.dxn_step_d, g.inv_dxn_step));
     return d >= g.D ? d - g.D : d;  // == d % D: h <= 360 so q <= 360 / dxn_step = D
 }
 
@@ -110,8 +140,8 @@ CVLG_HD uint32_t cell_code_t(uint32_t t, double lat, double lon, double speed, d
     if (speed > g.speed_ceiling) return kCodeSpeedCeiling;
     if (!in_grid) return kCodeUnbinnable;
     const uint32_t d = dxn_bin(heading, g);
-    const uint32_t r = linear_bin(lat, g.lat_min, g.lat_step, g.R);
-    const uint32_t c = linear_bin(lon, g.lon_min, g.lon_step, g.C);
+    const uint32_t r = linear_bin_fast(lat, g.lat_min, g.lat_step, g.inv_lat_step, g.R);
+    const uint32_t c = linear_bin_fast(lon, g.lon_min, g.lon_step, g.inv_lon_step, g.C);
     return ((t * g.D + d) * g.R + r) * g.C + c;
 }
 

@@ -159,6 +159,7 @@ GridParams make_params(const cvlg_grid_spec* s, const cvlg_filter_rules* r, cons
     g.drop_missing = rr->drop_missing;
     g.speed_ceiling = rr->speed_ceiling;
     g.t_magic = time_magic(s->min_step);
+    set_inverse_steps(g);
     return g;
 }
 

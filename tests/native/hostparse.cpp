@@ -83,10 +83,42 @@ uint32_t hp_cell_code(const double* gd, const uint32_t* gi, int32_t require_in_g
     g.require_in_grid = require_in_grid;
     g.drop_missing = 1;
     g.speed_ceiling = speed_ceiling;
+    g.t_magic = cvlg::time_magic(g.min_step);
+    cvlg::set_inverse_steps(g);
     return cvlg::cell_code(epoch, lat, lon, speed, heading, g);
 }
 
 uint32_t hp_extent_bins(double lo, double hi, double step) { return cvlg::extent_bins(lo, hi, step); }
+
+// binning fast path (snapped_floor) against the exact division + snap, over random quotients
+// concentrated around bin edges, for the given steps; returns mismatches
+uint64_t hp_fuzz_snapped_floor(uint64_t seed, uint64_t count, const double* steps, int n_steps) {
+    uint64_t x = seed * 0x9E3779B97F4A7C15ull + 11;
+    auto rnd = [&]() {
+        x ^= x << 13;
+        x ^= x >> 7;
+        x ^= x << 17;
+        return x;
+    };
+    uint64_t bad = 0;
+    for (uint64_t i = 0; i < count; ++i) {
+        const double step = steps[rnd() % n_steps];
+        const double inv = 1.0 / step;
+        const double k = static_cast<double>(rnd() % 5000);
+        double d;
+        switch (rnd() % 4) {
+            case 0: d = k * step; break;                                     // on an edge
+            case 1: d = k * step + (static_cast<double>(rnd() % 2001) - 1000.0) * 1e-12; break;
+            case 2: d = k * step * (1.0 + (static_cast<double>(rnd() % 2001) - 1000.0) * 1e-15); break;
+            default: d = (static_cast<double>(rnd() >> 11) / 9007199254740992.0) * 5000.0 * step;
+        }
+        if (d < 0) d = 0;
+        const double fast = cvlg::snapped_floor(d, step, inv);
+        const double exact = floor(cvlg::snap_to_integer(d / step));
+        if (fast != exact) ++bad;
+    }
+    return bad;
+}
 
 // ---- K1 fast path (fastparse.cuh) -------------------------------------------------------------
 // The field is placed at buffer offset 40 + shift (shift 0..3 exercises every word alignment),

@@ -99,3 +99,13 @@ def test_class_masks(hp):
     hp.hp_check_class_masks.restype = ctypes.c_uint64
     hp.hp_check_class_masks.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
     assert hp.hp_check_class_masks(1, 3_000_000) == 0
+
+
+def test_binning_fast_path(hp):
+    """floor(snap(d / step)) via RN(d * RN(1/step)) with the 4e-9 edge guard equals the exact
+    division + snap of grid.cpp:10-36, on quotients concentrated at and around bin edges."""
+    hp.hp_fuzz_snapped_floor.restype = ctypes.c_uint64
+    hp.hp_fuzz_snapped_floor.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int]
+    steps = [0.1, 0.01, 0.013, 0.007, 0.25, 10.0, 90.0, 120.0, 45.0, 0.02, 1.0 / 3.0, 0.3]
+    arr = (ctypes.c_double * len(steps))(*steps)
+    assert hp.hp_fuzz_snapped_floor(1, 3_000_000, arr, len(steps)) == 0
