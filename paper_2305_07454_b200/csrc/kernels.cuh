@@ -11,7 +11,7 @@ namespace cvlg {
 
 // ---- decode (K0 header map, K1 tile decode) -------------------------------------------------
 constexpr int kTile = 16384;  // CSV bytes per decode tile
-constexpr int kHalo = 1024;   // bytes staged past the tile end (lines finishing in the next tile)
+constexpr int kHalo = 128;    // bytes staged past the tile end (fast-path lines are <= 95 bytes)
 constexpr int kPre = 16;      // bytes staged before the tile (previous-byte '\n' test)
 constexpr int kDecodeThreads = 256;
 constexpr int kLineCap = 384;  // data lines handled per pass over a tile

@@ -285,3 +285,27 @@ def test_zero_partitions(day_cache):
     with pytest.raises(cvlg.CvlError) as e:
         cvlg.run_pipeline(paths, spec_default(), n_partitions=0)
     assert e.value.code == "ZeroPartitions"
+
+
+def test_dense_short_lines_overflow_tiles(ref, tmp_path):
+    """Tiles holding more than 384 data lines (lines averaging < 43 bytes) take K1's overflow
+    slot region; mixed with long lines that cross the 16 KB tile boundary beyond the staged halo
+    (general path over global memory) and blank / CRLF lines."""
+    rng = random.Random(17)
+    short = []
+    for i in range(30000):  # "a,2021-05-09 HH:MM:SS,37,-92,1,5,9" ~ 34 bytes
+        j = rng.randrange(40)
+        short.append(b"%c%d,2021-05-09 %02d:%02d:%02d,%d.%d,-%d.%d,1,%d,%d" % (
+            97 + j % 26, j, (i // 3600) % 24, (i // 60) % 60, i % 60, 36 + rng.randrange(4),
+            rng.randrange(10), 90 + rng.randrange(5), rng.randrange(10), rng.randrange(130),
+            rng.randrange(360)))
+    longl = [b"L%03d,2021-05-09 10:%02d:%02d,37.123456789012345678901234567890123,-92.5%s,65101,12.5,45" % (
+        k, k // 60, k % 60, b"0" * rng.randrange(60, 700)) for k in range(200)]
+    lines = short + longl
+    rng.shuffle(lines)
+    blob_a = HEADER + b"\n" + b"\n".join(lines[:16000]) + b"\n"
+    blob_b = HEADER + b"\r\n" + b"\r\n\r\n".join(lines[16000:]) + b"\r\n"
+    paths = write_shards(tmp_path, [blob_a, blob_b])
+    est = assert_parity(ref, paths, spec_default())
+    assert est["rows_read"] == len(lines)
+    assert_parity(ref, paths, spec_coarse())
