@@ -170,13 +170,9 @@ __global__ void iota_kernel(uint32_t* v, uint64_t n) {
 
 __global__ void set_u32_kernel(uint32_t* p, uint32_t v) { *p = v; }
 
-__global__ void init_run_kernel(uint64_t* stats, long long* tsmm) {
+__global__ void init_run_kernel(uint64_t* stats) {
     const int i = threadIdx.x;
     if (i < kStCount) stats[i] = 0;
-    if (i == 0) {
-        tsmm[0] = LLONG_MAX;
-        tsmm[1] = LLONG_MIN;
-    }
 }
 
 unsigned blocks_for(uint64_t n, int bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
@@ -198,7 +194,7 @@ struct cvlg_context {
     int device = 0;
     cudaStream_t stream = nullptr, copy_stream = nullptr;
     bool own_stream = true;
-    DevBuf csv, shard_off, cmap, good, lb_flag, lb_val, counter, stats, tsmm;
+    DevBuf csv, shard_off, cmap, good, counter, stats;
     DevBuf ts, speed, code, loff, hslot, hscr, hend, tiles, thpos, hid_scr, hid, runs;
     DevBuf ts2, speed2, code2, loff2;  // dense copies for the slow (full-sort) path
     // per-journey features (cvlg_journey_features_*): lat/lon per slot, outputs per journey / cell
@@ -267,7 +263,6 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
     CK(cudaEventRecord(c->ev[0], s));
     // ---- setup -----------------------------------------------------------------------------
     c->stats.ensure(kStCount * 8);
-    c->tsmm.ensure(16);
     d_stats = c->stats.as<uint64_t>();
     c->shard_off.ensure((n_shards + 1) * 8);
     CK(cudaMemcpyAsync(c->shard_off.p, shard_off.data(), (n_shards + 1) * 8, cudaMemcpyHostToDevice, s));
@@ -325,7 +320,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         P.out.ovf_heads = c->counter.as<unsigned long long>() + 1;
         P.out.ovf_slot_cap = ovf_cap;
         P.out.ovf_head_cap = ovf_cap;
-        init_run_kernel<<<1, 32, 0, s>>>(d_stats, c->tsmm.as<long long>());
+        init_run_kernel<<<1, 32, 0, s>>>(d_stats);
         count_launch();
         if (h_cmap) {
             if (bad_headers) {
@@ -931,8 +926,8 @@ void cvlg_context_destroy(cvlg_context* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     cudaStreamSynchronize(c->copy_stream);
-    DevBuf* bufs[] = {&c->csv,    &c->shard_off, &c->cmap,     &c->good,     &c->lb_flag,
-                      &c->lb_val, &c->counter,   &c->stats,    &c->tsmm,     &c->ts,
+    DevBuf* bufs[] = {&c->csv,    &c->shard_off, &c->cmap,     &c->good,     &c->counter,
+                      &c->stats,  &c->ts,
                       &c->hscr,   &c->hend,      &c->tiles,    &c->thpos,    &c->ts2,
                       &c->hid_scr, &c->hid,      &c->runs,     &c->lat,      &c->lon,
                       &c->lat2,    &c->lon2,     &c->f_points, &c->f_tfirst, &c->f_tlast,
