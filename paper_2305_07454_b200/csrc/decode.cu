@@ -222,10 +222,10 @@ void launch_parse_headers(const uint8_t* csv, const uint64_t* shard_off, uint32_
 // ---------------------------------------------------------------------------------------------
 // K1
 constexpr int kStage = kPre + kTile + kHalo;
-constexpr int kStageAlloc = kStage + 112;  // word over-read padding, keeps 16 B alignment
+constexpr int kStageAlloc = kStage + 32;  // word over-read padding, keeps 16 B alignment
 constexpr int kWords = (kTile + kHalo) / 32;
 constexpr int kMaxShardsInTile = 32;
-constexpr int kDecodeCtasPerSm = 3;
+constexpr int kDecodeCtasPerSm = 4;
 constexpr int kNW = kDecodeThreads / 32;
 constexpr int kRounds = (kLineCap + kDecodeThreads - 1) / kDecodeThreads;
 constexpr int kHeadWords = kRounds * kNW;  // one ballot word per (round, warp)
@@ -242,6 +242,7 @@ struct DecodeSmem {
     uint32_t l_code[kLineCap];  // cell code (no head bit)
     uint32_t hbits[kHeadWords];
     alignas(8) long long l_ts[kLineCap];
+    alignas(8) uint8_t fs_raw[sizeof(FastState) * kDecodeThreads];  // per-thread fast-path state
 };
 
 __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kernel(DecodeParams P,
@@ -277,7 +278,9 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
         tma_load_1d(S.buf[b], P.csv + static_cast<uint64_t>(t) * kTile - kPre, kStage, &bar[b]);
     };
 
-    FastState fs;
+    // the per-thread fast-path state lives in shared memory (frees registers for occupancy)
+    FastState& fs = reinterpret_cast<FastState*>(S.fs_raw)[tid];
+    fs = FastState();
     uint32_t phase0 = 0, phase1 = 0;
     uint32_t c_acc = 0, c_inert = 0;
     const uint32_t G = gridDim.x;
