@@ -309,3 +309,47 @@ def test_dense_short_lines_overflow_tiles(ref, tmp_path):
     est = assert_parity(ref, paths, spec_default())
     assert est["rows_read"] == len(lines)
     assert_parity(ref, paths, spec_coarse())
+
+
+def test_benchmark_workload_c2_bitexact(ref, tmp_path):
+    """The bench workload itself (configs[1], c2: 100k journeys, seed 1, mean duration 500 s,
+    16 shards, 49,977,768 rows, default grid): lattice bits, raw counts and statistics identical
+    to cvl::run_pipeline (16 threads, 32 partitions) on the same shard files."""
+    import os
+    import paper_2305_07454_b200 as cvlg
+    blob, offs, rows = cvlg.synth_day(seed=1, journeys=100_000, shards=16, mean_duration=500.0)
+    assert rows == 49_977_768
+    paths = write_shards(tmp_path, [blob[offs[i]:offs[i + 1]].tobytes() for i in range(16)])
+    threads = max(1, min(16, os.cpu_count() or 1))
+    ep, er, est, _ = ref.run_pipeline(paths, spec_default(), None, n_partitions=2 * threads,
+                                      n_threads=threads)
+    st = cvlg.PipelineStats()
+    lat = cvlg.run_pipeline(paths, spec_default(), stats=st)
+    d = diff_lattice(ep, er, lat.planes, lat.raw)
+    assert d == "", d
+    assert stats_dict(st) == est
+    assert est["rows_read"] == rows
+
+
+def test_shuffled_10m_rows_bitexact(ref, tmp_path):
+    """SURVEY §8d's adversarial variant at scale: 20k journeys (~10M rows) of the bench generator
+    with every row shuffled across 8 shards, so the full (rank, ts) sort path runs."""
+    import numpy as np
+    import paper_2305_07454_b200 as cvlg
+    blob, offs, rows = cvlg.synth_day(seed=2, journeys=20_000, shards=4, mean_duration=500.0)
+    body = []
+    for i in range(4):
+        lines = blob[offs[i]:offs[i + 1]].tobytes().split(b"\n")
+        body.extend(l for l in lines[1:] if l)
+    rng = np.random.default_rng(7)
+    order = rng.permutation(len(body))
+    body = [body[k] for k in order]
+    shards = [HEADER + b"\n" + b"\n".join(body[i::8]) + b"\n" for i in range(8)]
+    paths = write_shards(tmp_path, shards)
+    ep, er, est, _ = ref.run_pipeline(paths, spec_default(), None, n_partitions=32, n_threads=16)
+    st = cvlg.PipelineStats()
+    lat = cvlg.run_pipeline(paths, spec_default(), stats=st)
+    d = diff_lattice(ep, er, lat.planes, lat.raw)
+    assert d == "", d
+    assert stats_dict(st) == est
+    assert est["rows_read"] == rows
