@@ -48,6 +48,9 @@ def parse_args():
                     help="bounded CPU sample for cpu_baseline / --impl reference")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shuffled", action="store_true",
+                    help="adversarial variant (SURVEY §8d): rows shuffled across shards, so the "
+                         "full (rank, ts) sort path runs")
     ap.add_argument("--no-features", action="store_true",
                     help="skip the per-journey feature-table timing (extra key, not the metric)")
     return ap.parse_args()
@@ -212,6 +215,9 @@ def run_ours(args):
     t_gen = time.perf_counter()
     blob, offs, rows = generate(args.journeys, args.shards, args.mean_duration, seed=1,
                                 mod=world, rem=rank)
+    if args.shuffled:
+        from paper_2305_07454_b200.cvlg import shuffle_rows
+        blob, offs = shuffle_rows(blob, offs, args.shards, seed=7)
     t_gen = time.perf_counter() - t_gen
     csv_bytes = int(offs[-1])
     bufs = [blob[offs[i]:offs[i + 1]] for i in range(len(offs) - 1)]
@@ -396,7 +402,9 @@ def run_ours(args):
                 "workload": ("c2: synthetic 50M-point trace, 100k journeys per GPU, device-resident"
                              if args.journeys == 100_000 else
                              f"synthetic trace, {args.journeys} journeys per GPU "
-                             f"(c3 = 1,000,000: full-day statewide shape), device-resident"),
+                             f"(c3 = 1,000,000: full-day statewide shape), device-resident")
+                            + (" | ADVERSARIAL: rows shuffled across shards (full-sort path)"
+                               if args.shuffled else ""),
                 "journeys_per_gpu": args.journeys, "rows_per_gpu": rows, "rows_total": total_rows,
                 "csv_bytes_per_gpu": csv_bytes, "shards": args.shards,
                 "grid": "default GridSpec 46x67x288x4 (3,550,464 cells)",

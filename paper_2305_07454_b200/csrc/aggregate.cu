@@ -71,11 +71,13 @@ __global__ void tile_field_kernel(const uint4* tiles, uint64_t n, int field, uin
 __global__ void heads_compact_kernel(const uint4* tiles, uint64_t n, const uint32_t* hpos,
                                      const uint32_t* hscr, const uint64_t* hid_scr, uint32_t* hslot,
                                      uint32_t* hend, uint64_t* hid) {
-    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    // one warp per tile: lanes copy the tile's heads
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x / 32) + (threadIdx.x >> 5);
     if (t >= n) return;
+    const uint32_t lane = threadIdx.x & 31;
     const uint4 v = tiles[t];
     const uint32_t base = hpos[t];
-    for (uint32_t i = 0; i < v.w; ++i) {
+    for (uint32_t i = lane; i < v.w; i += 32) {
         hslot[base + i] = hscr[v.z + i];
         hend[base + i] = i + 1 < v.w ? hscr[v.z + i + 1] : v.x + v.y;
         hid[base + i] = hid_scr[v.z + i];
@@ -153,7 +155,14 @@ __global__ void dict_insert_kernel(DictParams D) {
     }
     for (uint64_t probe = 0; probe <= D.mask; ++probe) {
         uint64_t o0, o1;
-        cas128(&D.table[2 * slot], kEmpty, kEmpty, e0, e1, o0, o1);
+        // read first: a journey id is inserted by every one of its run heads, and a failing CAS
+        // on a hot key is still a serialized read-modify-write at L2. Entries go from empty to
+        // their value once (one 128-bit CAS) and never change, so two non-empty halves are
+        // consistent; anything else is decided by the CAS itself.
+        o1 = ld_relaxed_u64(reinterpret_cast<const uint64_t*>(&D.table[2 * slot + 1]));
+        o0 = ld_relaxed_u64(reinterpret_cast<const uint64_t*>(&D.table[2 * slot]));
+        if (o0 == kEmpty || o1 == kEmpty)
+            cas128(&D.table[2 * slot], kEmpty, kEmpty, e0, e1, o0, o1);
         if (o0 == kEmpty && o1 == kEmpty) break;  // inserted
         if (!is_long) {
             if (o0 == e0 && o1 == e1) break;
@@ -718,7 +727,7 @@ void launch_heads_compact(const uint4* tiles, uint64_t n, const uint32_t* hpos, 
                           const uint64_t* hid_scr, uint32_t* hslot, uint32_t* hend, uint64_t* hid,
                           cudaStream_t s) {
     if (!n) return;
-    heads_compact_kernel<<<grid_for(n, 128), 128, 0, s>>>(tiles, n, hpos, hscr, hid_scr, hslot, hend, hid);
+    heads_compact_kernel<<<grid_for(n, 8), 256, 0, s>>>(tiles, n, hpos, hscr, hid_scr, hslot, hend, hid);
     count_launch();
 }
 

@@ -482,7 +482,10 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         c->jstart.ensure((J + 1) * 4);
         c->srank.ensure(sort_n * 4);
         uint32_t* jstart = c->jstart.as<uint32_t>();
-        {
+        // runs averaging < 4 records (row-shuffled input): the run merge cannot pay, go straight
+        // to the full sort (the head sort + order check would cost as much as the sort itself)
+        slow = H * 4 > n_parsed;
+        if (!slow) {
             const int rbits = bits_for(J - 1);
             const int mode = 1;  // sort by ts, then (stably) by rank
             CK(cudaMemsetAsync(d_invalid, 0, 4, s));

@@ -231,4 +231,51 @@ int64_t cvlg_synth_day_owned(uint64_t seed, uint32_t n_journeys, uint32_t n_shar
     return static_cast<int64_t>(total);
 }
 
+// Adversarial variant of a generated day: every data row of the input shards
+// (each shard = header line + rows) shuffled with a seeded Fisher-Yates permutation and dealt
+// round-robin to n_out shards, each starting with `header`. Returns bytes written, or < 0.
+int64_t cvlg_shuffle_rows(const uint8_t* blob, const uint64_t* offs, uint32_t n_in, uint64_t seed,
+                          const char* header, uint32_t n_out, uint8_t* out, uint64_t cap,
+                          uint64_t* out_offs) {
+    if (!blob || !offs || !out || !out_offs || !header || n_out == 0) return -1;
+    std::vector<std::pair<uint64_t, uint32_t>> rows;  // (offset, length without '\n')
+    for (uint32_t s = 0; s < n_in; ++s) {
+        uint64_t p = offs[s];
+        const uint64_t e = offs[s + 1];
+        while (p < e && blob[p] != '\n') ++p;  // skip the header line
+        ++p;
+        while (p < e) {
+            uint64_t q = p;
+            while (q < e && blob[q] != '\n') ++q;
+            if (q > p) rows.emplace_back(p, static_cast<uint32_t>(q - p));
+            p = q + 1;
+        }
+    }
+    uint64_t x = seed * 0x9E3779B97F4A7C15ull + 0x2545F4914F6CDD1Dull;
+    for (uint64_t i = rows.size(); i > 1; --i) {
+        x ^= x << 13;
+        x ^= x >> 7;
+        x ^= x << 17;
+        std::swap(rows[i - 1], rows[x % i]);
+    }
+    const uint64_t hl = std::strlen(header);
+    uint64_t w = 0;
+    for (uint32_t o = 0; o < n_out; ++o) {
+        out_offs[o] = w;
+        if (w + hl + 1 > cap) return -2;
+        std::memcpy(out + w, header, hl);
+        w += hl;
+        out[w++] = '\n';
+        for (uint64_t i = o; i < rows.size(); i += n_out) {
+            const auto& r = rows[i];
+            if (w + r.second + 1 > cap) return -2;
+            std::memcpy(out + w, blob + r.first, r.second);
+            w += r.second;
+            out[w++] = '\n';
+        }
+    }
+    out_offs[n_out] = w;
+    return static_cast<int64_t>(w);
+}
+
 }  // extern "C"

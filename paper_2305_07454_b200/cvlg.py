@@ -522,3 +522,20 @@ def synth_day(seed: int = 0, journeys: int = 100, shards: int = 8, sample_period
     if n < 0:
         raise CvlError(101, f"synth_day failed ({n})")
     return out[:n], list(offs), rows.value
+
+
+def shuffle_rows(blob: np.ndarray, offs: Sequence[int], n_out: int, seed: int = 7,
+                 header: bytes = b"Journey Id,Timestamp,Latitude,Longitude,Postal Code,Speed,Heading"):
+    """Adversarial variant: all data rows shuffled across n_out shards (C++)."""
+    out = np.empty(int(offs[-1]) + n_out * (len(header) + 1) + 64, dtype=np.uint8)
+    ooffs = (ctypes.c_uint64 * (n_out + 1))()
+    iof = (ctypes.c_uint64 * len(offs))(*offs)
+    fn = _lib.cvlg_shuffle_rows
+    fn.restype = ctypes.c_int64
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_char_p,
+                   ctypes.c_uint32, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
+    n = fn(blob.ctypes.data_as(ctypes.c_void_p), iof, len(offs) - 1, seed, header, n_out,
+           out.ctypes.data_as(ctypes.c_void_p), out.size, ooffs)
+    if n < 0:
+        raise CvlError(101, f"shuffle_rows failed ({n})")
+    return out[:n], list(ooffs)

@@ -17,6 +17,8 @@ ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--shuffle", action="store_true")
 a = ap.parse_args()
 blob, offs, rows = cvlg.synth_day(seed=1, journeys=a.journeys, shards=a.shards, mean_duration=500.0)
+if a.shuffle:  # adversarial variant: the full-sort path
+    blob, offs = cvlg.cvlg.shuffle_rows(blob, offs, a.shards, seed=7)
 spec = cvlg.GridSpec()
 T, _, R, C = spec.dims()
 d_csv = torch.from_numpy(blob).cuda()
