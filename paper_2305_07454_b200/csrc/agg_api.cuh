@@ -21,6 +21,7 @@ struct DictParams {
     uint64_t mask;
     uint32_t* hdict;
     unsigned long long* max_len;
+    uint32_t* full;  // set when a probe chain exceeds its bound (host re-runs with more room)
 };
 
 struct FoldParams {

@@ -153,7 +153,12 @@ __global__ void dict_insert_kernel(DictParams D) {
         const uint32_t lanes = __match_any_sync(__activemask(), len);
         if ((threadIdx.x & 31) == __ffs(lanes) - 1) atomicMax(D.max_len, static_cast<unsigned long long>(len));
     }
-    for (uint64_t probe = 0; probe <= D.mask; ++probe) {
+    const uint64_t max_probe = D.mask < 4096 ? D.mask : 4096;
+    for (uint64_t probe = 0;; ++probe) {
+        if (probe > max_probe) {  // table too full for this many distinct ids: re-run larger
+            atomicOr(D.full, 1u);
+            break;
+        }
         uint64_t o0, o1;
         // read first: a journey id is inserted by every one of its run heads, and a failing CAS
         // on a hot key is still a serialized read-modify-write at L2. Entries go from empty to

@@ -386,15 +386,17 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
     bool slow = false;
     uint64_t J = 0;
     if (n_parsed > 0) {
-        c->scal.ensure(64);
-        CK(cudaMemsetAsync(c->scal.p, 0, 64, s));
+        c->scal.ensure(128);
+        CK(cudaMemsetAsync(c->scal.p, 0, 128, s));
         unsigned long long* d_maxlen = c->scal.as<unsigned long long>();
         uint32_t* d_total = c->scal.as<uint32_t>() + 4;
         unsigned long long* d_orand = c->scal.as<unsigned long long>() + 4;
         unsigned long long* h_orand = reinterpret_cast<unsigned long long*>(hs + 40);
         uint32_t* d_invalid = c->scal.as<uint32_t>() + 12;
-        const uint64_t dcap = pow2_at_least(2 * H);
-        const uint64_t flag_n = std::max<uint64_t>({dcap, n_tiles + 1, N + 1});
+        // dictionary capacity: 2x the distinct ids, which are at most H (and usually far fewer:
+        // every run head inserts its journey); start at <= 8M entries, grow if a probe chain fills
+        uint64_t dcap = pow2_at_least(2 * std::min<uint64_t>(H, 1ull << 22));
+        const uint64_t flag_n = std::max<uint64_t>({pow2_at_least(2 * H), n_tiles + 1, N + 1});
         c->flags.ensure(flag_n * 4 + 16);
         c->pos.ensure(flag_n * 4 + 16);
         c->scan_tmp.ensure(scan_temp_words(flag_n) * 4 + 64);
@@ -412,28 +414,36 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
                              c->hend.as<uint32_t>(), c->hid.as<uint64_t>(), s);
 
         // ---- journey dictionary ----------------------------------------------------------------
-        c->dict.ensure(dcap * 16);
         c->hdict.ensure(H * 4);
-        CK(cudaMemsetAsync(c->dict.p, 0xFF, dcap * 16, s));
-        DictParams DP;
-        DP.csv = d_csv;
-        DP.shard_off = P.shard_off;
-        DP.cmap = P.cmap;
-        DP.n_shards = n_shards;
-        DP.csv_len = total;
-        DP.hid = c->hid.as<uint64_t>();
-        DP.n_heads = H;
-        DP.table = c->dict.as<unsigned long long>();
-        DP.mask = dcap - 1;
-        DP.hdict = c->hdict.as<uint32_t>();
-        DP.max_len = d_maxlen;
-        launch_dict_insert(DP, s);
-        TRACE("dict inserted");
-        launch_dict_flags(c->dict.as<unsigned long long>(), dcap, c->flags.as<uint32_t>(), s);
-        exclusive_scan_u32(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), dcap, d_total,
-                           c->scan_tmp.as<uint32_t>(), s);
-        CK(cudaMemcpyAsync(hs, c->scal.p, 32, cudaMemcpyDeviceToHost, s));
-        sync(c);
+        uint32_t* d_dict_full = c->scal.as<uint32_t>() + 16;
+        for (int attempt = 0;; ++attempt) {
+            c->dict.ensure(dcap * 16);
+            CK(cudaMemsetAsync(c->dict.p, 0xFF, dcap * 16, s));
+            CK(cudaMemsetAsync(d_dict_full, 0, 4, s));
+            DictParams DP;
+            DP.csv = d_csv;
+            DP.shard_off = P.shard_off;
+            DP.cmap = P.cmap;
+            DP.n_shards = n_shards;
+            DP.csv_len = total;
+            DP.hid = c->hid.as<uint64_t>();
+            DP.n_heads = H;
+            DP.table = c->dict.as<unsigned long long>();
+            DP.mask = dcap - 1;
+            DP.hdict = c->hdict.as<uint32_t>();
+            DP.max_len = d_maxlen;
+            DP.full = d_dict_full;
+            launch_dict_insert(DP, s);
+            TRACE("dict inserted");
+            launch_dict_flags(c->dict.as<unsigned long long>(), dcap, c->flags.as<uint32_t>(), s);
+            exclusive_scan_u32(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), dcap, d_total,
+                               c->scan_tmp.as<uint32_t>(), s);
+            CK(cudaMemcpyAsync(hs, c->scal.p, 128, cudaMemcpyDeviceToHost, s));
+            sync(c);
+            if (static_cast<uint32_t*>(static_cast<void*>(hs))[16] == 0) break;
+            if (dcap >= pow2_at_least(2 * H)) fail(CVLG_E_INTERNAL, "journey dictionary overflow");
+            dcap = pow2_at_least(2 * H);  // a probe chain filled up: exact bound
+        }
         const uint64_t max_len = hs[0];
         J = static_cast<uint32_t*>(static_cast<void*>(hs))[4];
         c->uslot.ensure(J * 4);
