@@ -345,7 +345,7 @@ constexpr int kChunk = 8;
 #define CVLG_LANE_CELLS 16
 #endif
 constexpr int kLaneCellsFast = CVLG_LANE_CELLS;  // per-lane cell table; a journey visits ~9 cells
-constexpr int kLaneCellsSlow = 12;  // (slow path also stages slot ids: less shared memory left)
+constexpr int kLaneCellsSlow = 10;  // (slow path also stages slot ids and timestamps: less shared memory left)
 
 __device__ __forceinline__ uint64_t table_find(const FoldParams& P, uint64_t key, bool insert,
                                                bool& fresh) {
@@ -373,6 +373,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
     __shared__ uint32_t s_code[kFoldWarps][32][kChunk + 1];
     __shared__ double s_speed[kFoldWarps][32][kChunk + 1];
     __shared__ uint32_t s_slot[kSlow ? kFoldWarps : 1][32][kChunk + 1];
+    __shared__ long long s_ts[kSlow ? kFoldWarps : 1][32][kSlow ? kChunk + 1 : 1];
     // per-lane (cell -> running subtotal) table, entry e of lane l at [e][l]
     __shared__ uint32_t t_g[kFoldWarps][kLaneCells][32];
     __shared__ uint32_t t_c[kFoldWarps][kLaneCells][32];
@@ -492,6 +493,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
             const bool in = static_cast<uint32_t>(k) < a;
             slv[it] = in ? (kSlow ? __ldg(&P.perm[p0 + k]) : static_cast<uint32_t>(p0 + k)) : 0u;
         }
+        long long tv[kSlow ? kIt : 1];
 #pragma unroll
         for (int it = 0; it < kIt; ++it) {
             const int src = it * kPer + lane / kChunk;
@@ -499,13 +501,17 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
             const bool in = static_cast<uint32_t>(k) < a;
             cv[it] = in ? __ldg(&P.code[slv[it]]) : 0u;
             sv[it] = in ? __ldg(&P.speed[slv[it]]) : 0.0;
+            if (kSlow) tv[kSlow ? it : 0] = in ? __ldg(&P.ts[slv[it]]) : 0;
         }
 #pragma unroll
         for (int it = 0; it < kIt; ++it) {
             const int src = it * kPer + lane / kChunk;
             s_code[warp][src][k] = cv[it];
             s_speed[warp][src][k] = sv[it];
-            if (kSlow) s_slot[warp][src][k] = slv[it];
+            if (kSlow) {
+                s_slot[warp][src][k] = slv[it];
+                s_ts[warp][src][kSlow ? k : 0] = tv[kSlow ? it : 0];
+            }
         }
         __syncwarp();
         // ---- sequential walk of this lane's chunk ---------------------------------------------
@@ -513,7 +519,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
             const uint32_t code = s_code[warp][lane][k] & kCodeMask;
             if (kSlow) {
                 const uint32_t slot = s_slot[warp][lane][k];
-                const int64_t t = P.ts[slot];
+                const int64_t t = s_ts[warp][lane][kSlow ? k : 0];
                 if (have_prev && t == prev_ts) {  // duplicate key: dropped before filtering
                     ++c_dup;
                     if (!payload_equal(P, P.loff[slot], P.loff[surv])) ++c_conf;
