@@ -114,6 +114,7 @@ void launch_heads_compact(const uint4* tiles, uint64_t n, const uint32_t* hpos, 
                           const uint64_t* hid_scr, uint32_t* hslot, uint32_t* hend, uint64_t* hid,
                           cudaStream_t s);
 void launch_densify(const DensifyParams& d, cudaStream_t s);
+void launch_ts_range(const int64_t* ts, const uint32_t* code, uint64_t n, long long* mm, cudaStream_t s);
 void launch_dict_insert(const DictParams& d, cudaStream_t s);
 void launch_dict_flags(const unsigned long long* table, uint64_t cap, uint32_t* flags,
                        cudaStream_t s);

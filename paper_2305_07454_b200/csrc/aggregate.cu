@@ -7,6 +7,8 @@
 //   journey ids -> lexicographic ranks, items sorted (rank, sec)  :305-328
 //   cellmap[(g, rank)] += speed in (rank, sec) order              :331-358
 //   finalize: sort by (g, journey), fold subtotals in journey order, f32 narrow :161-204
+#include <climits>
+
 #include "agg_api.cuh"
 #include "kernels.cuh"
 #include "sort_api.cuh"
@@ -298,6 +300,33 @@ __global__ void slot_keys_kernel(const uint32_t* hslot, const uint32_t* hrank, u
     keys[i] = mode == 0 ? ((static_cast<uint64_t>(r) << tsbits) | t) : t;
     vals[i] = static_cast<uint32_t>(i);
     srank[i] = r;
+}
+
+// min / max epoch over non-rejected slots (the slow path's combined sort key)
+__global__ void ts_range_kernel(const int64_t* ts, const uint32_t* code, uint64_t n, long long* mm) {
+    long long lo = LLONG_MAX, hi = LLONG_MIN;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if ((code[i] & kCodeMask) == kCodeRejected) continue;
+        const long long t = ts[i];
+        lo = t < lo ? t : lo;
+        hi = t > hi ? t : hi;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long a = __shfl_xor_sync(0xFFFFFFFFu, lo, o), b = __shfl_xor_sync(0xFFFFFFFFu, hi, o);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&mm[0], lo);
+        atomicMax(&mm[1], hi);
+    }
+}
+
+__global__ void ts_range_init_kernel(long long* mm) {
+    mm[0] = LLONG_MAX;
+    mm[1] = LLONG_MIN;
 }
 
 __global__ void slot_jstart_kernel(const uint32_t* perm, const uint32_t* srank, uint64_t n,
@@ -740,6 +769,16 @@ void launch_heads_compact(const uint4* tiles, uint64_t n, const uint32_t* hpos, 
     if (!n) return;
     heads_compact_kernel<<<grid_for(n, 8), 256, 0, s>>>(tiles, n, hpos, hscr, hid_scr, hslot, hend, hid);
     count_launch();
+}
+
+void launch_ts_range(const int64_t* ts, const uint32_t* code, uint64_t n, long long* mm, cudaStream_t s) {
+    ts_range_init_kernel<<<1, 1, 0, s>>>(mm);
+    count_launch();
+    if (n) {
+        ts_range_kernel<<<static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 148 * 8)), 256, 0, s>>>(
+            ts, code, n, mm);
+        count_launch();
+    }
 }
 
 void launch_densify(const DensifyParams& d, cudaStream_t s) {

@@ -574,14 +574,34 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             }
             c->last_slots = NS;
             const int rbits = bits_for(J);
-            const int mode = 1;
+            // one sort on (rank << span_bits | ts - ts_lo) when the kept timestamps' span and the
+            // rank fit 64 bits (a day: 17 + 17 bits); else ts then (stably) rank
+            int64_t key_ts_min = ts_min;
+            int key_tsbits = tsbits;
+            int mode = 1;
+            {
+                long long* d_mm = reinterpret_cast<long long*>(c->scal.as<uint32_t>() + 18);
+                launch_ts_range(c->ts.as<int64_t>(), c->code.as<uint32_t>(), NS, d_mm, s);
+                CK(cudaMemcpyAsync(hs + 48, d_mm, 16, cudaMemcpyDeviceToHost, s));
+                sync(c);
+                const int64_t lo = static_cast<int64_t>(hs[48]), hi = static_cast<int64_t>(hs[49]);
+                if (lo <= hi) {
+                    const uint64_t span = static_cast<uint64_t>(hi) - static_cast<uint64_t>(lo);
+                    const int sb = span == 0 ? 1 : bits_for(span);
+                    if (sb + rbits <= 64) {
+                        mode = 0;
+                        key_ts_min = lo;
+                        key_tsbits = sb;
+                    }
+                }
+            }
             launch_slot_keys(c->hslot.as<uint32_t>(), c->hrank.as<uint32_t>(), H,
-                             c->ts.as<int64_t>(), c->code.as<uint32_t>(), NS, ts_min, tsbits, mode,
+                             c->ts.as<int64_t>(), c->code.as<uint32_t>(), NS, key_ts_min, key_tsbits, mode,
                              static_cast<uint32_t>(J), c->keys.as<uint64_t>(),
                              c->vals.as<uint32_t>(), c->srank.as<uint32_t>(), s);
             radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(),
                              c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), NS, 0,
-                             mode == 0 ? tsbits + rbits : tsbits, c->sort_tmp.p, s, d_orand,
+                             mode == 0 ? key_tsbits + rbits : key_tsbits, c->sort_tmp.p, s, d_orand,
                              h_orand);
             if (mode == 1) {
                 launch_gather_rank_keys(c->srank.as<uint32_t>(), c->vals.as<uint32_t>(), NS,
