@@ -329,6 +329,29 @@ __global__ void ts_range_init_kernel(long long* mm) {
     mm[1] = LLONG_MIN;
 }
 
+// Same keys without a search: one thread per run head writes its run's slots (dense layout: a
+// run ends at the next head), thread 0 also the slots before the first head (rejected lines).
+__global__ void run_keys_kernel(const uint32_t* hslot, const uint32_t* hrank, uint64_t n_heads,
+                                const int64_t* ts, const uint32_t* code, uint64_t n_slots,
+                                int64_t ts_min, int tsbits, int mode, uint32_t reject_rank,
+                                uint64_t* keys, uint32_t* vals, uint32_t* srank) {
+    const uint64_t h = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (h >= n_heads) return;
+    auto put = [&](uint64_t i, uint32_t r) {
+        uint64_t t = 0;
+        if ((code[i] & kCodeMask) == kCodeRejected) r = reject_rank;
+        else t = static_cast<uint64_t>(ts[i]) - static_cast<uint64_t>(ts_min);
+        keys[i] = mode == 0 ? ((static_cast<uint64_t>(r) << tsbits) | t) : t;
+        vals[i] = static_cast<uint32_t>(i);
+        srank[i] = r;
+    };
+    if (h == 0)
+        for (uint64_t i = 0; i < hslot[0]; ++i) put(i, reject_rank);
+    const uint64_t end = h + 1 < n_heads ? hslot[h + 1] : n_slots;
+    const uint32_t r = hrank[h];
+    for (uint64_t i = hslot[h]; i < end; ++i) put(i, r);
+}
+
 __global__ void slot_jstart_kernel(const uint32_t* perm, const uint32_t* srank, uint64_t n,
                                    uint32_t reject_rank, uint32_t* jstart) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -849,9 +872,15 @@ void launch_slot_keys(const uint32_t* hslot, const uint32_t* hrank, uint64_t n_h
                       const int64_t* ts, const uint32_t* code, uint64_t n_slots, int64_t ts_min,
                       int tsbits, int mode, uint32_t reject_rank, uint64_t* keys, uint32_t* vals,
                       uint32_t* srank, cudaStream_t s) {
-    slot_keys_kernel<<<grid_for(n_slots, 256), 256, 0, s>>>(hslot, hrank, n_heads, ts, code,
-                                                            n_slots, ts_min, tsbits, mode,
-                                                            reject_rank, keys, vals, srank);
+    if (n_heads == 0) {
+        slot_keys_kernel<<<grid_for(n_slots, 256), 256, 0, s>>>(hslot, hrank, n_heads, ts, code,
+                                                                n_slots, ts_min, tsbits, mode,
+                                                                reject_rank, keys, vals, srank);
+    } else {
+        run_keys_kernel<<<grid_for(n_heads, 256), 256, 0, s>>>(hslot, hrank, n_heads, ts, code,
+                                                               n_slots, ts_min, tsbits, mode,
+                                                               reject_rank, keys, vals, srank);
+    }
     count_launch();
 }
 
