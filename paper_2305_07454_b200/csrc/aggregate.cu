@@ -598,9 +598,13 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
                 const bool maybe_seen = (seen & bit) != 0;
                 seen |= bit;
                 uint32_t e = n_cells;
-                if (maybe_seen) {
-                    e = 0;
-                    while (e < n_cells && t_g[warp][e][lane] != code) ++e;
+                if (maybe_seen) {  // all entries at once: independent loads, no dependent chain
+                    uint32_t match = 0;
+#pragma unroll
+                    for (int q = 0; q < kLaneCells; ++q)
+                        match |= (t_g[warp][q][lane] == code ? 1u : 0u) << q;
+                    match &= (n_cells >= 32 ? 0xFFFFFFFFu : ((1u << n_cells) - 1u));
+                    e = match ? static_cast<uint32_t>(__ffs(match) - 1) : n_cells;
                 }
                 if (e < n_cells) {
                     cur_sum = t_s[warp][e][lane];
