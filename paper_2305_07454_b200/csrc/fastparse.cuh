@@ -152,7 +152,7 @@ CVLG_HD bool fast_number(const uint32_t* w, const uint8_t* buf, uint32_t b, uint
     const uint32_t a0 = fs_r(x0, x1, sh), a1 = fs_r(x1, x2, sh), a2 = fs_r(x2, x3, sh);
     const int s = 12 - static_cast<int>(n) + (neg ? 1 : 0);  // first byte after the sign
     int q = qguess;
-    const bool hit = q >= s && q >= 4 && (((q < 8 ? a1 : a2) >> (8 * (q & 3))) & 0xFF) == '.';
+    const bool hit = q >= s && q >= 4 && buf[o + q] == '.';
     if (!hit) {  // rightmost point among the field's bytes in the last 8 (else -1)
         const uint32_t z1 = eqflags(a1, 0x2E2E2E2Eu) & bytes_from_rt(s - 4);
         const uint32_t z2 = eqflags(a2, 0x2E2E2E2Eu) & bytes_from_rt(s - 8);
@@ -162,15 +162,17 @@ CVLG_HD bool fast_number(const uint32_t* w, const uint8_t* buf, uint32_t b, uint
     const int D = static_cast<int>(n) - (neg ? 1 : 0) - (q >= 0 ? 1 : 0);  // digits (if one point)
     if (D <= 0) return false;
     if (D <= 8) {
-        uint32_t r1 = a1, r2 = a2;
+        // the last 8 bytes as one 64-bit string (byte 0 = window position 4)
+        const uint64_t a = (static_cast<uint64_t>(a2) << 32) | a1;
+        uint64_t r = a;
         if (q >= 0) {  // bytes at positions <= q take the byte below them
-            const uint32_t s1 = fs_l(a0, a1, 8), s2 = fs_l(a1, a2, 8);
-            const uint32_t m1 = bytes_from_rt(q - 3), m2 = bytes_from_rt(q - 7);  // positions > q
-            r1 = (a1 & m1) | (s1 & ~m1);
-            r2 = (a2 & m2) | (s2 & ~m2);
+            const uint64_t sft = (a << 8) | (a0 >> 24);
+            const uint64_t keep_hi = q >= 11 ? 0ull : (~0ull << (8 * (q - 3)));  // positions > q
+            r = (a & keep_hi) | (sft & ~keep_hi);
         }
-        r1 = keep_from(r1, 8 - D);  // digits occupy [12 - D, 12)
-        r2 = keep_from(r2, 4 - D);
+        const uint64_t dig = ~0ull << (8 * (8 - D));  // digits occupy [12 - D, 12)
+        r = (r & dig) | (0x3030303030303030ull & ~dig);
+        const uint32_t r1 = static_cast<uint32_t>(r), r2 = static_cast<uint32_t>(r >> 32);
         if (!digits3(r1, r2, 0x30303030u)) return false;
         const double x = div_pow10(static_cast<double>(swar4(r1) * 10000u + swar4(r2)), q >= 0 ? 11 - q : 0);
         v = neg ? -x : x;
