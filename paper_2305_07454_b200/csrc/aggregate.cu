@@ -392,9 +392,13 @@ __device__ bool payload_equal(const FoldParams& P, uint64_t la, uint64_t lb) {
 // running (sum, count) is parked in the (cell, journey) hash table and the new cell's is loaded
 // (re-entries continue the same fold), so per-(cell, journey) subtotals are exact.
 constexpr int kFoldWarps = 4;
-constexpr int kChunk = 8;
+constexpr int kChunk = 8;        // slow path window (staged through registers: slot indirection)
+#ifndef CVLG_FOLD_CHUNK
+#define CVLG_FOLD_CHUNK 16
+#endif
+constexpr int kChunkFast = CVLG_FOLD_CHUNK;  // fast path window (cp.async straight to shared)
 #ifndef CVLG_LANE_CELLS
-#define CVLG_LANE_CELLS 16
+#define CVLG_LANE_CELLS 10
 #endif
 constexpr int kLaneCellsFast = CVLG_LANE_CELLS;  // per-lane cell table; a journey visits ~9 cells
 constexpr int kLaneCellsSlow = 10;  // (slow path also stages slot ids and timestamps: less shared memory left)
@@ -422,8 +426,9 @@ __device__ __forceinline__ uint64_t table_find(const FoldParams& P, uint64_t key
 template <bool kSlow>
 __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P) {
     constexpr int kLaneCells = kSlow ? kLaneCellsSlow : kLaneCellsFast;
-    __shared__ uint32_t s_code[kFoldWarps][32][kChunk + 1];
-    __shared__ double s_speed[kFoldWarps][32][kChunk + 1];
+    constexpr int kCh = kSlow ? kChunk : kChunkFast;
+    __shared__ uint32_t s_code[kFoldWarps][32][kCh + 1];
+    __shared__ double s_speed[kFoldWarps][32][kCh + 1];
     __shared__ uint32_t s_slot[kSlow ? kFoldWarps : 1][32][kChunk + 1];
     __shared__ long long s_ts[kSlow ? kFoldWarps : 1][32][kSlow ? kChunk + 1 : 1];
     // per-lane (cell -> running subtotal) table, entry e of lane l at [e][l]
@@ -529,40 +534,57 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
 
     while (__any_sync(0xFFFFFFFFu, active)) {
         const uint64_t left = end - pos;
-        const uint32_t avail = !active ? 0u : (left < kChunk ? static_cast<uint32_t>(left) : kChunk);
-        // ---- stage every lane's next chunk: 32/kChunk lane chunks per coalesced load ----------
-        // (all loads first, then the shared stores: every load of the window is in flight at once)
-        constexpr int kPer = 32 / kChunk;
+        const uint32_t avail = !active ? 0u : (left < kCh ? static_cast<uint32_t>(left) : kCh);
+        // ---- stage every lane's next chunk: 32/kCh lane chunks per coalesced access ----------------
+        constexpr int kPer = 32 / kCh;
         constexpr int kIt = 32 / kPer;
-        uint32_t slv[kIt], cv[kIt];
-        double sv[kIt];
-        const int k = lane % kChunk;
+        const int k = lane % kCh;
+        if constexpr (!kSlow) {  // fast path: cp.async global -> shared, every copy in flight at once
 #pragma unroll
-        for (int it = 0; it < kIt; ++it) {
-            const int src = it * kPer + lane / kChunk;
-            const uint64_t p0 = __shfl_sync(0xFFFFFFFFu, pos, src);
-            const uint32_t a = __shfl_sync(0xFFFFFFFFu, avail, src);
-            const bool in = static_cast<uint32_t>(k) < a;
-            slv[it] = in ? (kSlow ? __ldg(&P.perm[p0 + k]) : static_cast<uint32_t>(p0 + k)) : 0u;
-        }
-        long long tv[kSlow ? kIt : 1];
+            for (int it = 0; it < kIt; ++it) {
+                const int src = it * kPer + lane / kCh;
+                const uint64_t p0 = __shfl_sync(0xFFFFFFFFu, pos, src);
+                const uint32_t a = __shfl_sync(0xFFFFFFFFu, avail, src);
+                if (static_cast<uint32_t>(k) < a) {
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                                     static_cast<uint32_t>(__cvta_generic_to_shared(&s_code[warp][src][k]))),
+                                 "l"(&P.code[p0 + k])
+                                 : "memory");
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                                     static_cast<uint32_t>(__cvta_generic_to_shared(&s_speed[warp][src][k]))),
+                                 "l"(&P.speed[p0 + k])
+                                 : "memory");
+                }
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+        } else {  // (all loads first, then the shared stores: every load of the window in flight)
+            uint32_t slv[kIt], cv[kIt];
+            double sv[kIt];
+            long long tv[kIt];
 #pragma unroll
-        for (int it = 0; it < kIt; ++it) {
-            const int src = it * kPer + lane / kChunk;
-            const uint32_t a = __shfl_sync(0xFFFFFFFFu, avail, src);
-            const bool in = static_cast<uint32_t>(k) < a;
-            cv[it] = in ? __ldg(&P.code[slv[it]]) : 0u;
-            sv[it] = in ? __ldg(&P.speed[slv[it]]) : 0.0;
-            if (kSlow) tv[kSlow ? it : 0] = in ? __ldg(&P.ts[slv[it]]) : 0;
-        }
+            for (int it = 0; it < kIt; ++it) {
+                const int src = it * kPer + lane / kCh;
+                const uint64_t p0 = __shfl_sync(0xFFFFFFFFu, pos, src);
+                const uint32_t a = __shfl_sync(0xFFFFFFFFu, avail, src);
+                const bool in = static_cast<uint32_t>(k) < a;
+                slv[it] = in ? __ldg(&P.perm[p0 + k]) : 0u;
+            }
 #pragma unroll
-        for (int it = 0; it < kIt; ++it) {
-            const int src = it * kPer + lane / kChunk;
-            s_code[warp][src][k] = cv[it];
-            s_speed[warp][src][k] = sv[it];
-            if (kSlow) {
+            for (int it = 0; it < kIt; ++it) {
+                const int src = it * kPer + lane / kCh;
+                const uint32_t a = __shfl_sync(0xFFFFFFFFu, avail, src);
+                const bool in = static_cast<uint32_t>(k) < a;
+                cv[it] = in ? __ldg(&P.code[slv[it]]) : 0u;
+                sv[it] = in ? __ldg(&P.speed[slv[it]]) : 0.0;
+                tv[it] = in ? __ldg(&P.ts[slv[it]]) : 0;
+            }
+#pragma unroll
+            for (int it = 0; it < kIt; ++it) {
+                const int src = it * kPer + lane / kCh;
+                s_code[warp][src][k] = cv[it];
+                s_speed[warp][src][k] = sv[it];
                 s_slot[warp][src][k] = slv[it];
-                s_ts[warp][src][kSlow ? k : 0] = tv[kSlow ? it : 0];
+                s_ts[warp][src][kSlow ? k : 0] = tv[it];
             }
         }
         __syncwarp();
