@@ -186,8 +186,12 @@ __global__ void __launch_bounds__(256) radix_hist8_kernel(const uint64_t* keys, 
     }
 }
 
+// plan[d] for digit d = 1 + (index of the buffer its pass reads: 0 = keys, 1 = alt) when the pass
+// runs, 0 when the digit is constant (skipped); plan[8] = buffer holding the result. Decided on
+// the device, so the host never waits for the histograms.
 __global__ void __launch_bounds__(256) radix_digit_base_kernel(const uint32_t* hist, uint64_t n, uint32_t* base,
-                                                               unsigned long long* constant_mask) {
+                                                               unsigned long long* constant_mask,
+                                                               int d_begin, int d_end, uint32_t* plan) {
     __shared__ uint32_t sm[256 / 32 + 1];
     for (int p = 0; p < 8; ++p) {
         const uint32_t v = hist[p * 256 + threadIdx.x];
@@ -195,11 +199,39 @@ __global__ void __launch_bounds__(256) radix_digit_base_kernel(const uint32_t* h
         base[p * 256 + threadIdx.x] = block_exclusive_scan<256>(v, sm, tot);
         if (v == n) atomicOr(constant_mask, 1ull << p);
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long c = *constant_mask;
+        uint32_t cur = 0;
+        for (int d = 0; d < 8; ++d) {
+            const bool run = d >= d_begin && d < d_end && !((c >> d) & 1);
+            plan[d] = run ? 1 + cur : 0;
+            if (run) cur ^= 1;
+        }
+        plan[8] = cur;
+    }
+}
+
+// keys/vals <- alt when the result ended in the alternate buffers (plan[8] == 1)
+__global__ void radix_result_copy_kernel(uint64_t* keys, uint32_t* vals, const uint64_t* keys_alt,
+                                         const uint32_t* vals_alt, uint64_t n, const uint32_t* plan) {
+    if (plan[8] == 0) return;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        keys[i] = keys_alt[i];
+        vals[i] = vals_alt[i];
+    }
 }
 
 __global__ void __launch_bounds__(kRThreads) radix_onesweep_kernel(
-    const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_out, uint32_t* vals_out, uint64_t n,
-    int shift, const uint32_t* digit_base, uint32_t* status, uint32_t* tile_counter) {
+    uint64_t* keys_a, uint32_t* vals_a, uint64_t* keys_b, uint32_t* vals_b, uint64_t n, int shift,
+    const uint32_t* digit_base, uint32_t* status, uint32_t* tile_counter, const uint32_t* plan) {
+    const uint32_t pl = plan[shift / 8];
+    if (pl == 0) return;  // constant digit: order unchanged, pass skipped
+    const uint64_t* keys_in = pl == 1 ? keys_a : keys_b;
+    const uint32_t* vals_in = pl == 1 ? vals_a : vals_b;
+    uint64_t* keys_out = pl == 1 ? keys_b : keys_a;
+    uint32_t* vals_out = pl == 1 ? vals_b : vals_a;
     __shared__ uint32_t wc[kRWarps][256];
     __shared__ uint32_t tile_off[256];
     __shared__ uint32_t s_tile;
@@ -316,7 +348,7 @@ uint64_t radix_temp_bytes(uint64_t n) {
     const uint64_t tiles = (n + kRTile - 1) / kRTile;
     const uint64_t counts = 256 * tiles;
     const uint64_t legacy = (counts + scan_temp_words(counts) + 16) * 4 + 64;
-    const uint64_t onesweep = (2 * 8 * 256 + 16 + 8 * counts) * 4 + 64;  // hist, base, flags, status
+    const uint64_t onesweep = (2 * 8 * 256 + 2 + 8 + 16 + 8 * counts) * 4 + 64;  // hist, base, mask, counters, plan, status
     return std::max(legacy, onesweep);
 }
 
@@ -324,45 +356,32 @@ void radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32
                       uint64_t n, int begin_bit, int end_bit, void* d_tmp, cudaStream_t s,
                       unsigned long long* d_orand, unsigned long long* h_orand) {
     if (n <= 1 || end_bit <= begin_bit) return;
-    if (n < (1ull << 30) && d_orand && h_orand) {  // one-sweep passes
+    if (n < (1ull << 30) && d_orand && h_orand) {  // one-sweep passes, planned on the device
         const uint32_t n_tiles = static_cast<uint32_t>((n + kRTile - 1) / kRTile);
         uint32_t* hist = static_cast<uint32_t*>(d_tmp);
         uint32_t* dbase = hist + 8 * 256;
         unsigned long long* cmask = reinterpret_cast<unsigned long long*>(dbase + 8 * 256);
         uint32_t* counters = reinterpret_cast<uint32_t*>(cmask + 1);  // 8
-        uint32_t* status = counters + 8;                              // [8][n_tiles][256]
-        cudaMemsetAsync(hist, 0, (2 * 8 * 256 + 16) * 4, s);
+        uint32_t* plan = counters + 8;                                // 9 (+ pad to 16)
+        uint32_t* status = plan + 16;                                 // [digit][n_tiles][256]
+        const int d_begin = begin_bit / 8, d_end = std::min(8, (end_bit + 7) / 8);
+        cudaMemsetAsync(hist, 0, (2 * 8 * 256 + 2 + 8) * 4, s);
+        cudaMemsetAsync(status + static_cast<uint64_t>(d_begin) * n_tiles * 256, 0,
+                        static_cast<uint64_t>(d_end - d_begin) * n_tiles * 256 * 4, s);
         const unsigned hb = static_cast<unsigned>(std::min<uint64_t>((n + 4095) / 4096, 148 * 4));
         radix_hist8_kernel<<<hb, 256, 0, s>>>(keys, n, hist);
         count_launch();
-        radix_digit_base_kernel<<<1, 256, 0, s>>>(hist, n, dbase, cmask);
+        radix_digit_base_kernel<<<1, 256, 0, s>>>(hist, n, dbase, cmask, d_begin, d_end, plan);
         count_launch();
-        cudaMemcpyAsync(h_orand, cmask, 8, cudaMemcpyDeviceToHost, s);
-        cudaStreamSynchronize(s);
-        const uint64_t constant = h_orand[0];
-        int n_pass = 0;
-        for (int shift = begin_bit; shift < end_bit; shift += 8)
-            if (!((constant >> (shift / 8)) & 1)) ++n_pass;
-        if (n_pass) cudaMemsetAsync(status, 0, static_cast<uint64_t>(n_pass) * n_tiles * 256 * 4, s);
-        uint64_t* ki = keys;
-        uint32_t* vi = vals;
-        uint64_t* ko = keys_alt;
-        uint32_t* vo = vals_alt;
-        int p = 0;
-        for (int shift = begin_bit; shift < end_bit; shift += 8) {
-            if ((constant >> (shift / 8)) & 1) continue;  // digit constant: order unchanged
+        for (int d = d_begin; d < d_end; ++d) {
             radix_onesweep_kernel<<<n_tiles, kRThreads, 0, s>>>(
-                ki, vi, ko, vo, n, shift, dbase + (shift / 8) * 256,
-                status + static_cast<uint64_t>(p) * n_tiles * 256, counters + p);
+                keys, vals, keys_alt, vals_alt, n, 8 * d, dbase + d * 256,
+                status + static_cast<uint64_t>(d) * n_tiles * 256, counters + d, plan);
             count_launch();
-            ++p;
-            std::swap(ki, ko);
-            std::swap(vi, vo);
         }
-        if (ki != keys) {
-            cudaMemcpyAsync(keys, ki, n * 8, cudaMemcpyDeviceToDevice, s);
-            cudaMemcpyAsync(vals, vi, n * 4, cudaMemcpyDeviceToDevice, s);
-        }
+        radix_result_copy_kernel<<<static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 148 * 8)), 256, 0, s>>>(
+            keys, vals, keys_alt, vals_alt, n, plan);
+        count_launch();
         return;
     }
     // constant-digit detection
