@@ -48,6 +48,11 @@ def parse_args():
                     help="bounded CPU sample for cpu_baseline / --impl reference")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--days", type=int, default=1,
+                    help="c5 shape: N consecutive days (seeds 1..N, same journey ids every day; the "
+                         "time bin ignores the date, so days fold onto one time-of-day lattice)")
+    ap.add_argument("--fine", action="store_true",
+                    help="c5 grid: 0.01 degree cells and 1-minute bins (1.78 G cells, 14 GB lattice)")
     ap.add_argument("--shuffled", action="store_true",
                     help="adversarial variant (SURVEY §8d): rows shuffled across shards, so the "
                          "full (rank, ts) sort path runs")
@@ -136,8 +141,23 @@ def measured_peak_hbm() -> tuple[float, str]:
 
 
 def generate(journeys: int, shards: int, mean_duration: float, seed: int, mod: int = 1,
-             rem: int = 0):
+             rem: int = 0, days: int = 1):
     from paper_2305_07454_b200.cvlg import synth_day
+    if days > 1:  # c5 shape: day k uses seed + k and date + k; its shards follow day k-1's
+        import datetime
+        import numpy as np
+        if mod != 1:
+            raise SystemExit("--days > 1 is single-GPU only in this bench")
+        blobs, offs, rows = [], [0], 0
+        for k in range(days):
+            d = (datetime.date(2021, 5, 9) + datetime.timedelta(days=k)).isoformat()
+            b, o, r = synth_day(seed=seed + k, journeys=journeys, shards=shards,
+                                mean_duration=mean_duration, day=d)
+            base = offs[-1]
+            offs.extend(base + int(x) for x in o[1:])
+            blobs.append(b)
+            rows += r
+        return np.concatenate(blobs), offs, rows
     if mod == 1:
         return synth_day(seed=seed, journeys=journeys, shards=shards, mean_duration=mean_duration)
     from paper_2305_07454_b200.distributed import synth_day_owned
@@ -211,10 +231,11 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2305_07454_b200 as cvlg
 
-    spec = cvlg.GridSpec()
+    spec = (cvlg.GridSpec(lat_step=0.01, lon_step=0.01, min_step=1) if args.fine
+            else cvlg.GridSpec())
     t_gen = time.perf_counter()
     blob, offs, rows = generate(args.journeys, args.shards, args.mean_duration, seed=1,
-                                mod=world, rem=rank)
+                                mod=world, rem=rank, days=args.days)
     if args.shuffled:
         from paper_2305_07454_b200.cvlg import shuffle_rows
         blob, offs = shuffle_rows(blob, offs, args.shards, seed=7)
@@ -364,7 +385,10 @@ def run_ours(args):
     tfile = ROOT / "profiles" / "decode_traffic.json"
     if tfile.exists():
         try:
-            traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+            tj = json.loads(tfile.read_text())
+            # the capture holds for the workload it was taken on only
+            if tj.get("csv_bytes") == csv_bytes:
+                traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     stage_avg = [sum(s[i] for s in stage) / len(stage) for i in range(4)]
@@ -399,15 +423,21 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generator algorithm, byte-identical; seed 1)",
             "config": {
-                "workload": ("c2: synthetic 50M-point trace, 100k journeys per GPU, device-resident"
+                "workload": (f"c5 shape on 1 GPU: {args.days} consecutive days x {args.journeys} "
+                             "journeys (same ids every day), device-resident"
+                             if args.days > 1 else
+                             "c2: synthetic 50M-point trace, 100k journeys per GPU, device-resident"
                              if args.journeys == 100_000 else
                              f"synthetic trace, {args.journeys} journeys per GPU "
                              f"(c3 = 1,000,000: full-day statewide shape), device-resident")
                             + (" | ADVERSARIAL: rows shuffled across shards (full-sort path)"
-                               if args.shuffled else ""),
+                               if args.shuffled else "")
+                            + (" | fine 1-minute / 0.01 deg lattice" if args.fine else ""),
                 "journeys_per_gpu": args.journeys, "rows_per_gpu": rows, "rows_total": total_rows,
                 "csv_bytes_per_gpu": csv_bytes, "shards": args.shards,
-                "grid": "default GridSpec 46x67x288x4 (3,550,464 cells)",
+                "grid": ("c5 fine grid: 0.01 deg cells, 1-minute bins (T=1440, 460x670: "
+                         f"{1440 * 4 * 460 * 670:,} cells)" if args.fine
+                         else "default GridSpec 46x67x288x4 (3,550,464 cells)"),
                 "l2": "inputs (%.2f GB) larger than L2 (126 MB); no flush needed" % (csv_bytes / 1e9),
                 "parallelism": f"dp{world} (journey-hash shards)",
                 "input_generation_s": round(t_gen, 2),
