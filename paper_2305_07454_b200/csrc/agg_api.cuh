@@ -24,6 +24,8 @@ struct DictParams {
     uint32_t* full;  // set when a probe chain exceeds its bound (host re-runs with more room)
 };
 
+constexpr int kFoldThreads = 128;  // fold CTA size (4 warps, one journey per lane)
+
 struct FoldParams {
     // journeys: [jstart[j], jstart[j+1]) indexes `perm`
     uint64_t n_journeys;
@@ -50,6 +52,16 @@ struct FoldParams {
     double* spill_sum;
     uint32_t* spill_cnt;
     uint64_t spill_mask;
+    // time-bin windows (0 = off): a (cell, journey) subtotal can only be revisited in a window of
+    // the same time bin, so closed windows go straight to the pair list; a later window of an
+    // already-closed bin (another day) reloads that bin's block through the per-lane directory
+    int win;
+    uint32_t drc;             // cells per time bin (D * R * C)
+    uint32_t n_bins;          // T
+    uint32_t epoch;           // directory tag of this launch (>= 1)
+    uint4* dir;               // [lanes][T]: (journey, epoch, pair base, count)
+    uint32_t* dead_list;      // pair slots vacated by reloads
+    uint32_t* dead_count;
     // conflict re-parse
     const uint8_t* csv;
     const uint64_t* shard_off;
@@ -141,6 +153,12 @@ void launch_slot_keys(const uint32_t* hslot, const uint32_t* hrank, uint64_t n_h
 void launch_slot_jstart(const uint32_t* perm, const uint32_t* srank, uint64_t n,
                         uint32_t reject_rank, uint32_t* jstart, cudaStream_t s);
 void launch_fold(const FoldParams& p, bool slow, cudaStream_t s);
+// CTAs of the (persistent) fold launch: the directory holds one row per lane of this grid
+unsigned fold_grid(uint64_t n_journeys, bool slow);
+// moves the live pairs of [0, n) over the `dead` vacated slots: the first n - dead stay live
+void launch_pair_compact(uint64_t* key, double* sum, uint32_t* cnt, uint64_t n, uint64_t dead,
+                         const uint32_t* dead_list, uint32_t* src_list, uint32_t* counters,
+                         cudaStream_t s);
 void launch_pair_vals(uint32_t* vals, uint64_t n, cudaStream_t s);
 void launch_rank_slot(const uint32_t* uslot, const uint32_t* perm, uint64_t n, uint32_t* rank_slot,
                       cudaStream_t s);

@@ -7,6 +7,7 @@
 //   journey ids -> lexicographic ranks, items sorted (rank, sec)  :305-328
 //   cellmap[(g, rank)] += speed in (rank, sec) order              :331-358
 //   finalize: sort by (g, journey), fold subtotals in journey order, f32 narrow :161-204
+#include <algorithm>
 #include <climits>
 
 #include "agg_api.cuh"
@@ -19,6 +20,7 @@ namespace {
 
 constexpr uint64_t kEmpty = ~0ull;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr uint64_t kDeadPair = ~0ull;  // pair slot vacated by a window reload (compacted away)
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
     x ^= x >> 33;
@@ -391,7 +393,7 @@ __device__ bool payload_equal(const FoldParams& P, uint64_t la, uint64_t lb) {
 // Accumulators live in registers while consecutive records share a cell; on a cell change the
 // running (sum, count) is parked in the (cell, journey) hash table and the new cell's is loaded
 // (re-entries continue the same fold), so per-(cell, journey) subtotals are exact.
-constexpr int kFoldWarps = 4;
+constexpr int kFoldWarps = kFoldThreads / 32;
 constexpr int kChunk = 8;        // slow path window (staged through registers: slot indirection)
 #ifndef CVLG_FOLD_CHUNK
 #define CVLG_FOLD_CHUNK 16
@@ -403,11 +405,17 @@ constexpr int kChunkFast = CVLG_FOLD_CHUNK;  // fast path window (cp.async strai
 constexpr int kLaneCellsFast = CVLG_LANE_CELLS;  // per-lane cell table; a journey visits ~9 cells
 constexpr int kLaneCellsSlow = 10;  // (slow path also stages slot ids and timestamps: less shared memory left)
 
+constexpr uint64_t kSpillProbes = 4096;
+constexpr uint32_t kBinSpilled = 0x80000000u;  // t_c flag: this entry's time-bin window spilled
+
 __device__ __forceinline__ uint64_t table_find(const FoldParams& P, uint64_t key, bool insert,
                                                bool& fresh) {
     uint64_t slot = mix64(key) & P.spill_mask;
     fresh = false;
-    for (uint64_t probe = 0; probe <= P.spill_mask; ++probe) {
+    // probes are bounded (inserts that give up count as overflow: the host re-runs with a larger
+    // table), so a lookup that stops at the same bound is still exact
+    const uint64_t limit = P.spill_mask < kSpillProbes ? P.spill_mask + 1 : kSpillProbes;
+    for (uint64_t probe = 0; probe < limit; ++probe) {
         uint64_t cur = P.spill_key[slot];
         if (cur == kEmpty && insert) {
             cur = atomicCAS(reinterpret_cast<unsigned long long*>(&P.spill_key[slot]), kEmpty, key);
@@ -462,6 +470,12 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
     int64_t prev_ts = 0;
     uint64_t surv = 0;
     bool have_prev = false;
+    // time-bin windows: entries [0, wstart) belong to closed windows, [wstart, n_cells) to the
+    // current one; bins of closed windows are covered by the current segment [seg_lo, cur_tb]
+    // (bins rise along a segment) and up to four older segment hulls (lo | hi << 16)
+    uint32_t wstart = 0, wlo = 0, cur_tb = kNone, seg_lo = 0;
+    uint32_t iv0 = 0xFFFFu, iv1 = 0xFFFFu, iv2 = 0xFFFFu, iv3 = 0xFFFFu;
+    const uint64_t dir_row = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * P.n_bins;
 
     auto start_journey = [&]() {
         cur_g = kNone;
@@ -470,6 +484,9 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
         evict = 0;
         spilled = false;
         have_prev = false;
+        wstart = 0;
+        cur_tb = kNone;
+        iv0 = iv1 = iv2 = iv3 = 0xFFFFu;
         if (kSlow) {
             pos = P.jstart[j];
             end = P.jstart[j + 1];
@@ -505,7 +522,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
             return;
         }
         P.spill_sum[t] = s;
-        P.spill_cnt[t] = c;
+        P.spill_cnt[t] = c & ~kBinSpilled;
     };
     // write the whole journey out: appended pairs, or the spill table once it has spilled
     auto flush_journey = [&]() {
@@ -523,12 +540,82 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
                 }
                 P.pair_key[at] = (static_cast<uint64_t>(t_g[warp][e][lane]) << P.rank_bits) | j;
                 P.pair_sum[at] = t_s[warp][e][lane];
-                P.pair_cnt[at] = t_c[warp][e][lane];
+                P.pair_cnt[at] = t_c[warp][e][lane] & ~kBinSpilled;
             }
         } else {
             for (uint32_t e = 0; e < n_cells; ++e)
                 spill_store(t_g[warp][e][lane], t_s[warp][e][lane], t_c[warp][e][lane]);
         }
+    };
+    // closed-window entries [0, upto) -> pair list at `base` (one directory block per time bin,
+    // entries of one bin are adjacent in the table), then the rest of the table moves down
+    auto flush_closed = [&](uint32_t upto, uint32_t base) {
+        uint32_t e = 0;
+        while (e < upto) {
+            const uint32_t tb = t_g[warp][e][lane] / P.drc;
+            const uint32_t lo = tb * P.drc;
+            uint32_t f = e, flag = 0;
+            do {
+                const uint64_t at = static_cast<uint64_t>(base) + f;
+                const uint32_t cn = t_c[warp][f][lane];
+                flag |= cn & kBinSpilled;
+                if (at < P.pair_cap) {
+                    P.pair_key[at] = (static_cast<uint64_t>(t_g[warp][f][lane]) << P.rank_bits) | j;
+                    P.pair_sum[at] = t_s[warp][f][lane];
+                    P.pair_cnt[at] = cn & ~kBinSpilled;
+                } else {
+                    ++c_ovf;
+                }
+                ++f;
+            } while (f < upto && t_g[warp][f][lane] - lo < P.drc);
+            P.dir[dir_row + tb] = make_uint4(static_cast<uint32_t>(j), P.epoch, base + e, (f - e) | flag);
+            e = f;
+        }
+        for (uint32_t q = upto; q < n_cells; ++q) {
+            t_g[warp][q - upto][lane] = t_g[warp][q][lane];
+            t_s[warp][q - upto][lane] = t_s[warp][q][lane];
+            t_c[warp][q - upto][lane] = t_c[warp][q][lane];
+        }
+        n_cells -= upto;
+        cur = cur >= upto ? cur - upto : 0;
+        wstart = wstart >= upto ? wstart - upto : 0;
+    };
+    auto in_segments = [&](uint32_t tb) {
+        auto in = [&](uint32_t iv) { return tb >= (iv & 0xFFFFu) && tb <= (iv >> 16); };
+        return in(iv0) || in(iv1) || in(iv2) || in(iv3);
+    };
+    auto push_segment = [&](uint32_t lo, uint32_t hi) {
+        const uint32_t l3 = min(iv3 & 0xFFFFu, iv2 & 0xFFFFu), h3 = max(iv3 >> 16, iv2 >> 16);
+        iv3 = l3 | (h3 << 16);  // oldest two merge into their hull (a superset: still exact-safe)
+        iv2 = iv1;
+        iv1 = iv0;
+        iv0 = lo | (hi << 16);
+    };
+    // a window of an already-closed bin opened: bring back that bin's flushed block (if any);
+    // a bin whose window spilled has more of its subtotals in the spill table: the window
+    // continues in spilled state (lookups)
+    auto reopen = [&](uint32_t tb) {
+        if (n_cells) {  // every entry is closed now: flush them (keeps bins contiguous)
+            const uint32_t base = atomicAdd(P.pair_count, n_cells);
+            flush_closed(n_cells, base);
+        }
+        const uint4 d = P.dir[dir_row + tb];
+        if (d.x == static_cast<uint32_t>(j) && d.y == P.epoch) {
+            const uint32_t cnt = d.w & ~kBinSpilled;
+            const uint32_t dl = atomicAdd(P.dead_count, cnt);
+            for (uint32_t q = 0; q < cnt; ++q) {
+                const uint64_t at = static_cast<uint64_t>(d.z) + q;
+                t_g[warp][q][lane] = static_cast<uint32_t>(P.pair_key[at] >> P.rank_bits);
+                t_s[warp][q][lane] = P.pair_sum[at];
+                t_c[warp][q][lane] = P.pair_cnt[at] | (d.w & kBinSpilled);
+                P.pair_key[at] = kDeadPair;
+                P.dead_list[dl + q] = static_cast<uint32_t>(at);
+            }
+            n_cells = cnt;
+            spilled = (d.w & kBinSpilled) != 0;
+            P.dir[dir_row + tb] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        wstart = 0;
     };
     if (active) start_journey();
 
@@ -616,6 +703,24 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
                     t_s[warp][cur][lane] = cur_sum;
                     t_c[warp][cur][lane] = cur_cnt;
                 }
+                if (P.win && (cur_tb == kNone || code - wlo >= P.drc)) {  // a new time-bin window
+                    const uint32_t tb = code / P.drc;
+                    wlo = tb * P.drc;
+                    bool again = false;
+                    if (cur_tb != kNone) {
+                        if (tb < cur_tb) {  // bins fell (midnight, next day): a new segment
+                            push_segment(seg_lo, cur_tb);
+                            seg_lo = tb;
+                        }
+                        again = in_segments(tb);
+                    } else {
+                        seg_lo = tb;
+                    }
+                    cur_tb = tb;
+                    wstart = n_cells;
+                    spilled = false;  // (window mode: spilled is per window)
+                    if (again) reopen(tb);
+                }
                 const uint64_t bit = 1ull << ((code * 0x9E3779B1u) >> 26);
                 const bool maybe_seen = (seen & bit) != 0;
                 seen |= bit;
@@ -632,6 +737,10 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
                     cur_sum = t_s[warp][e][lane];
                     cur_cnt = t_c[warp][e][lane];
                 } else {
+                    if (n_cells == kLaneCells && wstart > 0) {  // room: flush closed windows
+                        const uint32_t base = atomicAdd(P.pair_count, wstart);
+                        flush_closed(wstart, base);
+                    }
                     if (n_cells < kLaneCells) {
                         e = n_cells++;
                     } else {  // table full: move the oldest-assigned entry to the spill table
@@ -641,14 +750,15 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
                         spilled = true;
                     }
                     cur_sum = 0.0;
-                    cur_cnt = 0;
+                    cur_cnt = P.win && spilled ? kBinSpilled : 0u;  // (marks the bin's block)
                     if (spilled && maybe_seen) {  // the cell may have been evicted earlier: continue its fold
                         bool fresh;
                         const uint64_t t = table_find(P, (static_cast<uint64_t>(code) << 32) | j,
                                                       false, fresh);
-                        if (t != kEmpty) {
+                        if (t != kEmpty && P.spill_cnt[t]) {
                             cur_sum = P.spill_sum[t];
-                            cur_cnt = P.spill_cnt[t];
+                            cur_cnt |= P.spill_cnt[t];
+                            P.spill_cnt[t] = 0;  // moved back out (a later eviction re-fills it)
                         }
                     }
                     t_g[warp][e][lane] = code;
@@ -660,6 +770,18 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
             ++cur_cnt;
         }
         __syncwarp();
+        // ---- flush closed windows of nearly full tables, one pair-list reservation per warp ------
+        if (P.win) {
+            const bool want = active && wstart > 0 && n_cells + 3 >= kLaneCells;
+            if (__any_sync(0xFFFFFFFFu, want)) {
+                const uint32_t c = want ? wstart : 0u;
+                const uint32_t incl = warp_inclusive_sum(c);
+                uint32_t base = 0;
+                if (lane == 31) base = atomicAdd(P.pair_count, incl);
+                base = __shfl_sync(0xFFFFFFFFu, base, 31);
+                if (want) flush_closed(wstart, base + incl - c);
+            }
+        }
         // ---- advance the stream ----------------------------------------------------------------
         if (!kSlow && active && jn < P.n_journeys) {  // advance the next-journey prefetch
             if (jstage == 0) {
@@ -719,7 +841,7 @@ __global__ void spill_drain_kernel(FoldParams P) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (i > P.spill_mask) return;
     const uint64_t k = P.spill_key[i];
-    if (k == kEmpty) return;
+    if (k == kEmpty || P.spill_cnt[i] == 0) return;  // (cnt 0: moved back out by its lane)
     const uint32_t pos = atomicAdd(P.pair_count, 1u);
     if (pos >= P.pair_cap) {
         atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[kStOverflow]), 1ull);
@@ -916,6 +1038,57 @@ void launch_slot_jstart(const uint32_t* perm, const uint32_t* srank, uint64_t n,
     count_launch();
 }
 
+// enough lanes for every journey, capped at what is resident at once (journeys are handed out
+// dynamically, so CTAs beyond the resident set would find nothing left to do)
+unsigned fold_grid(uint64_t n_journeys, bool slow) {
+    static int per_sm[2] = {0, 0};
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], fold_lane_kernel<false>, kFoldWarps * 32, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], fold_lane_kernel<true>, kFoldWarps * 32, 0);
+        if (sms <= 0) sms = 148;
+    }
+    const uint64_t cap = static_cast<uint64_t>(sms) * std::max(1, per_sm[slow ? 1 : 0]);
+    return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n_journeys + kFoldWarps * 32 - 1) / (kFoldWarps * 32), cap)));
+}
+
+// live pairs of the tail [n - dead, n) -> src list (any order)
+__global__ void pair_tail_live_kernel(const uint64_t* key, uint64_t n, uint64_t dead, uint32_t* src,
+                                      uint32_t* counter) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i >= dead) return;
+    const uint64_t at = n - dead + i;
+    if (key[at] != kDeadPair) src[atomicAdd(counter, 1u)] = static_cast<uint32_t>(at);
+}
+
+// vacated slots of the head [0, n - dead) take the tail's live pairs
+__global__ void pair_fill_kernel(uint64_t* key, double* sum, uint32_t* cnt, uint64_t n, uint64_t dead,
+                                 const uint32_t* dead_list, const uint32_t* src, uint32_t* counter) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i >= dead) return;
+    const uint32_t at = dead_list[i];
+    if (at >= n - dead) return;
+    const uint32_t from = src[atomicAdd(counter, 1u)];
+    key[at] = key[from];
+    sum[at] = sum[from];
+    cnt[at] = cnt[from];
+}
+
+void launch_pair_compact(uint64_t* key, double* sum, uint32_t* cnt, uint64_t n, uint64_t dead,
+                         const uint32_t* dead_list, uint32_t* src_list, uint32_t* counters,
+                         cudaStream_t s) {
+    if (!dead) return;
+    cudaMemsetAsync(counters, 0, 8, s);
+    pair_tail_live_kernel<<<grid_for(dead, 256), 256, 0, s>>>(key, n, dead, src_list, counters);
+    pair_fill_kernel<<<grid_for(dead, 256), 256, 0, s>>>(key, sum, cnt, n, dead, dead_list, src_list,
+                                                         counters + 1);
+    count_launch();
+    count_launch();
+}
+
 void launch_fold(const FoldParams& p, bool slow, cudaStream_t s) {
     if (!slow && p.n_heads) {
         run_list_kernel<<<grid_for(p.n_heads, 256), 256, 0, s>>>(p.perm, p.hslot, p.hend, p.n_heads,
@@ -923,11 +1096,7 @@ void launch_fold(const FoldParams& p, bool slow, cudaStream_t s) {
         count_launch();
     }
     if (p.n_journeys) {
-        const uint64_t warps = p.n_journeys;
-        const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((warps + 7) / 8, 148ull * 64));
-        (void)blocks;
-        // enough lanes for every journey, capped at the resident capacity (dynamic assignment)
-        const unsigned lb = static_cast<unsigned>(std::min<uint64_t>((p.n_journeys + kFoldWarps * 32 - 1) / (kFoldWarps * 32), 148ull * 16));
+        const unsigned lb = fold_grid(p.n_journeys, slow);
         if (slow) fold_lane_kernel<true><<<lb, kFoldWarps * 32, 0, s>>>(p);
         else fold_lane_kernel<false><<<lb, kFoldWarps * 32, 0, s>>>(p);
         count_launch();

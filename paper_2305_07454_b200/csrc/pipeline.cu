@@ -54,14 +54,15 @@ void cuda_check(cudaError_t e, const char* what) {
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
-    void ensure(size_t bytes) {
-        if (bytes <= cap && p) return;
+    bool ensure(size_t bytes) {  // true when (re)allocated: contents undefined
+        if (bytes <= cap && p) return false;
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
         const size_t want = std::max<size_t>(bytes, 256);
         CK(cudaMalloc(&p, want));
         cap = want;
+        return true;
     }
     template <typename T>
     T* as() const { return static_cast<T*>(p); }
@@ -203,7 +204,8 @@ struct cvlg_context {
     uint64_t f_J = 0, f_cells = 0;
     DevBuf dict, hdict, flags, pos, uslot, rank_of_slot, hrank, scal;
     DevBuf keys, vals, keys_alt, vals_alt, sort_tmp, scan_tmp, srank, jstart;
-    DevBuf pair_key, pair_sum, pair_cnt, spill_key, spill_sum, spill_cnt;
+    DevBuf pair_key, pair_sum, pair_cnt, spill_key, spill_sum, spill_cnt, fold_dir, dead;
+    uint32_t fold_epoch = 0;
     DevBuf planes, raw, rank_slot, x_keys, x_sum, x_cnt;
     HostPinned h_small, h_csv;
     // last cvlg_partial_device run: pairs kept in pair_key/pair_sum/pair_cnt
@@ -621,9 +623,11 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         // ---- per-journey fold ------------------------------------------------------------------
         const int rbits = bits_for(J - 1);
         const uint64_t pair_bound = slow ? n_parsed : std::min<uint64_t>(n_parsed, H + transitions);
-        c->pair_key.ensure(pair_bound * 8 + 8);
-        c->pair_sum.ensure(pair_bound * 8 + 8);
-        c->pair_cnt.ensure(pair_bound * 4 + 4);
+        // time-bin windows write a reloaded bin's pairs twice (the first copy is vacated): margin
+        const uint64_t pair_room = std::min<uint64_t>(pair_bound + pair_bound / 2 + 1024, 0xFFFFFFF0ull);
+        c->pair_key.ensure(pair_room * 8 + 8);
+        c->pair_sum.ensure(pair_room * 8 + 8);
+        c->pair_cnt.ensure(pair_room * 4 + 4);
         uint32_t* d_pairs = c->scal.as<uint32_t>() + 13;
         FoldParams F;
         F.n_journeys = J;
@@ -643,7 +647,6 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         F.pair_sum = c->pair_sum.as<double>();
         F.pair_cnt = c->pair_cnt.as<uint32_t>();
         F.pair_count = d_pairs;
-        F.pair_cap = pair_bound;
         F.rank_bits = rbits;
         F.journey_counter = c->scal.as<uint64_t>() + 7;
         F.csv = d_csv;
@@ -651,10 +654,37 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         F.cmap = P.cmap;
         F.n_shards = n_shards;
         F.stats = d_stats;
+        // time-bin windows: a directory row of T entries per fold lane (off when it would not fit
+        // comfortably, or when disabled)
+        const uint64_t dir_bytes = static_cast<uint64_t>(fold_grid(J, slow)) * kFoldThreads * dims.T * 16;
+        const char* wenv = std::getenv("CVLG_FOLD_WINDOWS");
+        F.win = (wenv && wenv[0] == '0') ? 0 : (dir_bytes <= (4ull << 30) ? 1 : 0);
+        F.drc = static_cast<uint32_t>(dims.D * dims.RC);
+        F.n_bins = dims.T;
+        F.dir = nullptr;
+        F.dead_count = c->scal.as<uint32_t>() + 24;
+        if (F.win) {
+            if (c->fold_dir.ensure(dir_bytes)) {
+                CK(cudaMemsetAsync(c->fold_dir.p, 0, c->fold_dir.cap, s));
+                c->fold_epoch = 0;
+            }
+            F.dir = c->fold_dir.as<uint4>();
+            c->dead.ensure(pair_room * 8 + 8);
+            F.dead_list = c->dead.as<uint32_t>();
+        }
         // The spill table only holds journeys with more distinct cells than a lane keeps in
-        // shared memory; start small and re-run with the exact bound if it ever fills.
-        uint64_t scap = pow2_at_least(std::max<uint64_t>(1u << 18, pair_bound / 2));
+        // shared memory (or a window holds); start small and re-run with the exact bound (and
+        // without windows) if it ever fills.
+        uint64_t scap = pow2_at_least(std::max<uint64_t>(F.win ? 1u << 20 : 1u << 18,
+                                                         pair_bound / (F.win ? 16 : 2)));
+        F.pair_cap = F.win ? pair_room : pair_bound;
         for (int attempt = 0; attempt < 2; ++attempt) {
+            if (++c->fold_epoch == 0) {  // directory tags wrapped: clear the stale ones
+                if (F.dir) CK(cudaMemsetAsync(c->fold_dir.p, 0, c->fold_dir.cap, s));
+                c->fold_epoch = 1;
+            }
+            F.epoch = c->fold_epoch;
+            CK(cudaMemsetAsync(F.dead_count, 0, 4, s));
             c->spill_key.ensure(scap * 8);
             c->spill_sum.ensure(scap * 8);
             c->spill_cnt.ensure(scap * 4);
@@ -669,13 +699,23 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             F.spill_mask = scap - 1;
             launch_fold(F, slow, s);
             CK(cudaMemcpyAsync(hs, d_pairs, 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(hs) + 1, F.dead_count, 4, cudaMemcpyDeviceToHost, s));
             CK(cudaMemcpyAsync(hs + 1, d_stats + kStOverflow, 8, cudaMemcpyDeviceToHost, s));
             sync(c);
             if (hs[1] == 0) break;
             scap = pow2_at_least(2 * pair_bound);
+            F.win = 0;  // the retry is bounded by pair_bound
+            F.pair_cap = pair_bound;
+        }
+        const uint64_t n_written = std::min<uint64_t>(reinterpret_cast<uint32_t*>(hs)[0], F.pair_cap);
+        const uint64_t n_dead = F.win ? reinterpret_cast<uint32_t*>(hs)[1] : 0;
+        if (n_dead) {
+            launch_pair_compact(c->pair_key.as<uint64_t>(), c->pair_sum.as<double>(),
+                                c->pair_cnt.as<uint32_t>(), n_written, n_dead, F.dead_list,
+                                F.dead_list + pair_room, c->scal.as<uint32_t>() + 26, s);
         }
         CK(cudaEventRecord(c->ev[3], s));
-        const uint64_t n_pairs = std::min<uint64_t>(static_cast<uint32_t*>(static_cast<void*>(hs))[0], pair_bound);
+        const uint64_t n_pairs = n_written - n_dead;
 
         if (feat) {  // per-journey features over the fold's record order (features.cu)
             c->f_J = J;

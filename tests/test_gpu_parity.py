@@ -353,3 +353,62 @@ def test_shuffled_10m_rows_bitexact(ref, tmp_path):
     assert d == "", d
     assert stats_dict(st) == est
     assert est["rows_read"] == rows
+
+
+def _commuter_days(n_journeys, days, cells, seed):
+    """Every journey drives in the same 10 minutes of every day, hopping among `cells` nearby
+    0.01-degree cells with random headings: each day reopens the time bins of the previous days
+    (the fold's time-bin-window reload path); > 10 cells per window overflows the lane table."""
+    rng = random.Random(seed)
+    hmax = 80.0 if cells <= 8 else 360.0  # one heading sector: <= cells codes per window
+    out = []
+    for d in range(days):
+        lines = []
+        for j in range(n_journeys):
+            base_lat = 37.0 + (j % 40) * 0.05
+            base_lon = -93.0 + (j // 40) * 0.05
+            pts = [(base_lat + 0.01 * (k % 4) + 0.003, base_lon + 0.01 * (k // 4) + 0.004)
+                   for k in range(cells)]
+            for sec in range(0, 600, 3 + j % 3):
+                la, lo = pts[rng.randrange(cells)]
+                lines.append(b"c%05d,2021-05-%02d 08:%02d:%02d,%.6f,%.6f,65101,%.2f,%.2f" % (
+                    j, 9 + d, sec // 60, sec % 60, la, lo, rng.uniform(0, 80), rng.uniform(0, hmax)))
+        out.append(HEADER + b"\n" + b"\n".join(lines) + b"\n")
+    return out
+
+
+@pytest.mark.parametrize("windows", ["1", "0"])
+def test_fine_grid_reopened_bins(ref, tmp_path, monkeypatch, windows):
+    """c5's fine lattice (1-minute bins, 0.01-degree cells) over days that revisit the same time
+    bins: reloads of flushed window blocks, spilled windows, and the same with the window path off."""
+    import paper_2305_07454_b200 as cvlg
+    monkeypatch.setenv("CVLG_FOLD_WINDOWS", windows)
+    fine = cvlg.GridSpec(lat_step=0.01, lon_step=0.01, min_step=1)
+    for cells, days in ((6, 4), (16, 3)):
+        paths = write_shards(tmp_path / f"c{cells}", _commuter_days(300, days, cells, seed=cells))
+        assert_parity(ref, paths, fine)
+        assert_parity(ref, shuffle_rows(paths, tmp_path / f"s{cells}", 3, seed=5), fine)
+
+
+def test_c5_shape_fine_grid_7_days_bitexact(ref, tmp_path):
+    """configs[4]'s shape on one GPU: 7 consecutive days of the bench generator with the same
+    journey ids (10k journeys, ~35M rows) on the 1-minute / 0.01-degree lattice."""
+    import datetime
+    import os
+    import paper_2305_07454_b200 as cvlg
+    blobs = []
+    for k in range(7):
+        d = (datetime.date(2021, 5, 9) + datetime.timedelta(days=k)).isoformat()
+        blob, offs, _ = cvlg.synth_day(seed=1 + k, journeys=10_000, shards=2, mean_duration=500.0,
+                                       day=d)
+        blobs += [blob[offs[i]:offs[i + 1]].tobytes() for i in range(2)]
+    paths = write_shards(tmp_path, blobs)
+    fine = cvlg.GridSpec(lat_step=0.01, lon_step=0.01, min_step=1)
+    threads = max(1, min(16, os.cpu_count() or 1))
+    ep, er, est, _ = ref.run_pipeline(paths, fine, None, n_partitions=2 * threads,
+                                      n_threads=threads)
+    st = cvlg.PipelineStats()
+    lat = cvlg.run_pipeline(paths, fine, stats=st)
+    d = diff_lattice(ep, er, lat.planes, lat.raw)
+    assert d == "", d
+    assert stats_dict(st) == est

@@ -15,11 +15,20 @@ ap.add_argument("--journeys", type=int, default=100_000)
 ap.add_argument("--shards", type=int, default=16)
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--shuffle", action="store_true")
+ap.add_argument("--days", type=int, default=1)
+ap.add_argument("--fine", action="store_true")
 a = ap.parse_args()
-blob, offs, rows = cvlg.synth_day(seed=1, journeys=a.journeys, shards=a.shards, mean_duration=500.0)
+if a.days > 1:  # c5 shape: the bench's multi-day generator
+    sys.argv = sys.argv[:1]
+    import bench
+    blob, offs, rows = bench.generate(a.journeys, a.shards, 500.0, seed=1, days=a.days)
+    offs = list(offs)
+else:
+    blob, offs, rows = cvlg.synth_day(seed=1, journeys=a.journeys, shards=a.shards,
+                                      mean_duration=500.0)
 if a.shuffle:  # adversarial variant: the full-sort path
     blob, offs = cvlg.cvlg.shuffle_rows(blob, offs, a.shards, seed=7)
-spec = cvlg.GridSpec()
+spec = cvlg.GridSpec(lat_step=0.01, lon_step=0.01, min_step=1) if a.fine else cvlg.GridSpec()
 T, _, R, C = spec.dims()
 d_csv = torch.from_numpy(blob).cuda()
 d_planes = torch.empty((T, 8, R, C), dtype=torch.int32, device="cuda")
