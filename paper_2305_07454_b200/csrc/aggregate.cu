@@ -613,6 +613,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
             }
             n_cells = cnt;
             spilled = (d.w & kBinSpilled) != 0;
+            seen = ~0ull;  // reloaded (or spilled) codes: search for the rest of this window
             P.dir[dir_row + tb] = make_uint4(0u, 0u, 0u, 0u);
         }
         wstart = 0;
@@ -718,7 +719,8 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
                     }
                     cur_tb = tb;
                     wstart = n_cells;
-                    spilled = false;  // (window mode: spilled is per window)
+                    spilled = false;  // (window mode: spilled and the bloom filter are per window:
+                    seen = 0;         //  no entry of a fresh window's bin exists anywhere)
                     if (again) reopen(tb);
                 }
                 const uint64_t bit = 1ull << ((code * 0x9E3779B1u) >> 26);

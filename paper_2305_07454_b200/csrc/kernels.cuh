@@ -10,11 +10,14 @@
 namespace cvlg {
 
 // ---- decode (K0 header map, K1 tile decode) -------------------------------------------------
-constexpr int kTile = 16384;  // CSV bytes per decode tile
+#ifndef CVLG_TILE
+#define CVLG_TILE 16384
+#endif
+constexpr int kTile = CVLG_TILE;  // CSV bytes per decode tile
 constexpr int kHalo = 128;    // bytes staged past the tile end (fast-path lines are <= 95 bytes)
 constexpr int kPre = 16;      // bytes staged before the tile (previous-byte '\n' test)
-constexpr int kDecodeThreads = 256;
-constexpr int kLineCap = 352;  // data lines handled per pass over a tile
+constexpr int kDecodeThreads = kTile / 64;        // one thread per 64 tile bytes
+constexpr int kLineCap = 352 * kTile / 16384;  // data lines handled per pass over a tile
 
 // Slot word (one per data line): bits 0..30 = cell code (grid.cuh kCode*), bit 31 = run head.
 constexpr uint32_t kHeadBit = 0x80000000u;
