@@ -223,6 +223,10 @@ __global__ void radix_result_copy_kernel(uint64_t* keys, uint32_t* vals, const u
     }
 }
 
+// tile keys/values staged in shared memory in digit order before the scatter: each digit's keys
+// leave the tile as one contiguous run (coalesced stores instead of one sector per key)
+constexpr size_t kOsDynSmem = static_cast<size_t>(kRTile) * (8 + 4);
+
 __global__ void __launch_bounds__(kRThreads) radix_onesweep_kernel(
     uint64_t* keys_a, uint32_t* vals_a, uint64_t* keys_b, uint32_t* vals_b, uint64_t n, int shift,
     const uint32_t* digit_base, uint32_t* status, uint32_t* tile_counter, const uint32_t* plan) {
@@ -232,15 +236,22 @@ __global__ void __launch_bounds__(kRThreads) radix_onesweep_kernel(
     const uint32_t* vals_in = pl == 1 ? vals_a : vals_b;
     uint64_t* keys_out = pl == 1 ? keys_b : keys_a;
     uint32_t* vals_out = pl == 1 ? vals_b : vals_a;
+    extern __shared__ __align__(16) uint8_t os_smem[];
+    uint64_t* sk = reinterpret_cast<uint64_t*>(os_smem);
+    uint32_t* sv = reinterpret_cast<uint32_t*>(sk + kRTile);
     __shared__ uint32_t wc[kRWarps][256];
-    __shared__ uint32_t tile_off[256];
+    __shared__ uint32_t tile_off[256];  // global position of the tile's first key of each digit
+    __shared__ uint32_t dstart[256];    // tile-local position of that key
+    __shared__ uint32_t scan_sm[kRWarps + 1];
     __shared__ uint32_t s_tile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
     for (int i = threadIdx.x; i < kRWarps * 256; i += kRThreads) (&wc[0][0])[i] = 0;
     __syncthreads();
     const uint32_t tile = s_tile;
-    const uint64_t base = static_cast<uint64_t>(tile) * kRTile + static_cast<uint64_t>(warp) * kRWarpKeys;
+    const uint64_t tile0 = static_cast<uint64_t>(tile) * kRTile;
+    const uint64_t base = tile0 + static_cast<uint64_t>(warp) * kRWarpKeys;
+    const uint32_t tile_n = static_cast<uint32_t>(n - tile0 < kRTile ? n - tile0 : kRTile);
     uint64_t k[kRItems];
     uint32_t v[kRItems];
     uint32_t rank[kRItems];
@@ -292,6 +303,9 @@ __global__ void __launch_bounds__(kRThreads) radix_onesweep_kernel(
             }
             st[me] = kOsInc | (excl + run);
         }
+        uint32_t tot;
+        const uint32_t ds = block_exclusive_scan<kRThreads>(run, scan_sm, tot);
+        dstart[d] = ds;
         tile_off[d] = digit_base[d] + excl;
     }
     __syncthreads();
@@ -300,10 +314,18 @@ __global__ void __launch_bounds__(kRThreads) radix_onesweep_kernel(
         const uint64_t idx = base + static_cast<uint64_t>(i) * 32 + lane;
         if (idx < n) {
             const uint32_t d = static_cast<uint32_t>(k[i] >> shift) & 0xFFu;
-            const uint64_t pos = static_cast<uint64_t>(tile_off[d]) + wc[warp][d] + rank[i];
-            keys_out[pos] = k[i];
-            vals_out[pos] = v[i];
+            const uint32_t lp = dstart[d] + wc[warp][d] + rank[i];
+            sk[lp] = k[i];
+            sv[lp] = v[i];
         }
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < tile_n; j += kRThreads) {
+        const uint64_t key = sk[j];
+        const uint32_t d = static_cast<uint32_t>(key >> shift) & 0xFFu;
+        const uint64_t pos = static_cast<uint64_t>(tile_off[d]) + (j - dstart[d]);
+        keys_out[pos] = key;
+        vals_out[pos] = sv[j];
     }
 }
 
@@ -373,8 +395,14 @@ void radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32
         count_launch();
         radix_digit_base_kernel<<<1, 256, 0, s>>>(hist, n, dbase, cmask, d_begin, d_end, plan);
         count_launch();
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(radix_onesweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kOsDynSmem));
+            attr = true;
+        }
         for (int d = d_begin; d < d_end; ++d) {
-            radix_onesweep_kernel<<<n_tiles, kRThreads, 0, s>>>(
+            radix_onesweep_kernel<<<n_tiles, kRThreads, kOsDynSmem, s>>>(
                 keys, vals, keys_alt, vals_alt, n, 8 * d, dbase + d * 256,
                 status + static_cast<uint64_t>(d) * n_tiles * 256, counters + d, plan);
             count_launch();
