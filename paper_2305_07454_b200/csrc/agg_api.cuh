@@ -39,6 +39,9 @@ struct FoldParams {
     const double* speed;
     const uint32_t* code;
     const uint64_t* loff;
+    // slow path: the sorted (rank << span | ts - lo) keys, aligned with perm (nullable): equal keys
+    // within a journey = equal timestamps, read in order instead of gathering ts per slot
+    const uint64_t* skey;
     // (cell, journey) subtotals out: key = cell << rank_bits | rank
     uint64_t* pair_key;
     double* pair_sum;

@@ -649,6 +649,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
             uint32_t slv[kIt], cv[kIt];
             double sv[kIt];
             long long tv[kIt];
+            uint64_t p0s[kIt];
 #pragma unroll
             for (int it = 0; it < kIt; ++it) {
                 const int src = it * kPer + lane / kCh;
@@ -656,6 +657,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
                 const uint32_t a = __shfl_sync(0xFFFFFFFFu, avail, src);
                 const bool in = static_cast<uint32_t>(k) < a;
                 slv[it] = in ? __ldg(&P.perm[p0 + k]) : 0u;
+                p0s[it] = p0;
             }
 #pragma unroll
             for (int it = 0; it < kIt; ++it) {
@@ -664,7 +666,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P
                 const bool in = static_cast<uint32_t>(k) < a;
                 cv[it] = in ? __ldg(&P.code[slv[it]]) : 0u;
                 sv[it] = in ? __ldg(&P.speed[slv[it]]) : 0.0;
-                tv[it] = in ? __ldg(&P.ts[slv[it]]) : 0;
+                tv[it] = !in ? 0 : P.skey ? static_cast<long long>(P.skey[p0s[it] + k]) : __ldg(&P.ts[slv[it]]);
             }
 #pragma unroll
             for (int it = 0; it < kIt; ++it) {

@@ -206,6 +206,7 @@ struct cvlg_context {
     DevBuf keys, vals, keys_alt, vals_alt, sort_tmp, scan_tmp, srank, jstart;
     DevBuf pair_key, pair_sum, pair_cnt, spill_key, spill_sum, spill_cnt, fold_dir, dead;
     uint32_t fold_epoch = 0;
+    bool slow_key_ts = false;
     DevBuf planes, raw, rank_slot, x_keys, x_sum, x_cnt;
     HostPinned h_small, h_csv;
     // last cvlg_partial_device run: pairs kept in pair_key/pair_sum/pair_cnt
@@ -386,6 +387,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
     if (d_raw) CK(cudaMemsetAsync(d_raw, 0, raw_words * 4, s));
 
     bool slow = false;
+    c->slow_key_ts = false;
     uint64_t J = 0;
     if (n_parsed > 0) {
         c->scal.ensure(128);
@@ -612,6 +614,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
                                  c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), NS, 0,
                                  rbits, c->sort_tmp.p, s, d_orand, h_orand);
             }
+            c->slow_key_ts = mode == 0;  // keys hold (rank, ts - lo): the fold's dedup reads them
             launch_slot_jstart(c->vals.as<uint32_t>(), c->srank.as<uint32_t>(), NS,
                                static_cast<uint32_t>(J), jstart, s);
             set_u32_kernel<<<1, 1, 0, s>>>(jstart + J, static_cast<uint32_t>(n_parsed));
@@ -643,6 +646,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         F.speed = c->speed.as<double>();
         F.code = c->code.as<uint32_t>();
         F.loff = c->loff.as<uint64_t>();
+        F.skey = (slow && c->slow_key_ts) ? c->keys.as<uint64_t>() : nullptr;
         F.pair_key = c->pair_key.as<uint64_t>();
         F.pair_sum = c->pair_sum.as<double>();
         F.pair_cnt = c->pair_cnt.as<uint32_t>();
