@@ -57,3 +57,25 @@ def stats_dict(st) -> dict:
         "conflicting_duplicates": st.conflicting_duplicates, "accepted": st.accepted,
         "rejected": dict(st.rejected), "filtered": dict(st.filtered),
     }
+
+
+def commuter_days(n_journeys, days, cells, seed):
+    """Every journey drives in the same 10 minutes of every day, hopping among `cells` nearby
+    0.01-degree cells with random headings: each day reopens the time bins of the previous days
+    (the fold's time-bin-window reload path); > 10 cells per window overflows the lane table."""
+    rng = random.Random(seed)
+    hmax = 80.0 if cells <= 8 else 360.0  # one heading sector: <= cells codes per window
+    out = []
+    for d in range(days):
+        lines = []
+        for j in range(n_journeys):
+            base_lat = 37.0 + (j % 40) * 0.05
+            base_lon = -93.0 + (j // 40) * 0.05
+            pts = [(base_lat + 0.01 * (k % 4) + 0.003, base_lon + 0.01 * (k // 4) + 0.004)
+                   for k in range(cells)]
+            for sec in range(0, 600, 3 + j % 3):
+                la, lo = pts[rng.randrange(cells)]
+                lines.append(b"c%05d,2021-05-%02d 08:%02d:%02d,%.6f,%.6f,65101,%.2f,%.2f" % (
+                    j, 9 + d, sec // 60, sec % 60, la, lo, rng.uniform(0, 80), rng.uniform(0, hmax)))
+        out.append(HEADER + b"\n" + b"\n".join(lines) + b"\n")
+    return out

@@ -121,16 +121,23 @@ def test_slab_owner_partition():
 
 
 @pytest.mark.gpu
-def test_partial_export_finalize_two_shards_on_one_gpu(ref, day_cache, tmp_path):
+@pytest.mark.parametrize("case", ["coarse", "fine_multiday"])
+def test_partial_export_finalize_two_shards_on_one_gpu(ref, day_cache, tmp_path, case):
     """Journey-hash sharding into 2 'ranks' on one GPU: union of exported tuples finalized =
-    the single pipeline = the reference."""
+    the single pipeline = the reference (fine_multiday: the fold's time-bin window reloads and
+    the vacated-pair compaction run inside each rank's partial)."""
     import ctypes
     from pathlib import Path
     import paper_2305_07454_b200 as cvlg
     from paper_2305_07454_b200 import distributed as D
-    from helpers import HEADER, write_shards
+    from helpers import HEADER, commuter_days, write_shards
 
-    paths, _ = day_cache(seed=31, journeys=150)
+    if case == "coarse":
+        paths, _ = day_cache(seed=31, journeys=150)
+        spec = cvlg.GridSpec(lat_step=0.25, lon_step=0.25)
+    else:
+        paths = write_shards(tmp_path / "days", commuter_days(200, 3, 6, seed=2))
+        spec = cvlg.GridSpec(lat_step=0.01, lon_step=0.01, min_step=1)
     rows = []
     for p in paths:
         rows += [l for l in Path(p).read_bytes().split(b"\n")[1:] if l]
@@ -141,7 +148,6 @@ def test_partial_export_finalize_two_shards_on_one_gpu(ref, day_cache, tmp_path)
             h = ((h ^ c) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
         return h
 
-    spec = cvlg.GridSpec(lat_step=0.25, lon_step=0.25)
     T, Dn, R, C = spec.dims()
     tuples = []
     for rank in range(2):

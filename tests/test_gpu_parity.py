@@ -9,7 +9,7 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-from helpers import HEADER, diff_lattice, shuffle_rows, stats_dict, write_shards
+from helpers import HEADER, commuter_days, diff_lattice, shuffle_rows, stats_dict, write_shards
 
 pytestmark = pytest.mark.gpu
 
@@ -355,28 +355,6 @@ def test_shuffled_10m_rows_bitexact(ref, tmp_path):
     assert est["rows_read"] == rows
 
 
-def _commuter_days(n_journeys, days, cells, seed):
-    """Every journey drives in the same 10 minutes of every day, hopping among `cells` nearby
-    0.01-degree cells with random headings: each day reopens the time bins of the previous days
-    (the fold's time-bin-window reload path); > 10 cells per window overflows the lane table."""
-    rng = random.Random(seed)
-    hmax = 80.0 if cells <= 8 else 360.0  # one heading sector: <= cells codes per window
-    out = []
-    for d in range(days):
-        lines = []
-        for j in range(n_journeys):
-            base_lat = 37.0 + (j % 40) * 0.05
-            base_lon = -93.0 + (j // 40) * 0.05
-            pts = [(base_lat + 0.01 * (k % 4) + 0.003, base_lon + 0.01 * (k // 4) + 0.004)
-                   for k in range(cells)]
-            for sec in range(0, 600, 3 + j % 3):
-                la, lo = pts[rng.randrange(cells)]
-                lines.append(b"c%05d,2021-05-%02d 08:%02d:%02d,%.6f,%.6f,65101,%.2f,%.2f" % (
-                    j, 9 + d, sec // 60, sec % 60, la, lo, rng.uniform(0, 80), rng.uniform(0, hmax)))
-        out.append(HEADER + b"\n" + b"\n".join(lines) + b"\n")
-    return out
-
-
 @pytest.mark.parametrize("windows", ["1", "0"])
 def test_fine_grid_reopened_bins(ref, tmp_path, monkeypatch, windows):
     """c5's fine lattice (1-minute bins, 0.01-degree cells) over days that revisit the same time
@@ -385,7 +363,7 @@ def test_fine_grid_reopened_bins(ref, tmp_path, monkeypatch, windows):
     monkeypatch.setenv("CVLG_FOLD_WINDOWS", windows)
     fine = cvlg.GridSpec(lat_step=0.01, lon_step=0.01, min_step=1)
     for cells, days in ((6, 4), (16, 3)):
-        paths = write_shards(tmp_path / f"c{cells}", _commuter_days(300, days, cells, seed=cells))
+        paths = write_shards(tmp_path / f"c{cells}", commuter_days(300, days, cells, seed=cells))
         assert_parity(ref, paths, fine)
         assert_parity(ref, shuffle_rows(paths, tmp_path / f"s{cells}", 3, seed=5), fine)
 
