@@ -666,6 +666,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         F.drc = static_cast<uint32_t>(dims.D * dims.RC);
         F.n_bins = dims.T;
         F.dir = nullptr;
+        F.dead_list = nullptr;
         F.dead_count = c->scal.as<uint32_t>() + 24;
         if (F.win) {
             if (c->fold_dir.ensure(dir_bytes)) {
