@@ -292,12 +292,12 @@ def run_ours(args):
         dist.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
     ms_t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
-    rows_t = torch.tensor([float(rows)], dtype=torch.float64, device=f"cuda:{local}")
+    rows_t = torch.tensor([int(rows)], dtype=torch.int64, device=f"cuda:{local}")
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
         dist.all_reduce(rows_t, op=dist.ReduceOp.SUM)
     ms_max = float(ms_t.item())
-    total_rows = float(rows_t.item())
+    total_rows = int(rows_t.item())
     value = total_rows / (ms_max / 1000.0)
 
     # ---- e2e through the host-buffer C ABI --------------------------------------------------------
