@@ -89,6 +89,7 @@ struct FastState {
     DateCache dc;
     int q[4] = {-1, -1, -1, -1};
 };
+static_assert(sizeof(FastState) % 8 == 4, "odd word stride: conflict-free per-thread state");
 
 // Fast path of parse_record_impl for a line [p, e) (tile-relative) entirely staged in shared
 // memory whose header is canonical: journey, timestamp, latitude, longitude as fields 0..3, then

@@ -223,8 +223,14 @@ struct DateCache {
     uint32_t k0 = 0x30373931u;  // "1970"
     uint32_t k1 = 0x2D31302Du;  // "-01-"
     uint32_t k2 = 0x3130u;      // "01"
-    int64_t day_sec = 0;
+    // days * 86400 as two words: 4-byte alignment keeps FastState at an odd word count (9), so
+    // the per-thread states in shared memory fall on distinct banks
+    uint32_t ds_lo = 0, ds_hi = 0;
 };
+
+CVLG_HD int64_t day_sec(const DateCache& dc) {
+    return static_cast<int64_t>((static_cast<uint64_t>(dc.ds_hi) << 32) | dc.ds_lo);
+}
 
 // validates "YYYY-MM-DD" (datetime.cpp:53-61: month 1..12, day 1..days_in_month) and fills the
 // cache; false -> the general parser decides
@@ -241,7 +247,9 @@ CVLG_HD bool date_refill(uint32_t t0, uint32_t t1, uint32_t t2, DateCache& dc) {
     dc.k0 = t0;
     dc.k1 = t1;
     dc.k2 = t2 & 0xFFFFu;
-    dc.day_sec = days_from_civil(y, static_cast<unsigned>(mo), static_cast<unsigned>(d)) * 86400;
+    const int64_t ds = days_from_civil(y, static_cast<unsigned>(mo), static_cast<unsigned>(d)) * 86400;
+    dc.ds_lo = static_cast<uint32_t>(static_cast<uint64_t>(ds));
+    dc.ds_hi = static_cast<uint32_t>(static_cast<uint64_t>(ds) >> 32);
     return true;
 }
 
@@ -267,7 +275,7 @@ CVLG_HD bool fast_timestamp(const uint32_t* w, uint32_t off, DateCache& dc, int6
     const uint32_t s = (ss & 0xFu) * 10u + ((ss >> 8) & 0xFu);
     if (h > 23 || mi > 59 || s > 59) return false;
     mod = h * 60u + mi;
-    ts = dc.day_sec + static_cast<int64_t>(mod * 60u + s);
+    ts = day_sec(dc) + static_cast<int64_t>(mod * 60u + s);
     return true;
 }
 
