@@ -390,3 +390,39 @@ def test_c5_shape_fine_grid_7_days_bitexact(ref, tmp_path):
     d = diff_lattice(ep, er, lat.planes, lat.raw)
     assert d == "", d
     assert stats_dict(st) == est
+
+
+def test_randomized_differential(ref, day_cache, tmp_path):
+    """48 seeded random cases against cvl::run_pipeline: generator settings (journeys, shard count,
+    sample period < 1 for duplicates, mean duration, bbox partly off-grid), a random valid grid
+    (steps, minute bins, direction sectors and offset), filter rules, optional row shuffling
+    across shards and optional multi-day manifests."""
+    import paper_2305_07454_b200 as cvlg
+    rng = random.Random(2305)
+    steps = [0.5, 0.25, 0.1, 0.05, 0.02, 0.013]
+    mins = [1, 2, 5, 15, 30, 60, 1440]
+    dxns = [(90, 0.0), (90, 45.0), (120, -30.0), (180, 10.0), (360, 0.0)]
+    for case in range(48):
+        seed = 100 + case
+        journeys = rng.choice([5, 20, 60])
+        period = rng.choice([1.0, 1.0, 0.5])
+        bbox = rng.choice([None, (35.0, 41.0, -96.5, -88.5)])
+        paths, _ = day_cache(seed=seed, journeys=journeys, shards=rng.choice([1, 3, 8]),
+                             sample_period=period, mean_duration=rng.choice([60.0, 200.0]),
+                             bbox=bbox)
+        if rng.random() < 0.3:
+            more, _ = day_cache(seed=seed + 1000, journeys=journeys, shards=2, day="2021-05-10")
+            paths = paths + more
+        if rng.random() < 0.3:
+            paths = shuffle_rows(paths, tmp_path / f"s{case}", rng.choice([2, 5]), seed=case)
+        while True:  # a random grid of at most 40M cells (the reference's frames are dense)
+            step = rng.choice(steps)
+            dxn, off = rng.choice(dxns)
+            spec = cvlg.GridSpec(lat_step=step,
+                                 lon_step=rng.choice(steps) if rng.random() < 0.3 else step,
+                                 min_step=rng.choice(mins), dxn_step=dxn, dxn_offset=off)
+            t, d, r, c = spec.dims()
+            if t * d * r * c <= 40_000_000:
+                break
+        rules = cvlg.FilterRules(require_in_grid=True, speed_ceiling=rng.choice([250.0, 100.0]))
+        assert_parity(ref, paths, spec, rules)
