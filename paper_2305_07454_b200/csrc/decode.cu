@@ -521,9 +521,17 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                 }
                 uint8_t why = kNeedGeneral;
                 if (in_smem && kind >= 0) why = fast_parse(bufb, S.cm, p_rel, p_rel + len, kind, fs, o);
-                if (why == kNeedGeneral)
+                if (why == kNeedGeneral) {  // (a separate out-struct: `o` itself never escapes to
+                    LineOut og;              //  the out-of-line call, so it stays in registers)
+                    og.ts = 0;
+                    og.speed = 0.0;
+                    og.id_rel = 0;
+                    og.id_len = 0;
+                    og.minute = kNoMinute;
                     why = general_parse(in_smem ? tile_s + p_rel : gline, static_cast<int32_t>(len), P.cmap[s],
-                                        p_rel, o);
+                                        p_rel, og);
+                    o = og;
+                }
                 uint32_t code = kCodeRejected;
                 if (why == kAccepted) {
                     const uint32_t t = o.minute != kNoMinute ? time_bin_mod(o.minute, P.grid)
