@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
     __shared__ uint64_t sh_off[kMaxShardsInTile + 2];
     __shared__ uint32_t sh_first, sh_count, sh_overflow, sh_good;
     __shared__ int sh_kind;
-    __shared__ unsigned long long sh_send;
+    __shared__ uint32_t sh_send_rel;
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ uint32_t s_cnt[8];  // rejects[4], heads, transitions, accepted, rows
     __shared__ unsigned long long s_ovf[2];
@@ -331,7 +331,10 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
             const bool one = c == 0 && !over;
             sh_kind = one ? canonical_kind(P.cmap[lo]) : -1;
             sh_good = (one && P.shard_good[lo] && tb != P.shard_off[lo]) ? 1u : 0u;
-            sh_send = P.shard_off[lo + 1];
+            {
+                const uint64_t se = P.shard_off[lo + 1] - tb;
+                sh_send_rel = se > 0xFFFFFFFFull ? 0xFFFFFFFFu : static_cast<uint32_t>(se);
+            }
         }
         if (tma) {
             if (b == 0) {
@@ -451,22 +454,23 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                 o.id_rel = 0;
                 o.id_len = 0;
                 const uint32_t p_rel = S.starts[li];
-                const uint64_t p = tb + p_rel;
                 uint32_t s;
-                uint64_t s_end;
+                uint32_t se_rel;  // shard end relative to the tile start (clamped to 32 bits)
                 int kind;
                 if (one_shard) {
                     s = sh_first;
-                    s_end = sh_send;
+                    se_rel = sh_send_rel;
                     kind = sh_kind;
                 } else {
-                    s = shard_of(p);
-                    s_end = P.shard_off[s + 1];
+                    s = shard_of(tb + p_rel);
+                    const uint64_t se = P.shard_off[s + 1] - tb;
+                    se_rel = se > 0xFFFFFFFFull ? 0xFFFFFFFFu : static_cast<uint32_t>(se);
                     kind = canonical_kind(P.cmap[s]);
                 }
-                // line end: next '\n' at or after p (within the staged bytes), clamped to the shard end;
-                // a 96-bit window of the newline bitmap covers every line of <= 95 bytes
-                uint64_t e = 0;
+                // line end (tile-relative): next '\n' at or after p within the staged bytes,
+                // clamped to the shard end; a 96-bit window of the newline bitmap covers every line
+                // of <= 95 bytes
+                uint32_t e_rel = 0;
                 bool found = false;
                 {
                     const uint32_t w = p_rel >> 5, sh = p_rel & 31;
@@ -479,7 +483,7 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                     else if (m2) x = p_rel + 63 + __ffs(m2);
                     if (x != 0xFFFFFFFFu) {
                         if (x < staged_len) {
-                            e = tb + x;
+                            e_rel = x;
                             found = true;
                         }
                     } else {
@@ -488,7 +492,7 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                             if (mm) {
                                 const uint32_t y = 32 * v + (__ffs(mm) - 1);
                                 if (y < staged_len) {
-                                    e = tb + y;
+                                    e_rel = y;
                                     found = true;
                                 }
                                 break;
@@ -496,15 +500,17 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                         }
                     }
                 }
-                if (!found) {
+                if (!found) {  // the line runs past the staged bytes: scan global memory
+                    const uint64_t s_end = tb + se_rel;
                     uint64_t x = tb + staged_len;
                     while (x < P.avail_end && x < s_end && P.csv[x] != '\n') ++x;
-                    e = x;
+                    const uint64_t xr = x - tb;
+                    e_rel = xr > 0xFFFFFFFFull ? 0xFFFFFFFFu : static_cast<uint32_t>(xr);
                 }
-                if (e > s_end) e = s_end;
-                const bool in_smem = e <= stage_end;
-                const uint8_t* gline = P.csv + p;
-                uint32_t len = static_cast<uint32_t>(e - p);
+                if (e_rel > se_rel) e_rel = se_rel;
+                const bool in_smem = e_rel <= staged_len;
+                const uint8_t* gline = P.csv + tb + p_rel;
+                uint32_t len = e_rel - p_rel;
                 const uint8_t last = in_smem ? tile_s[p_rel + len - 1] : gline[len - 1];
                 if (last == '\r') --len;
                 if (len == 0) {  // "\r\n" / "\r<shard end>": empty, not a data line (inert slot)
@@ -512,7 +518,7 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                     const uint64_t slot = slot0 + li;
                     P.out.ts[slot] = 0;
                     P.out.speed[slot] = 0.0;
-                    P.out.loff[slot] = p;
+                    P.out.loff[slot] = tb + p_rel;
                     S.l_ts[li] = 0;
                     S.l_code[li] = kCodeRejected;
                     S.id_rel[li] = 0;
@@ -544,7 +550,7 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                 const uint64_t slot = slot0 + li;
                 P.out.ts[slot] = o.ts;
                 P.out.speed[slot] = o.speed;
-                P.out.loff[slot] = p;
+                P.out.loff[slot] = tb + p_rel;
                 if (P.out.lat) {
                     P.out.lat[slot] = why == kAccepted ? o.lat : 0.0;
                     P.out.lon[slot] = why == kAccepted ? o.lon : 0.0;
