@@ -399,6 +399,7 @@ constexpr int kChunk = 8;        // slow path window (staged through registers: 
 #define CVLG_FOLD_CHUNK 16
 #endif
 constexpr int kChunkFast = CVLG_FOLD_CHUNK;  // fast path window (cp.async straight to shared)
+static_assert(32 % kChunkFast == 0 && 32 % kChunk == 0, "a window staging round covers 32 / kCh lanes");
 #ifndef CVLG_LANE_CELLS
 #define CVLG_LANE_CELLS 10
 #endif
@@ -432,7 +433,10 @@ __device__ __forceinline__ uint64_t table_find(const FoldParams& P, uint64_t key
 }
 
 template <bool kSlow>
-__global__ void __launch_bounds__(kFoldWarps * 32) fold_lane_kernel(FoldParams P) {
+#ifndef CVLG_FOLD_MINB
+#define CVLG_FOLD_MINB 1
+#endif
+__global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_kernel(FoldParams P) {
     constexpr int kLaneCells = kSlow ? kLaneCellsSlow : kLaneCellsFast;
     constexpr int kCh = kSlow ? kChunk : kChunkFast;
     __shared__ uint32_t s_code[kFoldWarps][32][kCh + 1];
