@@ -257,6 +257,7 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
     __shared__ uint32_t sh_send_rel;
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ uint32_t s_cnt[8];  // rejects[4], heads, transitions, accepted, rows
+    __shared__ uint32_t s_inert;
     __shared__ unsigned long long s_ovf[2];
     __shared__ long long c_ts;
     __shared__ uint32_t c_id, c_len, c_code;
@@ -267,6 +268,7 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
         mbar_init(&bar[1], 1);
     }
     if (tid < 8) s_cnt[tid] = 0;
+    if (tid == 8) s_inert = 0;
     __syncthreads();
 
     auto can_tma = [&](uint32_t t) {
@@ -282,15 +284,14 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
     // the per-thread fast-path state lives in shared memory (frees registers for occupancy)
     FastState& fs = reinterpret_cast<FastState*>(S.fs_raw)[tid];
     fs = FastState();
-    uint32_t phase0 = 0, phase1 = 0;
-    uint32_t c_acc = 0, c_inert = 0;
-    const uint32_t G = gridDim.x;
+    uint32_t phases = 0;  // mbarrier phase of buffer b in bit b
+    uint32_t c_acc = 0;
     uint32_t tile = tile_begin + blockIdx.x;
     if (tid == 0 && tile < P.tile_end && can_tma(tile)) issue(tile, 0);
 
-    for (uint32_t it = 0; tile < P.tile_end; ++it, tile += G) {
+    for (uint32_t it = 0; tile < P.tile_end; ++it, tile += gridDim.x) {
         const int b = it & 1;
-        const uint32_t nxt = tile + G;
+        const uint32_t nxt = tile + gridDim.x;
         if (tid == 0 && nxt < P.tile_end && can_tma(nxt)) issue(nxt, b ^ 1);
 
         const uint64_t tb = static_cast<uint64_t>(tile) * kTile;
@@ -337,13 +338,8 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
             }
         }
         if (tma) {
-            if (b == 0) {
-                mbar_wait(&bar[0], phase0);
-                phase0 ^= 1;
-            } else {
-                mbar_wait(&bar[1], phase1);
-                phase1 ^= 1;
-            }
+            mbar_wait(&bar[b], (phases >> b) & 1u);
+            phases ^= 1u << b;
         }
         __syncthreads();
 
@@ -514,7 +510,7 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                 const uint8_t last = in_smem ? tile_s[p_rel + len - 1] : gline[len - 1];
                 if (last == '\r') --len;
                 if (len == 0) {  // "\r\n" / "\r<shard end>": empty, not a data line (inert slot)
-                    ++c_inert;
+                    atomicAdd(&s_inert, 1u);  // rare: a shared counter, not a register
                     const uint64_t slot = slot0 + li;
                     P.out.ts[slot] = 0;
                     P.out.speed[slot] = 0.0;
@@ -689,11 +685,13 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
     }
 
     // ---- stats (once per CTA) ---------------------------------------------------------------------
-    const uint32_t acc = warp_sum(c_acc), inert = warp_sum(c_inert);
+    const uint32_t acc = warp_sum(c_acc);
     if (lane == 0 && acc) atomicAdd(&s_cnt[6], acc);
-    if (lane == 0 && inert) atomicSub(&s_cnt[7], inert);
-    if (lane == 0 && inert)
-        atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[kStInert]), static_cast<unsigned long long>(inert));
+    __syncthreads();
+    if (tid == 0 && s_inert) {
+        s_cnt[7] -= s_inert;
+        atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[kStInert]), static_cast<unsigned long long>(s_inert));
+    }
     __syncthreads();
     if (tid == 0) {
         unsigned long long* st = reinterpret_cast<unsigned long long*>(P.stats);
