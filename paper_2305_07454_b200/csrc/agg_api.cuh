@@ -65,6 +65,7 @@ struct FoldParams {
     uint4* dir;               // [lanes][T]: (journey, epoch, pair base, count)
     uint32_t* dead_list;      // pair slots vacated by reloads
     uint32_t* dead_count;
+    uint32_t* abort_flag;     // set by a failed spill insert: every warp stops (the host re-runs)
     // conflict re-parse
     const uint8_t* csv;
     const uint64_t* shard_off;

@@ -406,7 +406,7 @@ static_assert(32 % kChunkFast == 0 && 32 % kChunk == 0, "a window staging round 
 constexpr int kLaneCellsFast = CVLG_LANE_CELLS;  // per-lane cell table; a journey visits ~9 cells
 constexpr int kLaneCellsSlow = 10;  // (slow path also stages slot ids and timestamps: less shared memory left)
 
-constexpr uint64_t kSpillProbes = 4096;
+constexpr uint64_t kSpillProbes = 512;  // (a full table fails fast; the host re-runs it larger)
 constexpr uint32_t kBinSpilled = 0x80000000u;  // t_c flag: this entry's time-bin window spilled
 
 __device__ __forceinline__ uint64_t table_find(const FoldParams& P, uint64_t key, bool insert,
@@ -523,6 +523,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
         const uint64_t t = table_find(P, (static_cast<uint64_t>(g) << 32) | j, true, fresh);
         if (t == kEmpty) {
             ++c_ovf;
+            atomicExch(P.abort_flag, 1u);
             return;
         }
         P.spill_sum[t] = s;
@@ -624,7 +625,13 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
     };
     if (active) start_journey();
 
+    uint32_t round = 0;
     while (__any_sync(0xFFFFFFFFu, active)) {
+        if ((++round & 31) == 0) {  // a spill insert failed somewhere: this attempt is void, stop
+            uint32_t a = 0;
+            if (lane == 0) a = *reinterpret_cast<volatile const uint32_t*>(P.abort_flag);
+            if (__shfl_sync(0xFFFFFFFFu, a, 0)) break;
+        }
         const uint64_t left = end - pos;
         const uint32_t avail = !active ? 0u : (left < kCh ? static_cast<uint32_t>(left) : kCh);
         // ---- stage every lane's next chunk: 32/kCh lane chunks per coalesced access ----------------

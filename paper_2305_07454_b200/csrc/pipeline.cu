@@ -668,6 +668,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         F.dir = nullptr;
         F.dead_list = nullptr;
         F.dead_count = c->scal.as<uint32_t>() + 24;
+        F.abort_flag = c->scal.as<uint32_t>() + 28;
         if (F.win) {
             if (c->fold_dir.ensure(dir_bytes)) {
                 CK(cudaMemsetAsync(c->fold_dir.p, 0, c->fold_dir.cap, s));
@@ -680,8 +681,9 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         // The spill table only holds journeys with more distinct cells than a lane keeps in
         // shared memory (or a window holds); start small and re-run with the exact bound (and
         // without windows) if it ever fills.
+        // (windows keep most subtotals out of the spill table unless they are long: few bins)
         uint64_t scap = pow2_at_least(std::max<uint64_t>(F.win ? 1u << 20 : 1u << 18,
-                                                         pair_bound / (F.win ? 16 : 2)));
+                                                         pair_bound / (F.win && dims.T > 48 ? 16 : 2)));
         F.pair_cap = F.win ? pair_room : pair_bound;
         for (int attempt = 0; attempt < 2; ++attempt) {
             if (++c->fold_epoch == 0) {  // directory tags wrapped: clear the stale ones
@@ -690,6 +692,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             }
             F.epoch = c->fold_epoch;
             CK(cudaMemsetAsync(F.dead_count, 0, 4, s));
+            CK(cudaMemsetAsync(F.abort_flag, 0, 4, s));
             c->spill_key.ensure(scap * 8);
             c->spill_sum.ensure(scap * 8);
             c->spill_cnt.ensure(scap * 4);
@@ -708,9 +711,14 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             CK(cudaMemcpyAsync(hs + 1, d_stats + kStOverflow, 8, cudaMemcpyDeviceToHost, s));
             sync(c);
             if (hs[1] == 0) break;
+            const bool pairs_full = reinterpret_cast<uint32_t*>(hs)[0] > F.pair_cap;
+            TRACE(pairs_full ? "fold: pair list overflow, re-run without windows"
+                             : "fold: spill table overflow, re-run with a larger table");
             scap = pow2_at_least(2 * pair_bound);
-            F.win = 0;  // the retry is bounded by pair_bound
-            F.pair_cap = pair_bound;
+            if (pairs_full) {  // windows can write more pairs than pair_bound: the retry without
+                F.win = 0;     // them is bounded by it
+                F.pair_cap = pair_bound;
+            }
         }
         const uint64_t n_written = std::min<uint64_t>(reinterpret_cast<uint32_t*>(hs)[0], F.pair_cap);
         const uint64_t n_dead = F.win ? reinterpret_cast<uint32_t*>(hs)[1] : 0;

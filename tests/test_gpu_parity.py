@@ -426,3 +426,25 @@ def test_randomized_differential(ref, day_cache, tmp_path):
                 break
         rules = cvlg.FilterRules(require_in_grid=True, speed_ceiling=rng.choice([250.0, 100.0]))
         assert_parity(ref, paths, spec, rules)
+
+
+def test_daily_bins_fine_cells_spill_retry(ref, tmp_path):
+    """One time bin per day (min_step = 1440) on 0.01-degree cells over 3 days: every journey is a
+    single time-bin window holding ~150 cells, so the fold's window tables spill into the
+    (cell, journey) hash table, which overflows its first size and re-runs larger."""
+    import os
+    import paper_2305_07454_b200 as cvlg
+    blobs = []
+    for k in range(3):
+        blob, offs, _ = cvlg.synth_day(seed=50 + k, journeys=12_000, shards=2, mean_duration=500.0,
+                                       day="2021-05-%02d" % (9 + k))
+        blobs += [blob[offs[i]:offs[i + 1]].tobytes() for i in range(2)]
+    paths = write_shards(tmp_path, blobs)
+    spec = cvlg.GridSpec(lat_step=0.01, lon_step=0.01, min_step=1440)
+    threads = max(1, min(16, os.cpu_count() or 1))
+    ep, er, est, _ = ref.run_pipeline(paths, spec, None, n_partitions=2 * threads, n_threads=threads)
+    st = cvlg.PipelineStats()
+    lat = cvlg.run_pipeline(paths, spec, stats=st)
+    d = diff_lattice(ep, er, lat.planes, lat.raw)
+    assert d == "", d
+    assert stats_dict(st) == est
