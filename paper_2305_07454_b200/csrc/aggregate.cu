@@ -451,7 +451,13 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
     uint32_t c_acc = 0, c_oog = 0, c_spd = 0, c_miss = 0, c_unb = 0, c_dup = 0, c_conf = 0,
              c_ovf = 0;
 
-    uint64_t j = atomicAdd(reinterpret_cast<unsigned long long*>(P.journey_counter), 1ull);
+    // first journey: spread over every CTA and warp (lane-major), so a run with fewer journeys
+    // than lanes still occupies all SMs; later ones come from the shared counter
+    const uint64_t n_lanes = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    auto next_journey = [&]() {
+        return n_lanes + atomicAdd(reinterpret_cast<unsigned long long*>(P.journey_counter), 1ull);
+    };
+    uint64_t j = static_cast<uint64_t>(lane * kFoldWarps + warp) * gridDim.x + blockIdx.x;
     bool active = j < P.n_journeys;
     uint32_t ri = 0, re = 0;    // fast path: remaining runs of the journey, [ri, re) in perm
     // fast path prefetch: the next run of this journey (runs[ri]) and the next journey (its run
@@ -514,7 +520,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
                 nrun = P.runs[ri];
                 jn = ~0ull;
             } else {  // last run open: take the next journey now (not earlier: no hoarding)
-                jn = atomicAdd(reinterpret_cast<unsigned long long*>(P.journey_counter), 1ull);
+                jn = next_journey();
             }
         }
     };
@@ -815,11 +821,11 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
                 end = nrun.y;
                 ++ri;
                 if (ri < re) nrun = P.runs[ri];
-                else jn = atomicAdd(reinterpret_cast<unsigned long long*>(P.journey_counter), 1ull);
+                else jn = next_journey();
             } else {
                 flush_journey();
                 if (kSlow) {
-                    j = atomicAdd(reinterpret_cast<unsigned long long*>(P.journey_counter), 1ull);
+                    j = next_journey();
                 } else {
                     if (jstage == 1) {  // first run of the prefetched journey not in yet
                         jn_run = P.runs[jn_ri];
