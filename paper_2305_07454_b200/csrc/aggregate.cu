@@ -95,12 +95,35 @@ __global__ void densify_kernel(DensifyParams D) {
     const int lane = threadIdx.x & 31;
     const uint4 v = D.tiles[t];
     const uint32_t dst = D.lpos[t];
-    for (uint32_t k = lane; k < v.y; k += 32) {
-        D.ts_out[dst + k] = D.ts[v.x + k];
-        D.speed_out[dst + k] = D.speed[v.x + k];
-        D.code_out[dst + k] = D.code[v.x + k];
-        D.loff_out[dst + k] = D.loff[v.x + k];
-        if (D.lat) {
+    // four rounds of loads in flight before their stores (memory-level parallelism)
+    for (uint32_t k0 = lane; k0 < v.y; k0 += 128) {
+        int64_t ts[4];
+        double sp[4];
+        uint32_t cd[4];
+        uint64_t lo[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t k = k0 + 32u * u;
+            if (k < v.y) {
+                ts[u] = D.ts[v.x + k];
+                sp[u] = D.speed[v.x + k];
+                cd[u] = D.code[v.x + k];
+                lo[u] = D.loff[v.x + k];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t k = k0 + 32u * u;
+            if (k < v.y) {
+                D.ts_out[dst + k] = ts[u];
+                D.speed_out[dst + k] = sp[u];
+                D.code_out[dst + k] = cd[u];
+                D.loff_out[dst + k] = lo[u];
+            }
+        }
+    }
+    if (D.lat) {
+        for (uint32_t k = lane; k < v.y; k += 32) {
             D.lat_out[dst + k] = D.lat[v.x + k];
             D.lon_out[dst + k] = D.lon[v.x + k];
         }
