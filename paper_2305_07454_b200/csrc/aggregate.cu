@@ -75,16 +75,36 @@ __global__ void tile_field_kernel(const uint4* tiles, uint64_t n, int field, uin
 __global__ void heads_compact_kernel(const uint4* tiles, uint64_t n, const uint32_t* hpos,
                                      const uint32_t* hscr, const uint64_t* hid_scr, uint32_t* hslot,
                                      uint32_t* hend, uint64_t* hid) {
-    // one warp per tile: lanes copy the tile's heads
-    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x / 32) + (threadIdx.x >> 5);
-    if (t >= n) return;
+    // one thread per tile (journey-ordered input: a head or two per tile); tiles with many heads
+    // (shuffled rows) are copied by the whole warp afterwards
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     const uint32_t lane = threadIdx.x & 31;
-    const uint4 v = tiles[t];
-    const uint32_t base = hpos[t];
-    for (uint32_t i = lane; i < v.w; i += 32) {
-        hslot[base + i] = hscr[v.z + i];
-        hend[base + i] = i + 1 < v.w ? hscr[v.z + i + 1] : v.x + v.y;
-        hid[base + i] = hid_scr[v.z + i];
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    uint32_t base = 0;
+    if (t < n) {
+        v = tiles[t];
+        base = hpos[t];
+    }
+    const bool small = v.w <= 8;
+    if (small) {
+        for (uint32_t i = 0; i < v.w; ++i) {
+            hslot[base + i] = hscr[v.z + i];
+            hend[base + i] = i + 1 < v.w ? hscr[v.z + i + 1] : v.x + v.y;
+            hid[base + i] = hid_scr[v.z + i];
+        }
+    }
+    uint32_t big = __ballot_sync(0xFFFFFFFFu, !small);
+    while (big) {
+        const int src = __ffs(big) - 1;
+        big &= big - 1;
+        const uint32_t x = __shfl_sync(0xFFFFFFFFu, v.x, src), y = __shfl_sync(0xFFFFFFFFu, v.y, src),
+                       z = __shfl_sync(0xFFFFFFFFu, v.z, src), w = __shfl_sync(0xFFFFFFFFu, v.w, src);
+        const uint32_t bb = __shfl_sync(0xFFFFFFFFu, base, src);
+        for (uint32_t i = lane; i < w; i += 32) {
+            hslot[bb + i] = hscr[z + i];
+            hend[bb + i] = i + 1 < w ? hscr[z + i + 1] : x + y;
+            hid[bb + i] = hid_scr[z + i];
+        }
     }
 }
 
@@ -982,7 +1002,7 @@ void launch_heads_compact(const uint4* tiles, uint64_t n, const uint32_t* hpos, 
                           const uint64_t* hid_scr, uint32_t* hslot, uint32_t* hend, uint64_t* hid,
                           cudaStream_t s) {
     if (!n) return;
-    heads_compact_kernel<<<grid_for(n, 8), 256, 0, s>>>(tiles, n, hpos, hscr, hid_scr, hslot, hend, hid);
+    heads_compact_kernel<<<grid_for(n, 256), 256, 0, s>>>(tiles, n, hpos, hscr, hid_scr, hslot, hend, hid);
     count_launch();
 }
 
