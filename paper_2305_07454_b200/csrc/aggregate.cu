@@ -525,7 +525,16 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
     bool have_prev = false;
     // time-bin windows: entries [0, wstart) belong to closed windows, [wstart, n_cells) to the
     // current one; bins of closed windows are covered by the current segment [seg_lo, cur_tb]
-    // (bins rise along a segment) and up to four older segment hulls (lo | hi << 16)
+    // (bins rise along a segment) and up to four older segment hulls (lo | hi << 16).
+    // Invariants (window mode), which make the fold exact:
+    //  * each (cell, journey) subtotal lives in exactly one place: this lane's table, the live
+    //    directory block of its bin in the pair list, or the spill table (spilled windows only;
+    //    an entry read back from the spill table is marked moved-out there: count 0);
+    //  * one bin's table entries are adjacent (a reopened bin first flushes every closed entry),
+    //    so a flush writes one directory block per bin and dir[bin] names the only live block;
+    //  * reloading a block vacates its pair slots (dead list, compacted after the fold) and
+    //    clears dir[bin];
+    //  * the reopen test is a superset test: a false positive costs one directory read.
     uint32_t wstart = 0, wlo = 0, cur_tb = kNone, seg_lo = 0;
     uint32_t iv0 = 0xFFFFu, iv1 = 0xFFFFu, iv2 = 0xFFFFu, iv3 = 0xFFFFu;
     const uint64_t dir_row = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * P.n_bins;
