@@ -66,6 +66,7 @@ struct FoldParams {
     uint32_t* dead_list;      // pair slots vacated by reloads
     uint32_t* dead_count;
     uint32_t* abort_flag;     // set by a failed spill insert: every warp stops (the host re-runs)
+    uint32_t flush_slack;     // chunk-end flush of closed windows once n_cells + slack >= table size
     // conflict re-parse
     const uint8_t* csv;
     const uint64_t* shard_off;

@@ -845,7 +845,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
         __syncwarp();
         // ---- flush closed windows of nearly full tables, one pair-list reservation per warp ------
         if (P.win) {
-            const bool want = active && wstart > 0 && n_cells + 3 >= kLaneCells;
+            const bool want = active && wstart > 0 && n_cells + P.flush_slack >= kLaneCells;
             if (__any_sync(0xFFFFFFFFu, want)) {
                 const uint32_t c = want ? wstart : 0u;
                 const uint32_t incl = warp_inclusive_sum(c);

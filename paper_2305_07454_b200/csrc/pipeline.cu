@@ -669,6 +669,9 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         F.dead_list = nullptr;
         F.dead_count = c->scal.as<uint32_t>() + 24;
         F.abort_flag = c->scal.as<uint32_t>() + 28;
+        // short windows (fine time bins) close often: flush earlier, in bigger batches (measured:
+        // slack 5 best at 1-minute bins, 1 at 5-minute bins)
+        F.flush_slack = dims.T >= 720 ? 5u : 1u;
         if (F.win) {
             if (c->fold_dir.ensure(dir_bytes)) {
                 CK(cudaMemsetAsync(c->fold_dir.p, 0, c->fold_dir.cap, s));
