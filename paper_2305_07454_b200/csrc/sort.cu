@@ -162,16 +162,54 @@ __global__ void __launch_bounds__(kRThreads) radix_scatter_kernel(
 
 // ---- one-sweep LSD passes ------------------------------------------------------------------------
 // (1) radix_hist8_kernel: global 256-bin histograms of all 8 byte digits in one read of the keys;
-// (2) radix_digit_base_kernel: per pass, exclusive digit offsets + "digit constant" flags (a digit
-//     is constant iff one bin holds every key: the pass is skipped, order unchanged);
+// (2) its last block (radix_digit_base_block): per pass, exclusive digit offsets + "digit
+//     constant" flags (a digit is constant iff one bin holds every key: the pass is skipped, order
+//     unchanged) and the pass plan;
 // (3) radix_onesweep_kernel per remaining pass: tiles taken in order from an atomic counter rank
 //     their keys (stable, as radix_scatter_kernel), publish per-digit counts, and resolve their
 //     per-digit offsets by a decoupled look-back over previous tiles (one 32-bit word per
 //     (tile, digit): 2-bit flag | 30-bit count), then scatter. One launch per pass.
 constexpr uint32_t kOsAgg = 1u << 30, kOsInc = 2u << 30, kOsMask = (1u << 30) - 1;
 
-__global__ void __launch_bounds__(256) radix_hist8_kernel(const uint64_t* keys, uint64_t n, uint32_t* hist) {
+// digit offsets + pass plan from the complete histograms (one block: the last histogram block)
+// plan[d] for digit d = 1 + (index of the buffer its pass reads: 0 = keys, 1 = alt) when the pass
+// runs, 0 when the digit is constant (skipped); plan[8] = buffer holding the result. Decided on
+// the device, so the host never waits for the histograms.
+__device__ void radix_digit_base_block(const uint32_t* hist, uint64_t n, uint32_t* base,
+                                       unsigned long long* constant_mask, int d_begin, int d_end,
+                                       uint32_t* plan) {
+    __shared__ uint32_t sm[256 / 32 + 1];
+    __shared__ unsigned long long cmask;
+    if (threadIdx.x == 0) cmask = 0;
+    __syncthreads();
+    for (int p = 0; p < 8; ++p) {
+        const uint32_t v = __ldcg(&hist[p * 256 + threadIdx.x]);
+        uint32_t tot;
+        base[p * 256 + threadIdx.x] = block_exclusive_scan<256>(v, sm, tot);
+        if (v == n) atomicOr(&cmask, 1ull << p);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long c = cmask;
+        *constant_mask = c;
+        uint32_t cur = 0;
+        for (int d = 0; d < 8; ++d) {
+            const bool run = d >= d_begin && d < d_end && !((c >> d) & 1);
+            plan[d] = run ? 1 + cur : 0;
+            if (run) cur ^= 1;
+        }
+        plan[8] = cur;
+    }
+}
+
+// global 256-bin histograms of all 8 byte digits in one read; the last block to finish derives
+// the digit offsets and the pass plan (no separate launch)
+__global__ void __launch_bounds__(256) radix_hist8_kernel(const uint64_t* keys, uint64_t n, uint32_t* hist,
+                                                          uint32_t* base, unsigned long long* constant_mask,
+                                                          int d_begin, int d_end, uint32_t* plan,
+                                                          uint32_t* done) {
     __shared__ uint32_t h[8][256];
+    __shared__ bool last;
     for (int i = threadIdx.x; i < 8 * 256; i += 256) (&h[0][0])[i] = 0;
     __syncthreads();
     for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < n; i += static_cast<uint64_t>(gridDim.x) * 256) {
@@ -184,32 +222,13 @@ __global__ void __launch_bounds__(256) radix_hist8_kernel(const uint64_t* keys, 
         const uint32_t v = (&h[0][0])[i];
         if (v) atomicAdd(&hist[i], v);
     }
-}
-
-// plan[d] for digit d = 1 + (index of the buffer its pass reads: 0 = keys, 1 = alt) when the pass
-// runs, 0 when the digit is constant (skipped); plan[8] = buffer holding the result. Decided on
-// the device, so the host never waits for the histograms.
-__global__ void __launch_bounds__(256) radix_digit_base_kernel(const uint32_t* hist, uint64_t n, uint32_t* base,
-                                                               unsigned long long* constant_mask,
-                                                               int d_begin, int d_end, uint32_t* plan) {
-    __shared__ uint32_t sm[256 / 32 + 1];
-    for (int p = 0; p < 8; ++p) {
-        const uint32_t v = hist[p * 256 + threadIdx.x];
-        uint32_t tot;
-        base[p * 256 + threadIdx.x] = block_exclusive_scan<256>(v, sm, tot);
-        if (v == n) atomicOr(constant_mask, 1ull << p);
-    }
+    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned long long c = *constant_mask;
-        uint32_t cur = 0;
-        for (int d = 0; d < 8; ++d) {
-            const bool run = d >= d_begin && d < d_end && !((c >> d) & 1);
-            plan[d] = run ? 1 + cur : 0;
-            if (run) cur ^= 1;
-        }
-        plan[8] = cur;
-    }
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    radix_digit_base_block(hist, n, base, constant_mask, d_begin, d_end, plan);
 }
 
 // keys/vals <- alt when the result ended in the alternate buffers (plan[8] == 1)
@@ -387,13 +406,12 @@ void radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32
         uint32_t* plan = counters + 8;                                // 9 (+ pad to 16)
         uint32_t* status = plan + 16;                                 // [digit][n_tiles][256]
         const int d_begin = begin_bit / 8, d_end = std::min(8, (end_bit + 7) / 8);
-        cudaMemsetAsync(hist, 0, (2 * 8 * 256 + 2 + 8) * 4, s);
+        uint32_t* done = plan + 15;  // (plan uses 9 of its 16 words)
+        cudaMemsetAsync(hist, 0, (2 * 8 * 256 + 2 + 8 + 16) * 4, s);
         cudaMemsetAsync(status + static_cast<uint64_t>(d_begin) * n_tiles * 256, 0,
                         static_cast<uint64_t>(d_end - d_begin) * n_tiles * 256 * 4, s);
         const unsigned hb = static_cast<unsigned>(std::min<uint64_t>((n + 4095) / 4096, 148 * 4));
-        radix_hist8_kernel<<<hb, 256, 0, s>>>(keys, n, hist);
-        count_launch();
-        radix_digit_base_kernel<<<1, 256, 0, s>>>(hist, n, dbase, cmask, d_begin, d_end, plan);
+        radix_hist8_kernel<<<hb, 256, 0, s>>>(keys, n, hist, dbase, cmask, d_begin, d_end, plan, done);
         count_launch();
         static bool attr = false;
         if (!attr) {
