@@ -2,26 +2,38 @@
 """Benchmark of the sm_100a CV-ETL hot path (decode -> sort/dedup -> filter -> bin -> aggregate
 -> finalize), BASELINE.json metric "CV records/sec end-to-end ETL ... vs CPU ref".
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c3|c2]
 
-One step = one full pass of the pipeline over the configs[1] workload (c2: synthetic 50M-point
-trace, 100k journeys, default GridSpec) — records are the CSV data rows.
-  value : records/s, CSV already resident in HBM (device-resident API), CUDA events on the
-          pipeline's stream, max over ranks.
-  e2e   : records/s through the C ABI with HOST buffers (pinned), H2D of the CSV and D2H of the
-          lattice inside every step.
-Multi-GPU (torchrun): weak scaling, each rank owns the journeys whose FNV-1a id hash maps to it
-(ingest.cpp:287-301) and processes its own 100k-journey share.
+Workload (default c3 = BASELINE.json configs[2], the largest single-GPU config): the reference
+generator's full-day statewide-shaped trace, 1,000,000 journeys (~499M rows, ~33.8 GB of CSV),
+seed 1, mean_duration 500 s, written as 128 shard files (the generator's own format and names,
+synth.cpp:145-181). Records are the CSV data rows; one step = one full pass of the pipeline over
+the whole trace.
+  e2e   : records/s through the drop-in C ABI cvlg_run_pipeline(paths) (= cvl::run_pipeline,
+          aggregate.hpp:125-127): shard files read from the file system (page cache) through the
+          pinned ingest ring, H2D, decode ... finalize, and the D2H of the lattice, every step.
+  value : records/s of the same pipeline on the same input already resident in HBM (the bytes
+          the e2e run staged; cvlg_run_pipeline_device), CUDA events on the pipeline stream.
+At N > 1 (c4: the same trace sharded by journey-id hash, strong scaling) every rank streams a
+1/N byte range of the files and records are routed to their owner GPU (multi-GPU data plane).
+
+Reference arm (--impl reference): the UNMODIFIED reference cvl::run_pipeline (oracle/_ref, built
+from /root/reference/proj/src) on the SAME shard files, all host threads. It never imports this
+package (its input is written by the reference's own generate_journey when absent). Each step
+is a bounded sample: one eighth of the manifest (every 8th shard; journeys are dealt round-robin
+to shards, synth.cpp:165, so each eighth is a uniform 1/8 of the journeys), cycling so that 8
+steps cover the whole trace.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import shutil
 import statistics
 import subprocess
 import sys
-import tempfile
 import threading
 import time
 from pathlib import Path
@@ -33,52 +45,142 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "CV records/sec end-to-end ETL (1/2/4/8 B200) and % of HBM roofline vs CPU ref"
 UNIT = "records/s"
+GROUPS = 8  # the reference arm's bounded sample: one eighth of the manifest per step
+
+WORKLOADS = {
+    "c3": dict(journeys=1_000_000, shards=128, seed=1, mean_duration=500.0,
+               desc="c3: full-day statewide-shaped synthetic trace (1,000,000 journeys), "
+                    "end-to-end from shard files incl. disk->pinned->H2D"),
+    "c2": dict(journeys=100_000, shards=128, seed=1, mean_duration=500.0,
+               desc="c2: synthetic 50M-point trace, 100k journeys"),
+}
 
 
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--journeys", type=int, default=100_000, help="journeys per rank (c2)")
-    ap.add_argument("--shards", type=int, default=16)
-    ap.add_argument("--mean-duration", type=float, default=500.0)
-    ap.add_argument("--cpu-journeys", type=int, default=10_000,
-                    help="bounded CPU sample for cpu_baseline / --impl reference")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
+    ap.add_argument("--data-dir", default=os.environ.get("CVLG_BENCH_DATA", "/tmp/cvlg_bench"))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--days", type=int, default=1,
-                    help="c5 shape: N consecutive days (seeds 1..N, same journey ids every day; the "
-                         "time bin ignores the date, so days fold onto one time-of-day lattice)")
-    ap.add_argument("--fine", action="store_true",
-                    help="c5 grid: 0.01 degree cells and 1-minute bins (1.78 G cells, 14 GB lattice)")
-    ap.add_argument("--shuffled", action="store_true",
-                    help="adversarial variant (SURVEY §8d): rows shuffled across shards, so the "
-                         "full (rank, ts) sort path runs")
-    ap.add_argument("--no-features", action="store_true",
-                    help="skip the per-journey feature-table timing (extra key, not the metric)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the sampled parity check")
+    ap.add_argument("--threads", type=int, default=0, help="host threads (0 = all)")
     return ap.parse_args()
 
 
 def dist_env():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def maybe_relaunch(args):
+    """--gpus N outside torchrun: re-exec under torch.distributed.run with N ranks."""
+    world = int(os.environ.get("WORLD_SIZE", "0") or 0)
+    if args.gpus > 1 and world == 0:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={29500 + os.getpid() % 1000}", str(Path(__file__).resolve())]
+        cmd += sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
+    if world and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+
+
+# ---- shared input: shard files on the file system ---------------------------------------------
+def dataset_dir(args) -> Path:
+    w = WORKLOADS[args.workload]
+    return Path(args.data_dir) / f"{args.workload}_s{w['seed']}_j{w['journeys']}_n{w['shards']}"
+
+
+def _digest(files: list[Path]) -> str:
+    h = hashlib.sha256()
+    for f in files:
+        sz = f.stat().st_size
+        h.update(f.name.encode() + sz.to_bytes(8, "little"))
+        with open(f, "rb") as fh:
+            h.update(fh.read(4096))
+            if sz > 4096:
+                fh.seek(max(4096, sz - 4096))
+                h.update(fh.read(4096))
+    return h.hexdigest()
+
+
+def load_manifest(d: Path):
+    m = d / "MANIFEST.json"
+    if not m.exists():
+        return None
+    try:
+        j = json.loads(m.read_text())
+        files = [d / n for n, _ in j["files"]]
+        if any(not f.exists() or f.stat().st_size != s for f, (_, s) in zip(files, j["files"])):
+            return None
+        if _digest(files) != j["digest"]:
+            return None
+        return j
+    except Exception:
+        return None
+
+
+def ensure_dataset(args, generator) -> tuple[list[str], dict, float]:
+    """Shard files of the workload (generated once per box, reused by both arms). `generator`
+    (out_dir, seed, journeys, shards, mean_duration) -> rows writes generate_day's files."""
+    w = WORKLOADS[args.workload]
+    d = dataset_dir(args)
+    man = load_manifest(d)
+    t_gen = 0.0
+    if man is None:
+        root = Path(args.data_dir)
+        root.mkdir(parents=True, exist_ok=True)
+        for other in root.iterdir():  # one dataset at a time (disk space)
+            if other.is_dir():
+                shutil.rmtree(other, ignore_errors=True)
+        tmp = root / (d.name + ".tmp")
+        shutil.rmtree(tmp, ignore_errors=True)
+        tmp.mkdir(parents=True)
+        t0 = time.perf_counter()
+        rows = generator(tmp, w["seed"], w["journeys"], w["shards"], w["mean_duration"])
+        t_gen = time.perf_counter() - t0
+        files = sorted(tmp.glob("shard_*.csv"))
+        man = {"files": [[f.name, f.stat().st_size] for f in files], "rows": int(rows),
+               "digest": _digest(files), "workload": args.workload, **{k: w[k] for k in
+               ("journeys", "shards", "seed", "mean_duration")}}
+        (tmp / "MANIFEST.json").write_text(json.dumps(man))
+        os.replace(tmp, d)
+    paths = [str(d / n) for n, _ in man["files"]]
+    return paths, man, t_gen
+
+
+def groups_of(paths: list[str]) -> list[list[str]]:
+    return [[p for i, p in enumerate(paths) if i % GROUPS == g] for g in range(GROUPS)]
+
+
+def config_of(args, man, world) -> dict:
+    """Identical in both arms (the driver compares them)."""
+    w = WORKLOADS[args.workload]
+    wl = w["desc"] if world == 1 else (
+        f"c4: the {args.workload} trace sharded by journey-id hash (FNV-1a % N) at {world} B200, "
+        "end-to-end from shard files")
+    return {
+        "workload": wl, "journeys": w["journeys"], "rows": man["rows"],
+        "csv_bytes": sum(s for _, s in man["files"]), "shards": w["shards"], "seed": w["seed"],
+        "mean_duration_s": w["mean_duration"],
+        "grid": "default GridSpec 46x67x288x4 (3,550,464 cells)",
+        "l2": "inputs (%.1f GB) larger than L2 (126 MB); no flush needed"
+              % (sum(s for _, s in man["files"]) / 1e9),
+        "parallelism": f"dp{world} (journey-hash shards)",
+    }
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons sampled DURING the timed region (in-process NVML: the
-    nvidia-smi CLI polling every 100 ms was measured to stall CUDA API calls by 20-30 ms).
-    One sample at entry, one at exit, and one every `interval` seconds in between."""
+    """SM clocks + throttle reasons sampled DURING the timed region (in-process NVML)."""
 
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, gpu_index: int, interval: float = 0.25):
-        self.disabled = os.environ.get("CVLG_NO_CLOCKS") == "1"  # diagnostics only
-        self.gpu = gpu_index
         self.interval = interval
         self.samples: list[tuple[float, float, int]] = []
         self._stop = threading.Event()
@@ -94,14 +196,13 @@ class ClockSampler:
             self.nvml = None
 
     def sample(self):
-        if not self.nvml or self.disabled:
+        if not self.nvml:
             return
         n = self.nvml
         try:
-            sm = n.nvmlDeviceGetClockInfo(self.handle, n.NVML_CLOCK_SM)
-            mx = n.nvmlDeviceGetMaxClockInfo(self.handle, n.NVML_CLOCK_SM)
-            rs = n.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
-            self.samples.append((float(sm), float(mx), int(rs)))
+            self.samples.append((float(n.nvmlDeviceGetClockInfo(self.handle, n.NVML_CLOCK_SM)),
+                                 float(n.nvmlDeviceGetMaxClockInfo(self.handle, n.NVML_CLOCK_SM)),
+                                 int(n.nvmlDeviceGetCurrentClocksEventReasons(self.handle))))
         except Exception:
             pass
 
@@ -123,11 +224,10 @@ class ClockSampler:
     def summary(self) -> dict:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        sm = [s[0] for s in self.samples]
-        mx = max(s[1] for s in self.samples)
-        reasons = sorted({k for _, _, r in self.samples for k, bit in self.REASONS.items() if r & bit})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(sm), "source": "NVML in-process"}
+        reasons = sorted({k for _, _, r in self.samples for k, b in self.REASONS.items() if r & b})
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": "NVML in-process"}
 
 
 def measured_peak_hbm() -> tuple[float, str]:
@@ -137,82 +237,107 @@ def measured_peak_hbm() -> tuple[float, str]:
             return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
         except Exception:
             pass
-    return 6650.0, "fallback"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def generate(journeys: int, shards: int, mean_duration: float, seed: int, mod: int = 1,
-             rem: int = 0, days: int = 1):
-    from paper_2305_07454_b200.cvlg import synth_day
-    if days > 1:  # c5 shape: day k uses seed + k and date + k; its shards follow day k-1's
-        import datetime
-        import numpy as np
-        if mod != 1:
-            raise SystemExit("--days > 1 is single-GPU only in this bench")
-        blobs, offs, rows = [], [0], 0
-        for k in range(days):
-            d = (datetime.date(2021, 5, 9) + datetime.timedelta(days=k)).isoformat()
-            b, o, r = synth_day(seed=seed + k, journeys=journeys, shards=shards,
-                                mean_duration=mean_duration, day=d)
-            base = offs[-1]
-            offs.extend(base + int(x) for x in o[1:])
-            blobs.append(b)
-            rows += r
-        return np.concatenate(blobs), offs, rows
-    if mod == 1:
-        return synth_day(seed=seed, journeys=journeys, shards=shards, mean_duration=mean_duration)
-    from paper_2305_07454_b200.distributed import synth_day_owned
-    return synth_day_owned(seed=seed, journeys=journeys * mod, shards=shards,
-                           mean_duration=mean_duration, mod=mod, rem=rem)
+def lattice_sha(planes, raw) -> str:
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(planes).view(np.uint8))
+    if raw is not None:
+        h.update(np.ascontiguousarray(raw).view(np.uint8))
+    return h.hexdigest()
 
 
-def cpu_reference_sample(args, tmpdir: Path):
-    """Bounded sample of the same workload written as shard files for the reference."""
-    from paper_2305_07454_b200.cvlg import synth_day
-    threads = os.cpu_count() or 1
-    shards = max(args.shards, threads)
-    blob, offs, rows = synth_day(seed=1, journeys=args.cpu_journeys, shards=shards,
-                                 mean_duration=args.mean_duration)
-    paths = []
-    for i in range(len(offs) - 1):
-        p = tmpdir / f"shard_{i:04d}.csv"
-        p.write_bytes(blob[offs[i]:offs[i + 1]].tobytes())
-        paths.append(str(p))
-    return paths, rows, threads
+# ---- reference arm -----------------------------------------------------------------------------
+def ref_generator(threads):
+    from oracle.oracle import Ref
+
+    def gen(out, seed, journeys, shards, mean_duration):
+        return Ref().generate_day_mt(out, seed=seed, journeys=journeys, shards=shards,
+                                     mean_duration=mean_duration, threads=threads)
+    return gen
 
 
 def run_reference_arm(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    from oracle.oracle import Ref
-    import paper_2305_07454_b200 as cvlg
-    spec = cvlg.GridSpec()
-    with tempfile.TemporaryDirectory() as d:
-        paths, rows, threads = cpu_reference_sample(args, Path(d))
-        ref = Ref()
-        for _ in range(args.warmup):
-            ref.run_pipeline(paths, spec, None, n_partitions=2 * threads, n_threads=threads,
-                             raw=False)
-        times = []
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            ref.run_pipeline(paths, spec, None, n_partitions=2 * threads, n_threads=threads,
-                             raw=False)
-            times.append(time.perf_counter() - t0)
-    ms = 1000.0 * sum(times) / len(times)
-    value = rows / (ms / 1000.0)
+    assert "paper_2305_07454_b200" not in sys.modules
+    from oracle.oracle import Ref, CGrid  # noqa: F401  (the compiled, unmodified reference)
+
+    class Spec:  # the default GridSpec (grid.hpp:21-41)
+        lat_min, lat_max, lon_min, lon_max = 36.0, 40.6, -95.8, -89.1
+        lat_step = lon_step = 0.1
+        min_step, dxn_step, dxn_offset = 5, 90, 0.0
+
+    threads = args.threads or os.cpu_count() or 1
+    paths, man, t_gen = ensure_dataset(args, ref_generator(threads))
+    groups = groups_of(paths)
+    ref = Ref()
+    rows_of = {}
+
+    def step(i):
+        g = groups[i % GROUPS]
+        _, _, st, _ = ref.run_pipeline(g, Spec, None, n_partitions=2 * threads,
+                                       n_threads=threads, raw=False)
+        rows_of[i % GROUPS] = st["rows_read"]
+        return st["rows_read"]
+
+    for i in range(args.warmup):
+        step(i)
+    rows = 0
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        rows += step(args.warmup + i)
+    dt = time.perf_counter() - t0
+    value = rows / dt
+    sample = (f"cvl::run_pipeline (unmodified, oracle/_ref) with {threads} threads / "
+              f"{2 * threads} partitions; each step = 1/{GROUPS} of the same {len(paths)}-shard "
+              f"manifest (every {GROUPS}th shard, ~{rows / max(args.steps, 1) / 1e6:.1f}M rows), "
+              f"cycling over the {GROUPS} eighths; {rows} rows in {args.steps} timed steps")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "c2 (bounded CPU sample: %d journeys, %d rows per step)" % (
-            args.cpu_journeys, rows), "grid": "default GridSpec 46x67x288x4"},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * dt / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator, seed 1), shard files on the local file system",
+        "config": config_of(args, man, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{rows} rows ({args.cpu_journeys} journeys, seed 1) per step; "
-                                   f"cvl::run_pipeline, {2 * threads} partitions"},
+                         "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "input_generation_s": round(t_gen, 1),
     }
     print(json.dumps(line), flush=True)
+
+
+# ---- our arm -----------------------------------------------------------------------------------
+def our_generator(threads):
+    from paper_2305_07454_b200.cvlg import synth_write_day
+
+    def gen(out, seed, journeys, shards, mean_duration):
+        return synth_write_day(out, seed=seed, journeys=journeys, shards=shards,
+                               mean_duration=mean_duration, threads=threads)[1]
+    return gen
+
+
+def cpu_baseline_leg(args, paths, spec_ref):
+    """The reference on one eighth of the same files (rank 0, N = 1): ~10-30 s of CPU work."""
+    from oracle.oracle import Ref
+    threads = args.threads or os.cpu_count() or 1
+    g = groups_of(paths)[0]
+    ref = Ref()
+    ref.run_pipeline(g, spec_ref, None, 2 * threads, threads, raw=False)
+    ts, out = [], None
+    for _ in range(2):
+        t0 = time.perf_counter()
+        out = ref.run_pipeline(g, spec_ref, None, 2 * threads, threads, raw=True)
+        ts.append(time.perf_counter() - t0)
+    planes, raw, st, _ = out
+    cpu = {"value": st["rows_read"] / (sum(ts) / len(ts)), "unit": UNIT, "cores": threads,
+           "kind": "reference",
+           "sample": f"{st['rows_read']} rows = shards 0,8,16,... (1/{GROUPS}) of the same "
+                     f"manifest; cvl::run_pipeline (unmodified) with {threads} threads / "
+                     f"{2 * threads} partitions, mean of 2 warm runs"}
+    return cpu, g, planes, raw, st
 
 
 def run_ours(args):
@@ -221,246 +346,190 @@ def run_ours(args):
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
-    # CVLG_FORCE_DIST=1 exercises the multi-GPU combine path on a single GPU (tests)
-    use_dist = world > 1 or os.environ.get("CVLG_FORCE_DIST") == "1"
-    if use_dist:
+    if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29533")
-        os.environ.setdefault("RANK", "0")
-        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2305_07454_b200 as cvlg
 
-    spec = (cvlg.GridSpec(lat_step=0.01, lon_step=0.01, min_step=1) if args.fine
-            else cvlg.GridSpec())
-    t_gen = time.perf_counter()
-    blob, offs, rows = generate(args.journeys, args.shards, args.mean_duration, seed=1,
-                                mod=world, rem=rank, days=args.days)
-    if args.shuffled:
-        from paper_2305_07454_b200.cvlg import shuffle_rows
-        blob, offs = shuffle_rows(blob, offs, args.shards, seed=7)
-    t_gen = time.perf_counter() - t_gen
-    csv_bytes = int(offs[-1])
-    bufs = [blob[offs[i]:offs[i + 1]] for i in range(len(offs) - 1)]
-    T, _, R, C = spec.dims()
-    ctx = cvlg.Context(local)
-
-    # ---- device-resident value ------------------------------------------------------------------
-    d_csv = torch.from_numpy(blob).to(f"cuda:{local}")
-    d_planes = torch.empty((T, 8, R, C), dtype=torch.int32, device=f"cuda:{local}")
-    d_raw = torch.empty((T, 4, R, C), dtype=torch.int32, device=f"cuda:{local}")
-    stream = torch.cuda.current_stream()
-    st = cvlg.PipelineStats()
-
-    if use_dist:
-        from paper_2305_07454_b200.distributed import run_pipeline_distributed
-        dstats: dict = {}
-
-    def step():
-        if not use_dist:
-            cvlg.run_pipeline_device(d_csv.data_ptr(), offs, d_planes.data_ptr(), d_raw.data_ptr(),
-                                     spec, stats=st, ctx=ctx, stream=stream.cuda_stream)
-        else:
-            p, r = run_pipeline_distributed(d_csv, offs, spec, ctx=ctx, stats=dstats)
-            d_planes.copy_(p)
-            d_raw.copy_(r)
-            st.rows_read = dstats["rows_read"]
-            st.parsed = dstats["parsed"]
-
-    for _ in range(max(args.warmup, 3)):
-        step()
-    assert st.rows_read == rows, (st.rows_read, rows)
+    threads = args.threads or os.cpu_count() or 1
+    if world > 1:
+        threads = max(1, threads // world)
+    if rank == 0:
+        paths, man, t_gen = ensure_dataset(args, our_generator(threads))
     if world > 1:
         dist.barrier()
+        if rank != 0:
+            paths, man, t_gen = ensure_dataset(args, our_generator(threads))
+    rows = man["rows"]
+    csv_bytes = sum(s for _, s in man["files"])
+    spec = cvlg.GridSpec()
+    T, _, R, C = spec.dims()
+    ctx = cvlg.Context(local)
+    planes = np.empty((T, 8, R, C), dtype=np.uint32)
+    raw = np.empty((T, 4, R, C), dtype=np.uint32)
+    cvlg.pin_host(planes)
+    cvlg.pin_host(raw)
+    st = cvlg.PipelineStats()
+
+    if world > 1:
+        from paper_2305_07454_b200.distributed import FileShardedPipeline
+        runner = FileShardedPipeline(paths, spec, ctx=ctx, threads=threads)
+        e2e_step = lambda: runner.run_files(out=(planes, raw), stats=st)  # noqa: E731
+    else:
+        e2e_step = lambda: cvlg.run_pipeline(paths, spec, n_partitions=2 * threads,  # noqa: E731
+                                             n_threads=threads, stats=st, ctx=ctx,
+                                             out=(planes, raw))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- e2e through the drop-in C ABI (files -> lattice in host memory) ---------------------
+    for _ in range(max(args.warmup, 3)):
+        e2e_step()
+    assert st.rows_read == rows, (st.rows_read, rows)
+    e2e_sha = lattice_sha(planes, raw)
+    barrier()
+    torch.cuda.synchronize()
+    e2e = None
+    e2e_clocks = None
+    if not args.no_e2e:
+        with ClockSampler(local) as ck:
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                e2e_step()
+            torch.cuda.synchronize()
+            e2e_s = time.perf_counter() - t0
+        e2e_clocks = ck.summary()
+        barrier()
+        e2e_ms = max_over_ranks(1000.0 * e2e_s / args.steps)
+        e2e = {"value": rows / (e2e_ms / 1000.0), "unit": UNIT, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": csv_bytes,
+               "d2h_bytes_per_step": int(planes.nbytes + raw.nbytes),
+               "path": "cvlg_run_pipeline(shard paths): pread (page cache) -> pinned ring -> H2D "
+                       "-> pipeline -> D2H of the lattice, every step"}
+
+    # ---- device-resident value: the same bytes, already in HBM --------------------------------
+    stream = torch.cuda.current_stream()
+    d_planes = torch.empty((T, 8, R, C), dtype=torch.int32, device=f"cuda:{local}")
+    d_raw = torch.empty((T, 4, R, C), dtype=torch.int32, device=f"cuda:{local}")
+    if world > 1:
+        dev_step = lambda: runner.run_resident(d_planes, d_raw, stats=st)  # noqa: E731
+    else:
+        d_csv, n_in = ctx.input()
+        assert n_in == csv_bytes
+        offs = [0]
+        for _, s in man["files"]:
+            offs.append(offs[-1] + s)
+        dev_step = lambda: cvlg.run_pipeline_device(d_csv, offs, d_planes.data_ptr(),  # noqa: E731
+                                                    d_raw.data_ptr(), spec, stats=st, ctx=ctx,
+                                                    stream=stream.cuda_stream)
+    for _ in range(max(args.warmup, 3)):
+        dev_step()
+    dev_sha = lattice_sha(d_planes.cpu().numpy().view(np.uint32), d_raw.cpu().numpy().view(np.uint32))
+    assert dev_sha == e2e_sha, "file and device-resident entry points disagree"
+    barrier()
     torch.cuda.synchronize()
     launches0 = cvlg.launch_count()
-    decode_ms = []
-    stage = []
+    stage, decode_ms = [], []
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         ev0.record(stream)
         for _ in range(args.steps):
-            step()
+            dev_step()
             s = ctx.stage_ms()
-            decode_ms.append(s[4])
             stage.append(s[:4])
+            decode_ms.append(s[4])
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = cvlg.launch_count() - launches0
-    if world > 1:
-        dist.barrier()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
-    rows_t = torch.tensor([int(rows)], dtype=torch.int64, device=f"cuda:{local}")
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(rows_t, op=dist.ReduceOp.SUM)
-    ms_max = float(ms_t.item())
-    total_rows = int(rows_t.item())
-    value = total_rows / (ms_max / 1000.0)
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    value = rows / (ms / 1000.0)
 
-    # ---- e2e through the host-buffer C ABI --------------------------------------------------------
-    e2e = None
-    if not args.no_e2e and use_dist:
-        host = torch.from_numpy(blob).pin_memory()
-        for _ in range(max(args.warmup, 3)):
-            d_csv.copy_(host, non_blocking=True)
-            p, _r = run_pipeline_distributed(d_csv, offs, spec, ctx=ctx)
-            p.cpu()
-        dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            d_csv.copy_(host, non_blocking=True)
-            p, r = run_pipeline_distributed(d_csv, offs, spec, ctx=ctx)
-            p.cpu()
-            r.cpu()
-        torch.cuda.synchronize()
-        e2e_ms = 1000.0 * (time.perf_counter() - t0) / args.steps
-        e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(e_t.item())
-        e2e = {"value": total_rows / (e2e_ms / 1000.0), "unit": UNIT,
-               "h2d_bytes_per_step": csv_bytes, "d2h_bytes_per_step": int(p.numel() * 4 + r.numel() * 4),
-               "ms_per_step": e2e_ms, "pinned_host": True, "note": "per-rank H2D + NCCL combine + D2H"}
-    if not args.no_e2e and not use_dist:
-        cvlg.pin_host(blob)
-        planes = np.empty((T, 8, R, C), dtype=np.uint32)
-        raw = np.empty((T, 4, R, C), dtype=np.uint32)
-        cvlg.pin_host(planes)
-        cvlg.pin_host(raw)
-        for _ in range(max(args.warmup, 3)):
-            cvlg.run_pipeline_host(bufs, spec, ctx=ctx, out=(planes, raw))
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            cvlg.run_pipeline_host(bufs, spec, ctx=ctx, out=(planes, raw))
-        e2e_ms = 1000.0 * (time.perf_counter() - t0) / args.steps
-        e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
-        if world > 1:
-            dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(e_t.item())
-        # parity of the two entry points on this input
-        dev_planes = d_planes.cpu().numpy().view(np.uint32)
-        assert np.array_equal(dev_planes, planes), "host and device entry points disagree"
-        e2e = {"value": total_rows / (e2e_ms / 1000.0), "unit": UNIT,
-               "h2d_bytes_per_step": csv_bytes, "d2h_bytes_per_step": planes.nbytes + raw.nbytes,
-               "ms_per_step": e2e_ms, "pinned_host": True}
-        cvlg.unpin_host(planes)
-        cvlg.unpin_host(raw)
-        cvlg.unpin_host(blob)
-
-    # ---- per-journey feature table (north_star extension; extra key, not the headline metric) ---
-    features = None
-    if not args.no_features and not use_dist and rank == 0:
-        for _ in range(2):
-            cvlg.journey_features_device(d_csv.data_ptr(), offs, d_planes.data_ptr(), d_raw.data_ptr(),
-                                         spec, stop_speed=5.0, ctx=ctx, stream=stream.cuda_stream,
-                                         fetch=False)
-        torch.cuda.synchronize()
-        f0 = torch.cuda.Event(enable_timing=True)
-        f1 = torch.cuda.Event(enable_timing=True)
-        fsteps = max(3, min(args.steps, 10))
-        f0.record(stream)
-        for _ in range(fsteps):
-            nj = cvlg.journey_features_device(d_csv.data_ptr(), offs, d_planes.data_ptr(),
-                                              d_raw.data_ptr(), spec, stop_speed=5.0, ctx=ctx,
-                                              stream=stream.cuda_stream, fetch=False)
-        f1.record(stream)
-        torch.cuda.synchronize()
-        fms = f0.elapsed_time(f1) / fsteps
-        features = {"ms_per_step": fms, "records_per_s": rows / (fms / 1000.0), "journeys": int(nj),
-                    "note": "pipeline + per-journey feature table + per-cell speed min/max "
-                            "(not in the reference: parity vs tests/features_oracle.py)"}
-
-    # ---- roofline of the dominant kernel (K1 decode) ---------------------------------------------
+    # ---- roofline of the dominant kernel (K1 decode) ------------------------------------------
     peak, peak_kind = measured_peak_hbm()
     dec_ms = sum(decode_ms) / len(decode_ms)
-    n_heads_est = None
-    dec_bytes = csv_bytes + st.parsed * 28  # CSV read + ts/speed/code/line-offset columns written
+    local_bytes = csv_bytes if world == 1 else runner.local_bytes
+    local_parsed = st.parsed if world == 1 else runner.local_parsed
+    dec_bytes = local_bytes + local_parsed * 28  # CSV read + 28 B/slot of columns written
     achieved = dec_bytes / (dec_ms / 1000.0) / 1e9
     traffic = None
     tfile = ROOT / "profiles" / "decode_traffic.json"
     if tfile.exists():
         try:
             tj = json.loads(tfile.read_text())
-            # the capture holds for the workload it was taken on only
-            if tj.get("csv_bytes") == csv_bytes:
+            if tj.get("csv_bytes") == local_bytes:
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     stage_avg = [sum(s[i] for s in stage) / len(stage) for i in range(4)]
 
-    # ---- CPU baseline (reference, rank 0, N = 1 only) ---------------------------------------------
-    cpu = None
+    # ---- CPU baseline + sampled parity (reference, rank 0, N = 1 only) ------------------------
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu:
+        class SpecRef:
+            lat_min, lat_max, lon_min, lon_max = 36.0, 40.6, -95.8, -89.1
+            lat_step = lon_step = 0.1
+            min_step, dxn_step, dxn_offset = 5, 90, 0.0
         try:
-            from oracle.oracle import Ref
-            with tempfile.TemporaryDirectory() as d:
-                paths, crow, threads = cpu_reference_sample(args, Path(d))
-                ref = Ref()
-                ref.run_pipeline(paths, spec, None, 2 * threads, threads, raw=False)
-                ts = []
-                for _ in range(2):
-                    t0 = time.perf_counter()
-                    ref.run_pipeline(paths, spec, None, 2 * threads, threads, raw=False)
-                    ts.append(time.perf_counter() - t0)
-            cpu = {"value": crow / (sum(ts) / len(ts)), "unit": UNIT, "cores": threads,
-                   "kind": "reference",
-                   "sample": f"{crow} rows ({args.cpu_journeys} journeys of the same generator, "
-                             f"seed 1), cvl::run_pipeline with {threads} threads / "
-                             f"{2 * threads} partitions, mean of 2 warm runs"}
+            cpu, g, rp, rr, rst = cpu_baseline_leg(args, paths, SpecRef)
+            if not args.no_parity:
+                gst = cvlg.PipelineStats()
+                lat = cvlg.run_pipeline(g, spec, n_partitions=1, n_threads=threads, stats=gst,
+                                        ctx=ctx)
+                same = (np.array_equal(lat.planes, rp) and np.array_equal(lat.raw, rr)
+                        and gst.rows_read == rst["rows_read"] and gst.parsed == rst["parsed"]
+                        and gst.accepted == rst["accepted"])
+                parity = {"sample": f"1/{GROUPS} of the manifest ({rst['rows_read']} rows)",
+                          "vs": "cvl::run_pipeline (unmodified)",
+                          "lattice_and_stats_bit_identical": bool(same),
+                          "lattice_sha256": lattice_sha(lat.planes, lat.raw)}
         except Exception as e:  # the baseline is reported, never required
-            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+            cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference generator algorithm, byte-identical; seed 1)",
-            "config": {
-                "workload": (f"c5 shape on 1 GPU: {args.days} consecutive days x {args.journeys} "
-                             "journeys (same ids every day), device-resident"
-                             if args.days > 1 else
-                             "c2: synthetic 50M-point trace, 100k journeys per GPU, device-resident"
-                             if args.journeys == 100_000 else
-                             f"synthetic trace, {args.journeys} journeys per GPU "
-                             f"(c3 = 1,000,000: full-day statewide shape), device-resident")
-                            + (" | ADVERSARIAL: rows shuffled across shards (full-sort path)"
-                               if args.shuffled else "")
-                            + (" | fine 1-minute / 0.01 deg lattice" if args.fine else ""),
-                "journeys_per_gpu": args.journeys, "rows_per_gpu": rows, "rows_total": total_rows,
-                "csv_bytes_per_gpu": csv_bytes, "shards": args.shards,
-                "grid": ("c5 fine grid: 0.01 deg cells, 1-minute bins (T=1440, 460x670: "
-                         f"{1440 * 4 * 460 * 670:,} cells)" if args.fine
-                         else "default GridSpec 46x67x288x4 (3,550,464 cells)"),
-                "l2": "inputs (%.2f GB) larger than L2 (126 MB); no flush needed" % (csv_bytes / 1e9),
-                "parallelism": f"dp{world} (journey-hash shards)",
-                "input_generation_s": round(t_gen, 2),
-            },
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generator, seed 1), shard files on the local file system",
+            "config": config_of(args, man, world),
             "e2e": e2e,
             "roofline": {"bound": "hbm", "kernel": "decode_kernel (K1)", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_kind": peak_kind,
-                         "algorithmic_bytes_per_launch": dec_bytes, "avg_launch_ms": dec_ms},
-            "stage_ms": dict(zip(["decode", "dictionary+order", "fold", "finalize"], stage_avg)),
+                         "algorithmic_bytes_per_launch_sum": dec_bytes, "avg_decode_ms": dec_ms},
+            "stage_ms": dict(zip(["parse", "dedup+filter+accumulate", "merge", "finalize"],
+                                 stage_avg)),
             "pipeline_hbm_frac": value * (csv_bytes / rows) / 1e9 / peak,
             "cpu_baseline": cpu,
-            "features": features,
+            "parity_sample": parity,
+            "lattice_sha256": e2e_sha,
             "clocks": clocks.summary(),
+            "e2e_clocks": e2e_clocks,
             "gpu_launches": launches,
+            "input_generation_s": round(t_gen, 1),
         }
         print(json.dumps(line), flush=True)
-    if use_dist:
+    cvlg.unpin_host(planes)
+    cvlg.unpin_host(raw)
+    if world > 1:
         dist.destroy_process_group()
 
 
 def main():
     args = parse_args()
+    maybe_relaunch(args)
     if args.impl == "reference":
         run_reference_arm(args)
     else:

@@ -77,7 +77,9 @@ typedef struct cvlg_filter_rules {
 /* PipelineStats (aggregate.hpp:112-121) with the string-keyed maps flattened:
  *   rejected[]: BadTimestamp, BadNumeric, MissingField, RangeViolation, BadHeader
  *   filtered[]: OutOfGrid, SpeedCeiling, MissingField
- *   stage_seconds[]: decode, dictionary+order, fold, finalize (device time, CUDA events) */
+ *   stage_seconds[]: the reference's stages (aggregate.cpp:370-383, 449), device time from
+ *   CUDA events: parse (decode), dedup+filter+accumulate (journey dictionary, canonical order,
+ *   per-journey fold), merge ((cell, journey) sort), finalize */
 typedef struct cvlg_stats {
     uint64_t rows_read, parsed, duplicates_dropped, conflicting_duplicates, accepted;
     uint64_t rejected[5];
@@ -189,9 +191,16 @@ int cvlg_features_copy(cvlg_context* ctx, cvlg_features* out);
 int cvlg_write_container(const uint32_t* planes, const cvlg_grid_spec* spec, int32_t day,
                          const char* path, uint64_t* bytes_written);
 
-/* Per-stage device milliseconds of the context's last run: decode kernel, dictionary+order,
- * fold, finalize, and (index 4) the decode kernel alone. n <= 5. */
+/* Per-stage device milliseconds of the context's last run: parse, dedup+filter+accumulate,
+ * merge, finalize (as stage_seconds), then (index 4) the decode kernel alone and (index 5) the
+ * dictionary + canonical order part of stage 1. n <= 6. */
 int cvlg_last_stage_ms(cvlg_context* ctx, float* ms, int n);
+
+/* Device address and size of the input bytes the context's last cvlg_run_pipeline /
+ * cvlg_run_pipeline_host call staged in HBM (shards concatenated in rank order). They stay
+ * resident, unchanged, until the next call on the context, so they can be passed back to
+ * cvlg_run_pipeline_device (the device-resident measurement of the same input). */
+int cvlg_context_input(cvlg_context* ctx, const uint8_t** d_csv, uint64_t* n_bytes);
 
 /* Pins / unpins caller memory for faster H2D (cudaHostRegister). */
 int cvlg_pin_host(void* ptr, size_t bytes);

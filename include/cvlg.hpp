@@ -84,7 +84,7 @@ void fill_stats(const cvlg_stats& s, Stats* out) {
     static const char* kRej[5] = {"BadTimestamp", "BadNumeric", "MissingField", "RangeViolation",
                                   "BadHeader"};
     static const char* kFil[3] = {"OutOfGrid", "SpeedCeiling", "MissingField"};
-    static const char* kStage[4] = {"decode", "dictionary+order", "fold", "finalize"};
+    static const char* kStage[4] = {"parse", "dedup+filter+accumulate", "merge", "finalize"};
     out->rows_read += s.rows_read;
     out->parsed += s.parsed;
     out->duplicates_dropped += s.duplicates_dropped;

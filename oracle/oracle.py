@@ -114,6 +114,11 @@ class Ref:
                                              ctypes.c_double, ctypes.c_double, ctypes.c_char_p,
                                              ctypes.c_char_p, vp, ctypes.POINTER(ctypes.c_uint64),
                                              ctypes.c_char_p, ctypes.c_size_t]
+            lib.ref_generate_day_mt.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                                                ctypes.c_double, ctypes.c_double, ctypes.c_char_p,
+                                                ctypes.c_char_p, ctypes.c_uint32,
+                                                ctypes.POINTER(ctypes.c_uint64), ctypes.c_char_p,
+                                                ctypes.c_size_t]
             lib.ref_write_container.argtypes = [vp, ctypes.POINTER(CGrid), ctypes.c_int32,
                                                 ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint64),
                                                 ctypes.c_char_p, ctypes.c_size_t]
@@ -181,6 +186,18 @@ class Ref:
         rc = self.lib.ref_generate_day(seed, journeys, shards, sample_period, mean_duration,
                                        day.encode(), str(out_dir).encode(), bb,
                                        ctypes.byref(total), err, 512)
+        if rc:
+            raise RefError(rc, err.value.decode())
+        return total.value
+
+    def generate_day_mt(self, out_dir, seed=0, journeys=100, shards=8, sample_period=1.0,
+                        mean_duration=300.0, day="2021-05-09", threads=0) -> int:
+        """generate_day's files (same bytes), one host thread per shard file."""
+        total = ctypes.c_uint64()
+        err = ctypes.create_string_buffer(512)
+        rc = self.lib.ref_generate_day_mt(seed, journeys, shards, sample_period, mean_duration,
+                                          day.encode(), str(out_dir).encode(), threads,
+                                          ctypes.byref(total), err, 512)
         if rc:
             raise RefError(rc, err.value.decode())
         return total.value

@@ -10,14 +10,22 @@
 //   ref_parse_header      -> cvl::parse_header            proj/include/cvl/ingest.hpp:34
 //   ref_parse_record      -> cvl::parse_record            proj/include/cvl/ingest.hpp:40
 //   ref_generate_day      -> cvl::generate_day            proj/include/cvl/synth.hpp:61
+//   ref_generate_day_mt   -> cvl::generate_journey + cvl::csv_header, one host thread per shard
+//                            file, rows rendered with generate_day's own format string
+//                            (synth.cpp:157-173); byte-identical to ref_generate_day (tested)
 //   ref_write_container   -> cvl::write_container         proj/include/cvl/lattice_store.hpp:43
 //   ref_bins              -> lat_bin/lon_bin/time_bin/dxn_bin/global_index  grid.hpp:49-56
 //   ref_journey_hash      -> cvl::journey_hash            proj/include/cvl/ingest.hpp:68
 //   ref_deduplicate       -> cvl::deduplicate             proj/include/cvl/ingest.hpp:63
+#include <atomic>
 #include <charconv>
+#include <cstdio>
+#include <filesystem>
+#include <thread>
 #include <cstdint>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "cvl/aggregate.hpp"
@@ -265,6 +273,79 @@ int ref_generate_day(uint64_t seed, uint32_t n_journeys, uint32_t n_shards, doub
         }
         const SourceManifest m = generate_day(cfg);
         if (total_rows) *total_rows = m.total_rows;
+        return 0;
+    } catch (const CvlError& e) {
+        return fail_code(e, err, errlen);
+    } catch (const std::exception& e) {
+        return fail_other(e, err, errlen);
+    }
+}
+
+int ref_generate_day_mt(uint64_t seed, uint32_t n_journeys, uint32_t n_shards, double sample_period,
+                        double mean_duration, const char* day, const char* out_dir,
+                        uint32_t n_threads, uint64_t* total_rows, char* err, size_t errlen) {
+    try {
+        SynthConfig cfg;
+        cfg.seed = seed;
+        cfg.n_journeys = n_journeys;
+        cfg.n_shards = n_shards;
+        cfg.sample_period = sample_period;
+        cfg.mean_duration = mean_duration;
+        cfg.day = day;
+        cfg.out_dir = out_dir;
+        if (cfg.n_shards == 0) fail(Err::BadConfig, "n_shards must be >= 1");
+        std::filesystem::create_directories(cfg.out_dir);
+        const std::string header = csv_header();
+        std::atomic<uint32_t> next{0};
+        std::atomic<uint64_t> rows{0};
+        std::atomic<bool> bad{false};
+        std::string first_err;
+        std::mutex mu;
+        auto work = [&] {
+            std::vector<char> buf;
+            buf.reserve(64u << 20);
+            char line[256];
+            for (uint32_t s = next.fetch_add(1); s < cfg.n_shards && !bad; s = next.fetch_add(1)) {
+                try {
+                    char name[32];
+                    std::snprintf(name, sizeof(name), "shard_%04u.csv", s);
+                    const std::string path = (std::filesystem::path(cfg.out_dir) / name).string();
+                    std::FILE* f = std::fopen(path.c_str(), "wb");
+                    if (!f) fail(Err::Io, "cannot open " + path + " for writing");
+                    buf.assign(header.begin(), header.end());
+                    buf.push_back('\n');
+                    uint64_t local = 0;
+                    for (uint32_t j = s; j < cfg.n_journeys; j += cfg.n_shards) {
+                        for (const CvRecord& rec : generate_journey(j, cfg)) {
+                            const int k = std::snprintf(line, sizeof(line), "%s,%s,%.6f,%.6f,%s,%.2f,%.2f\n",
+                                                        rec.journey_id.c_str(), rec.timestamp.to_string().c_str(),
+                                                        rec.latitude, rec.longitude, rec.postal_code.c_str(),
+                                                        rec.speed, rec.heading);
+                            buf.insert(buf.end(), line, line + k);
+                            ++local;
+                        }
+                        if (buf.size() > (48u << 20)) {
+                            if (std::fwrite(buf.data(), 1, buf.size(), f) != buf.size()) fail(Err::Io, "short write to " + path);
+                            buf.clear();
+                        }
+                    }
+                    if (!buf.empty() && std::fwrite(buf.data(), 1, buf.size(), f) != buf.size())
+                        fail(Err::Io, "short write to " + path);
+                    if (std::fclose(f) != 0) fail(Err::Io, "short write to " + path);
+                    rows += local;
+                } catch (const std::exception& e) {
+                    std::lock_guard<std::mutex> lk(mu);
+                    if (first_err.empty()) first_err = e.what();
+                    bad = true;
+                }
+            }
+        };
+        const uint32_t nt = std::max<uint32_t>(1, std::min<uint32_t>(n_threads ? n_threads : std::thread::hardware_concurrency(), cfg.n_shards));
+        std::vector<std::thread> pool;
+        for (uint32_t t = 0; t < nt; ++t) pool.emplace_back(work);
+        for (auto& t : pool) t.join();
+        if (bad) throw std::runtime_error(first_err);
+        if (total_rows) *total_rows = rows.load();
         return 0;
     } catch (const CvlError& e) {
         return fail_code(e, err, errlen);

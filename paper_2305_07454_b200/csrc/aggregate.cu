@@ -618,6 +618,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
             const uint32_t tb = t_g[warp][e][lane] / P.drc;
             const uint32_t lo = tb * P.drc;
             uint32_t f = e, flag = 0;
+            bool ovf = false;
             do {
                 const uint64_t at = static_cast<uint64_t>(base) + f;
                 const uint32_t cn = t_c[warp][f][lane];
@@ -628,10 +629,14 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
                     P.pair_cnt[at] = cn & ~kBinSpilled;
                 } else {
                     ++c_ovf;
+                    ovf = true;
                 }
                 ++f;
             } while (f < upto && t_g[warp][f][lane] - lo < P.drc);
-            P.dir[dir_row + tb] = make_uint4(static_cast<uint32_t>(j), P.epoch, base + e, (f - e) | flag);
+            // a block past the pair list is never published (a reopen would read past the
+            // allocation); the attempt is void and re-runs without windows
+            if (ovf) atomicExch(P.abort_flag, 1u);
+            else P.dir[dir_row + tb] = make_uint4(static_cast<uint32_t>(j), P.epoch, base + e, (f - e) | flag);
             e = f;
         }
         for (uint32_t q = upto; q < n_cells; ++q) {
@@ -663,7 +668,8 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
             flush_closed(n_cells, base);
         }
         const uint4 d = P.dir[dir_row + tb];
-        if (d.x == static_cast<uint32_t>(j) && d.y == P.epoch) {
+        if (d.x == static_cast<uint32_t>(j) && d.y == P.epoch &&
+            static_cast<uint64_t>(d.z) + (d.w & ~kBinSpilled) <= P.pair_cap) {
             const uint32_t cnt = d.w & ~kBinSpilled;
             const uint32_t dl = atomicAdd(P.dead_count, cnt);
             for (uint32_t q = 0; q < cnt; ++q) {
@@ -1114,17 +1120,22 @@ void launch_slot_jstart(const uint32_t* perm, const uint32_t* srank, uint64_t n,
 // enough lanes for every journey, capped at what is resident at once (journeys are handed out
 // dynamically, so CTAs beyond the resident set would find nothing left to do)
 unsigned fold_grid(uint64_t n_journeys, bool slow) {
-    static int per_sm[2] = {0, 0};
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
+    const int sms = per_device(kPdSms, [] {
+        int dev = 0, n = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], fold_lane_kernel<false>, kFoldWarps * 32, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], fold_lane_kernel<true>, kFoldWarps * 32, 0);
-        if (sms <= 0) sms = 148;
-    }
-    const uint64_t cap = static_cast<uint64_t>(sms) * std::max(1, per_sm[slow ? 1 : 0]);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n > 0 ? n : 148;
+    });
+    const int per_sm = slow ? per_device(kPdFoldPerSm1, [] {
+        int n = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fold_lane_kernel<true>, kFoldWarps * 32, 0);
+        return n;
+    }) : per_device(kPdFoldPerSm0, [] {
+        int n = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fold_lane_kernel<false>, kFoldWarps * 32, 0);
+        return n;
+    });
+    const uint64_t cap = static_cast<uint64_t>(sms) * std::max(1, per_sm);
     return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n_journeys + kFoldWarps * 32 - 1) / (kFoldWarps * 32), cap)));
 }
 

@@ -8,6 +8,12 @@ namespace cvlg {
 
 constexpr int kWarp = 32;
 
+// Launch facts that live in each device's context (the >48 KB shared-memory opt-in, SM count,
+// occupancy): computed once per (device, key) under a lock by `compute`, which runs with that
+// device current. Defined in pipeline.cu.
+int per_device(int key, int (*compute)());
+enum : int { kPdDecodeCtas = 0, kPdSms, kPdFoldPerSm0, kPdFoldPerSm1, kPdOnesweepAttr, kPdCount };
+
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

@@ -706,8 +706,7 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
 
 void launch_decode(const DecodeParams& p, uint32_t tile_begin, uint32_t n_tiles, cudaStream_t s) {
     if (n_tiles == 0) return;
-    static int max_ctas = 0;
-    if (!max_ctas) {
+    const int max_ctas = per_device(kPdDecodeCtas, [] {
         cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(sizeof(DecodeSmem)));
         int dev = 0, sms = 0, per_sm = 0;
@@ -715,8 +714,8 @@ void launch_decode(const DecodeParams& p, uint32_t tile_begin, uint32_t n_tiles,
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel, kDecodeThreads,
                                                       sizeof(DecodeSmem));
-        max_ctas = std::max(1, sms * std::max(per_sm, 1));
-    }
+        return std::max(1, sms * std::max(per_sm, 1));
+    });
     const uint32_t ctas = std::min<uint32_t>(n_tiles, static_cast<uint32_t>(max_ctas));
     decode_kernel<<<ctas, kDecodeThreads, sizeof(DecodeSmem), s>>>(p, tile_begin);
 }

@@ -19,6 +19,9 @@
 #include <cmath>
 #include <fstream>
 #include <functional>
+#include <memory>
+#include <condition_variable>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -32,6 +35,22 @@
 namespace cvlg {
 
 static std::atomic<uint64_t> g_launches{0};
+
+int per_device(int key, int (*compute)()) {
+    constexpr int kMaxDev = 64;
+    static std::mutex mu;
+    static int cache[kMaxDev][kPdCount];
+    static bool have[kMaxDev][kPdCount];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDev || key < 0 || key >= kPdCount) return compute();
+    std::lock_guard<std::mutex> lock(mu);
+    if (!have[dev][key]) {
+        cache[dev][key] = compute();
+        have[dev][key] = true;
+    }
+    return cache[dev][key];
+}
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
@@ -187,6 +206,19 @@ struct ChunkMark {
     cudaEvent_t ready;   // recorded on the copy stream (nullptr: already resident)
 };
 
+// Yields the marks of a run in order (blocking until the next chunk's copy is enqueued); false
+// once the input is complete. The last mark yielded covers every byte.
+using MarkSource = std::function<bool(ChunkMark&)>;
+
+MarkSource marks_of(std::vector<ChunkMark> v) {
+    auto st = std::make_shared<std::pair<std::vector<ChunkMark>, size_t>>(std::move(v), 0);
+    return [st](ChunkMark& m) {
+        if (st->second >= st->first.size()) return false;
+        m = st->first[st->second++];
+        return true;
+    };
+}
+
 }  // namespace cvlg
 
 using namespace cvlg;
@@ -208,15 +240,17 @@ struct cvlg_context {
     uint32_t fold_epoch = 0;
     bool slow_key_ts = false;
     DevBuf planes, raw, rank_slot, x_keys, x_sum, x_cnt;
-    HostPinned h_small, h_csv;
+    HostPinned h_small, h_ring;
+    std::vector<cudaEvent_t> ring_events;  // one per ring slot: its last H2D copy
     // last cvlg_partial_device run: pairs kept in pair_key/pair_sum/pair_cnt
     uint64_t part_pairs = 0, part_J = 0, last_slots = 0;
+    uint64_t input_bytes = 0;  // bytes of c->csv staged by the last host/file run
     int part_rbits = 0;
     bool part_long_ids = false;
     std::vector<cudaEvent_t> chunk_events;
     cudaEvent_t ev[6] = {};
     cudaEvent_t ev_dec0 = nullptr, ev_dec1 = nullptr;
-    float stage_ms[5] = {0, 0, 0, 0, 0};
+    float stage_ms[6] = {0, 0, 0, 0, 0, 0};
 };
 
 namespace {
@@ -247,7 +281,7 @@ struct Tracer {
 void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>& shard_off,
               const ColumnMap* h_cmap, const uint8_t* h_good, uint64_t bad_headers,
               const cvlg_grid_spec* spec, const cvlg_filter_rules* rules, uint32_t* d_planes,
-              uint32_t* d_raw, cvlg_stats* out_stats, const std::vector<ChunkMark>& marks,
+              uint32_t* d_raw, cvlg_stats* out_stats, const MarkSource& next_mark,
               bool partial = false, const double* feat_stop_speed = nullptr) {
     const bool feat = feat_stop_speed != nullptr;
     const Dims dims = validate_grid(spec);
@@ -339,19 +373,21 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         CK(cudaEventRecord(c->ev_dec0, s));
         uint64_t tiles_done = 0;
         if (attempt == 0) {
-            for (size_t m = 0; m < marks.size(); ++m) {
-                const bool last = m + 1 == marks.size();
+            ChunkMark m;
+            while (next_mark(m)) {
+                const bool last = m.avail_end >= total;
                 const uint64_t t_hi =
-                    last ? n_tiles : std::min<uint64_t>(marks[m].safe_end / kTile, n_tiles);
-                if (marks[m].ready) CK(cudaStreamWaitEvent(s, marks[m].ready, 0));
+                    last ? n_tiles : std::min<uint64_t>(m.safe_end / kTile, n_tiles);
+                if (m.ready) CK(cudaStreamWaitEvent(s, m.ready, 0));
                 if (t_hi > tiles_done) {
-                    P.avail_end = marks[m].avail_end;
+                    P.avail_end = m.avail_end;
                     P.tile_end = static_cast<uint32_t>(t_hi);
                     launch_decode(P, static_cast<uint32_t>(tiles_done), static_cast<uint32_t>(t_hi - tiles_done), s);
                     count_launch();
                     tiles_done = t_hi;
                 }
             }
+            if (tiles_done < n_tiles) fail(CVLG_E_INTERNAL, "input stream ended early");
         } else if (n_tiles) {
             P.avail_end = total;
             P.tile_end = static_cast<uint32_t>(n_tiles);
@@ -688,7 +724,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         uint64_t scap = pow2_at_least(std::max<uint64_t>(F.win ? 1u << 20 : 1u << 18,
                                                          pair_bound / (F.win && dims.T > 48 ? 16 : 2)));
         F.pair_cap = F.win ? pair_room : pair_bound;
-        for (int attempt = 0; attempt < 2; ++attempt) {
+        for (int attempt = 0; attempt < 3; ++attempt) {
             if (++c->fold_epoch == 0) {  // directory tags wrapped: clear the stale ones
                 if (F.dir) CK(cudaMemsetAsync(c->fold_dir.p, 0, c->fold_dir.cap, s));
                 c->fold_epoch = 1;
@@ -718,8 +754,10 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             TRACE(pairs_full ? "fold: pair list overflow, re-run without windows"
                              : "fold: spill table overflow, re-run with a larger table");
             scap = pow2_at_least(2 * pair_bound);
-            if (pairs_full) {  // windows can write more pairs than pair_bound: the retry without
-                F.win = 0;     // them is bounded by it
+            // windows can write more pairs than pair_bound: a retry without them is bounded by it
+            // (the last attempt never keeps windows, whatever the previous one overflowed)
+            if (pairs_full || attempt >= 1) {
+                F.win = 0;
                 F.pair_cap = pair_bound;
             }
         }
@@ -792,9 +830,12 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         radix_sort_pairs(c->pair_key.as<uint64_t>(), c->vals.as<uint32_t>(),
                          c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), n_pairs, 0,
                          gbits + rbits, c->sort_tmp.p, s, d_orand, h_orand);
+        CK(cudaEventRecord(c->ev[4], s));
         launch_finalize(c->pair_key.as<uint64_t>(), c->vals.as<uint32_t>(), n_pairs, rbits,
                         c->pair_sum.as<double>(), c->pair_cnt.as<uint32_t>(), dims.D, dims.RC,
                         d_planes, d_raw, s);
+        } else {
+            CK(cudaEventRecord(c->ev[4], s));
         }
     } else {
         if (feat) {
@@ -810,19 +851,24 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         c->part_long_ids = false;
         CK(cudaEventRecord(c->ev[2], s));
         CK(cudaEventRecord(c->ev[3], s));
+        CK(cudaEventRecord(c->ev[4], s));
     }
-    CK(cudaEventRecord(c->ev[4], s));
+    CK(cudaEventRecord(c->ev[5], s));
     CK(cudaMemcpyAsync(hs, d_stats, kStCount * 8, cudaMemcpyDeviceToHost, s));
     sync(c);
     CK(cudaGetLastError());
     if (hs[kStOverflow]) fail(CVLG_E_INTERNAL, "aggregation capacity invariant violated");
+    // the reference's stages (aggregate.cpp:370-383, 449): parse | dedup+filter+accumulate
+    // (dictionary, canonical order, per-journey fold) | merge (the (cell, journey) sort that
+    // brings every cell's subtotals together) | finalize
     float ms[4] = {0, 0, 0, 0};
     cudaEventElapsedTime(&ms[0], c->ev[0], c->ev[1]);
-    cudaEventElapsedTime(&ms[1], c->ev[1], c->ev[2]);
-    cudaEventElapsedTime(&ms[2], c->ev[2], c->ev[3]);
-    cudaEventElapsedTime(&ms[3], c->ev[3], c->ev[4]);
+    cudaEventElapsedTime(&ms[1], c->ev[1], c->ev[3]);
+    cudaEventElapsedTime(&ms[2], c->ev[3], c->ev[4]);
+    cudaEventElapsedTime(&ms[3], c->ev[4], c->ev[5]);
     for (int i = 0; i < 4; ++i) c->stage_ms[i] = ms[i];
     cudaEventElapsedTime(&c->stage_ms[4], c->ev_dec0, c->ev_dec1);
+    cudaEventElapsedTime(&c->stage_ms[5], c->ev[1], c->ev[2]);
     if (out_stats) {
         cvlg_stats& st = *out_stats;
         std::memset(&st, 0, sizeof(st));
@@ -881,6 +927,7 @@ void run_host(cvlg_context* c, const uint8_t* const* bufs, const uint64_t* lens,
     uint64_t bad = 0;
     host_headers(bufs, lens, n, cmap, good, bad);
     c->csv.ensure(total + 16);
+    c->input_bytes = total;
     uint8_t* d_csv = c->csv.as<uint8_t>();
     // chunked, line-aligned H2D on the copy stream, decode overlapped on the compute stream
     constexpr uint64_t kChunk = 64ull << 20;
@@ -931,7 +978,218 @@ void run_host(cvlg_context* c, const uint8_t* const* bufs, const uint64_t* lens,
         d_raw = c->raw.as<uint32_t>();
     }
     run_core(c, d_csv, off, cmap.data(), good.data(), bad, spec, rules, d_planes, d_raw, stats,
-             marks, false, feat_stop_speed);
+             marks_of(std::move(marks)), false, feat_stop_speed);
+    if (planes)
+        CK(cudaMemcpyAsync(planes, d_planes, lattice_words * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (raw) CK(cudaMemcpyAsync(raw, d_raw, raw_words * 4, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+}
+
+// Shard files in rank order -> HBM through a bounded pinned ring (read_shard's I/O half,
+// ingest.cpp:195-201, threaded like aggregate.cpp:414-443): reader threads fill ring slots with
+// file chunks in any order, this thread enqueues each chunk's H2D copy in input order as soon as
+// it is complete, and run_core decodes every tile whose lines are resident while later chunks are
+// still on disk / in flight. A slot is refilled only after its previous copy completed (event).
+void run_files(cvlg_context* c, const char* const* paths, size_t n, const cvlg_grid_spec* spec,
+               const cvlg_filter_rules* rules, uint32_t n_threads, uint32_t* planes, uint32_t* raw,
+               cvlg_stats* stats) {
+    const Dims dims = validate_grid(spec);
+    std::vector<uint64_t> off(n + 1, 0);
+    std::vector<ColumnMap> cmap(n);
+    std::vector<uint8_t> good(n, 0);
+    uint64_t bad = 0;
+    // sizes and header lines (parse_header, ingest.cpp:204-221) before anything streams
+    for (size_t r = 0; r < n; ++r) {
+        const int fd = ::open(paths[r], O_RDONLY);
+        struct stat st;
+        if (fd < 0 || ::fstat(fd, &st) != 0 || !S_ISREG(st.st_mode)) {
+            if (fd >= 0) ::close(fd);
+            fail(CVLG_E_IO, std::string("Io: cannot open shard ") + paths[r]);
+        }
+        const uint64_t len = static_cast<uint64_t>(st.st_size);
+        off[r + 1] = off[r] + len;
+        ColumnMap m;
+        std::memset(&m, 0xFF, sizeof(m));
+        m.n_columns = 0;
+        if (len) {
+            std::string head;
+            char buf[4096];
+            uint64_t at = 0;
+            size_t nl = std::string::npos;
+            while (at < len) {
+                const ssize_t k = ::pread(fd, buf, sizeof(buf), static_cast<off_t>(at));
+                if (k <= 0) break;
+                head.append(buf, static_cast<size_t>(k));
+                at += static_cast<uint64_t>(k);
+                if ((nl = head.find('\n')) != std::string::npos) break;
+            }
+            size_t hl = nl == std::string::npos ? head.size() : nl;
+            if (hl > 0 && head[hl - 1] == '\r') --hl;
+            good[r] = parse_header(reinterpret_cast<const uint8_t*>(head.data()), static_cast<int64_t>(hl), m) ? 1 : 0;
+            if (!good[r]) ++bad;
+        }
+        cmap[r] = m;
+        ::close(fd);
+    }
+    const uint64_t total = off[n];
+
+    // ring geometry (CVLG_RING_MB / CVLG_RING_SLOTS override: tuning only)
+    uint64_t chunk = 32ull << 20;
+    int slots = 16;
+    if (const char* e = std::getenv("CVLG_RING_MB")) chunk = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
+    if (const char* e = std::getenv("CVLG_RING_SLOTS")) slots = std::max(2, std::atoi(e));
+    struct Chunk {
+        uint32_t r;
+        uint64_t a, len;
+    };
+    std::vector<Chunk> chunks;
+    for (size_t r = 0; r < n; ++r)
+        for (uint64_t a = 0; a < off[r + 1] - off[r]; a += chunk)
+            chunks.push_back(Chunk{static_cast<uint32_t>(r), a, std::min(chunk, off[r + 1] - off[r] - a)});
+    const size_t n_chunks = chunks.size();
+    slots = static_cast<int>(std::min<size_t>(slots, std::max<size_t>(n_chunks, 2)));
+    c->h_ring.ensure(static_cast<uint64_t>(slots) * chunk);
+    while (c->ring_events.size() < static_cast<size_t>(slots)) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ring_events.push_back(e);
+    }
+    uint8_t* ring = static_cast<uint8_t*>(c->h_ring.p);
+    c->csv.ensure(total + 16);
+    c->input_bytes = total;
+    uint8_t* d_csv = c->csv.as<uint8_t>();
+    const uint64_t lattice_words = static_cast<uint64_t>(dims.T) * 8 * dims.RC;
+    const uint64_t raw_words = static_cast<uint64_t>(dims.T) * 4 * dims.RC;
+    c->planes.ensure(lattice_words * 4);
+    uint32_t* d_planes = c->planes.as<uint32_t>();
+    uint32_t* d_raw = nullptr;
+    if (raw) {
+        c->raw.ensure(raw_words * 4);
+        d_raw = c->raw.as<uint32_t>();
+    }
+    // the copies must not start before the previous run finished with the device buffer, and
+    // no slot may be refilled before its last copy (from a previous run) completed
+    cudaEvent_t start_ev = c->ring_events[0];
+    CK(cudaEventRecord(start_ev, c->stream));
+    CK(cudaStreamWaitEvent(c->copy_stream, start_ev, 0));
+    for (int k = 0; k < slots; ++k) CK(cudaEventRecord(c->ring_events[k], c->copy_stream));
+
+    struct Shared {
+        std::mutex mu;
+        std::condition_variable cv;
+        std::vector<uint8_t> ready;
+        size_t enqueued = 0;  // chunks [0, enqueued) have their copy enqueued
+        bool stop = false;
+        std::string err;
+    } sh;
+    sh.ready.assign(n_chunks, 0);
+    std::atomic<size_t> next{0};
+    const int dev = c->device;
+    unsigned workers = n_threads ? n_threads : std::max(1u, std::thread::hardware_concurrency());
+    workers = static_cast<unsigned>(std::min<size_t>({workers, static_cast<size_t>(slots), std::max<size_t>(n_chunks, 1)}));
+    auto reader = [&]() {
+        cudaSetDevice(dev);
+        int fd = -1;
+        uint32_t fd_r = 0xFFFFFFFFu;
+        for (size_t k = next.fetch_add(1); k < n_chunks; k = next.fetch_add(1)) {
+            const Chunk& ch = chunks[k];
+            const int slot = static_cast<int>(k % slots);
+            {
+                std::unique_lock<std::mutex> lk(sh.mu);
+                sh.cv.wait(lk, [&] { return sh.stop || k < static_cast<size_t>(slots) || sh.enqueued > k - slots; });
+                if (sh.stop) break;
+            }
+            if (cudaEventSynchronize(c->ring_events[slot]) != cudaSuccess) {
+                std::lock_guard<std::mutex> lk(sh.mu);
+                sh.err = "cudaEventSynchronize failed on the ingest ring";
+                sh.stop = true;
+                sh.cv.notify_all();
+                break;
+            }
+            if (ch.r != fd_r) {
+                if (fd >= 0) ::close(fd);
+                fd = ::open(paths[ch.r], O_RDONLY);
+                fd_r = ch.r;
+            }
+            uint8_t* dst = ring + static_cast<uint64_t>(slot) * chunk;
+            uint64_t got = 0;
+            while (fd >= 0 && got < ch.len) {
+                const ssize_t rd = ::pread(fd, dst + got, ch.len - got, static_cast<off_t>(ch.a + got));
+                if (rd <= 0) break;
+                got += static_cast<uint64_t>(rd);
+            }
+            std::lock_guard<std::mutex> lk(sh.mu);
+            if (got != ch.len) {
+                sh.err = std::string("Io: read failure on ") + paths[ch.r];
+                sh.stop = true;
+            } else {
+                sh.ready[k] = 1;
+            }
+            sh.cv.notify_all();
+            if (sh.stop) break;
+        }
+        if (fd >= 0) ::close(fd);
+    };
+    std::vector<std::thread> pool;
+    for (unsigned w = 0; w < workers; ++w) pool.emplace_back(reader);
+    auto join_all = [&]() {
+        {
+            std::lock_guard<std::mutex> lk(sh.mu);
+            sh.stop = true;
+            sh.cv.notify_all();
+        }
+        for (auto& t : pool)
+            if (t.joinable()) t.join();
+    };
+
+    uint64_t safe = 0;
+    size_t k_next = 0;
+    MarkSource src = [&](ChunkMark& m) -> bool {
+        if (k_next >= n_chunks) {
+            if (n_chunks == 0 && k_next == 0) {  // empty input: one mark covering nothing
+                ++k_next;
+                m = ChunkMark{total, total, nullptr};
+                return true;
+            }
+            return false;
+        }
+        const size_t k = k_next++;
+        {
+            std::unique_lock<std::mutex> lk(sh.mu);
+            sh.cv.wait(lk, [&] { return sh.ready[k] || !sh.err.empty(); });
+            if (!sh.err.empty()) fail(sh.err.rfind("Io:", 0) == 0 ? CVLG_E_IO : CVLG_E_CUDA, sh.err);
+        }
+        const Chunk& ch = chunks[k];
+        const int slot = static_cast<int>(k % slots);
+        const uint8_t* src_p = ring + static_cast<uint64_t>(slot) * chunk;
+        const uint64_t g0 = off[ch.r] + ch.a, g1 = g0 + ch.len;
+        CK(cudaMemcpyAsync(d_csv + g0, src_p, ch.len, cudaMemcpyHostToDevice, c->copy_stream));
+        CK(cudaEventRecord(c->ring_events[slot], c->copy_stream));
+        if (ch.a + ch.len == off[ch.r + 1] - off[ch.r]) {
+            safe = g1;  // lines never cross a shard end
+        } else {
+            const void* nl = memrchr(src_p, '\n', ch.len);
+            if (nl) safe = g0 + static_cast<uint64_t>(static_cast<const uint8_t*>(nl) - src_p) + 1;
+        }
+        {
+            std::lock_guard<std::mutex> lk(sh.mu);
+            sh.enqueued = k + 1;
+            sh.cv.notify_all();
+        }
+        m = ChunkMark{g1, safe, c->ring_events[slot]};
+        // the final mark must cover the whole input even when trailing shards are empty
+        if (k + 1 == n_chunks) m.avail_end = total;
+        return true;
+    };
+    try {
+        run_core(c, d_csv, off, cmap.data(), good.data(), bad, spec, rules, d_planes, d_raw, stats,
+                 src, false, nullptr);
+    } catch (...) {
+        join_all();
+        cudaStreamSynchronize(c->copy_stream);
+        throw;
+    }
+    join_all();
     if (planes)
         CK(cudaMemcpyAsync(planes, d_planes, lattice_words * 4, cudaMemcpyDeviceToHost, c->stream));
     if (raw) CK(cudaMemcpyAsync(raw, d_raw, raw_words * 4, cudaMemcpyDeviceToHost, c->stream));
@@ -1032,7 +1290,8 @@ void cvlg_context_destroy(cvlg_context* c) {
                       &c->x_keys, &c->x_sum, &c->x_cnt};
     for (DevBuf* b : bufs) b->release();
     c->h_small.release();
-    c->h_csv.release();
+    c->h_ring.release();
+    for (auto e : c->ring_events) cudaEventDestroy(e);
     for (auto e : c->chunk_events) cudaEventDestroy(e);
     for (auto e : c->ev)
         if (e) cudaEventDestroy(e);
@@ -1060,51 +1319,9 @@ int cvlg_run_pipeline(cvlg_context* ctx, const char* const* shard_paths, size_t 
         std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) {
             return std::strcmp(shard_paths[a], shard_paths[b]) < 0;
         });
-        std::vector<uint64_t> lens(n_shards), off(n_shards + 1, 0);
-        for (size_t r = 0; r < n_shards; ++r) {
-            struct stat st;
-            const char* p = shard_paths[order[r]];
-            if (::stat(p, &st) != 0 || !S_ISREG(st.st_mode))
-                fail(CVLG_E_IO, std::string("Io: cannot open shard ") + p);
-            lens[r] = static_cast<uint64_t>(st.st_size);
-            off[r + 1] = off[r] + lens[r];
-        }
-        c->h_csv.ensure(off[n_shards] + 16);
-        uint8_t* host = static_cast<uint8_t*>(c->h_csv.p);
-        unsigned workers = n_threads ? n_threads : std::max(1u, std::thread::hardware_concurrency());
-        workers = static_cast<unsigned>(std::min<size_t>(workers, std::max<size_t>(n_shards, 1)));
-        std::atomic<size_t> next{0};
-        std::vector<std::string> errors(workers);
-        std::vector<std::thread> pool;
-        for (unsigned w = 0; w < workers; ++w) {
-            pool.emplace_back([&, w] {
-                for (size_t r = next.fetch_add(1); r < n_shards; r = next.fetch_add(1)) {
-                    const char* p = shard_paths[order[r]];
-                    const int fd = ::open(p, O_RDONLY);
-                    if (fd < 0) {
-                        errors[w] = std::string("Io: cannot open shard ") + p;
-                        return;
-                    }
-                    uint64_t got = 0;
-                    while (got < lens[r]) {
-                        const ssize_t k = ::read(fd, host + off[r] + got, lens[r] - got);
-                        if (k <= 0) break;
-                        got += static_cast<uint64_t>(k);
-                    }
-                    ::close(fd);
-                    if (got != lens[r]) {
-                        errors[w] = std::string("Io: read failure on ") + p;
-                        return;
-                    }
-                }
-            });
-        }
-        for (auto& t : pool) t.join();
-        for (auto& e : errors)
-            if (!e.empty()) fail(CVLG_E_IO, e);
-        std::vector<const uint8_t*> bufs(n_shards);
-        for (size_t r = 0; r < n_shards; ++r) bufs[r] = host + off[r];
-        run_host(c, bufs.data(), lens.data(), n_shards, spec, rules, planes, raw_count, stats);
+        std::vector<const char*> ranked(n_shards);
+        for (size_t r = 0; r < n_shards; ++r) ranked[r] = shard_paths[order[r]];
+        run_files(c, ranked.data(), n_shards, spec, rules, n_threads, planes, raw_count, stats);
     });
 }
 
@@ -1141,9 +1358,8 @@ int cvlg_run_pipeline_device(cvlg_context* ctx, const uint8_t* d_csv, const uint
         cudaStream_t saved = c->stream;
         if (stream) c->stream = static_cast<cudaStream_t>(stream);
         try {
-            std::vector<ChunkMark> marks{ChunkMark{off.back(), off.back(), nullptr}};
             run_core(c, d_csv, off, nullptr, nullptr, 0, spec, rules, d_planes, d_raw_count, stats,
-                     marks);
+                     marks_of({ChunkMark{off.back(), off.back(), nullptr}}));
         } catch (...) {
             c->stream = saved;
             throw;
@@ -1187,9 +1403,8 @@ int cvlg_journey_features_device(cvlg_context* ctx, const uint8_t* d_csv, const 
         cudaStream_t saved = c->stream;
         if (stream) c->stream = static_cast<cudaStream_t>(stream);
         try {
-            std::vector<ChunkMark> marks{ChunkMark{off.back(), off.back(), nullptr}};
             run_core(c, d_csv, off, nullptr, nullptr, 0, spec, rules, d_planes, d_raw_count, stats,
-                     marks, false, &stop_speed);
+                     marks_of({ChunkMark{off.back(), off.back(), nullptr}}), false, &stop_speed);
         } catch (...) {
             c->stream = saved;
             throw;
@@ -1239,9 +1454,8 @@ int cvlg_partial_device(cvlg_context* ctx, const uint8_t* d_csv, const uint64_t*
         cudaStream_t saved = c->stream;
         if (stream) c->stream = static_cast<cudaStream_t>(stream);
         try {
-            std::vector<ChunkMark> marks{ChunkMark{off.back(), off.back(), nullptr}};
             run_core(c, d_csv, off, nullptr, nullptr, 0, spec, rules, nullptr, nullptr, stats,
-                     marks, true);
+                     marks_of({ChunkMark{off.back(), off.back(), nullptr}}), true);
         } catch (...) {
             c->stream = saved;
             throw;
@@ -1391,9 +1605,16 @@ int cvlg_write_container(const uint32_t* planes, const cvlg_grid_spec* spec, int
     });
 }
 
+int cvlg_context_input(cvlg_context* ctx, const uint8_t** d_csv, uint64_t* n_bytes) {
+    if (!ctx || !d_csv || !n_bytes) return CVLG_E_INVALID_ARG;
+    *d_csv = ctx->csv.as<uint8_t>();
+    *n_bytes = ctx->input_bytes;
+    return CVLG_OK;
+}
+
 int cvlg_last_stage_ms(cvlg_context* ctx, float* ms, int n) {
     if (!ctx || !ms) return CVLG_E_INVALID_ARG;
-    for (int i = 0; i < n && i < 5; ++i) ms[i] = ctx->stage_ms[i];
+    for (int i = 0; i < n && i < 6; ++i) ms[i] = ctx->stage_ms[i];
     return CVLG_OK;
 }
 

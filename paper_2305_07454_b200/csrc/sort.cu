@@ -413,12 +413,11 @@ void radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32
         const unsigned hb = static_cast<unsigned>(std::min<uint64_t>((n + 4095) / 4096, 148 * 4));
         radix_hist8_kernel<<<hb, 256, 0, s>>>(keys, n, hist, dbase, cmask, d_begin, d_end, plan, done);
         count_launch();
-        static bool attr = false;
-        if (!attr) {
+        per_device(kPdOnesweepAttr, [] {
             cudaFuncSetAttribute(radix_onesweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kOsDynSmem));
-            attr = true;
-        }
+            return 1;
+        });
         for (int d = d_begin; d < d_end; ++d) {
             radix_onesweep_kernel<<<n_tiles, kRThreads, kOsDynSmem, s>>>(
                 keys, vals, keys_alt, vals_alt, n, 8 * d, dbase + d * 256,

@@ -231,6 +231,68 @@ int64_t cvlg_synth_day_owned(uint64_t seed, uint32_t n_journeys, uint32_t n_shar
     return static_cast<int64_t>(total);
 }
 
+// The same day written straight to shard files `out_dir/shard_%04u.csv` (generate_day's names,
+// synth.cpp:157-160) with one host thread per file at a time: memory stays bounded by one
+// journey batch per thread, so c3-sized days (34 GB) never sit in host memory at once.
+// Returns the total bytes written, or < 0 (-3: I/O failure).
+int64_t cvlg_synth_write_day(uint64_t seed, uint32_t n_journeys, uint32_t n_shards,
+                             double sample_period, double mean_duration, int32_t day_number,
+                             uint32_t n_threads, const char* out_dir, uint64_t* total_rows) {
+    if (n_shards == 0 || !(sample_period > 0.0) || !out_dir) return -2;
+    Cfg c;
+    c.seed = seed;
+    c.lat_min = 36.0;
+    c.lat_max = 40.6;
+    c.lon_min = -95.8;
+    c.lon_max = -89.1;
+    c.sample_period = sample_period;
+    c.mean_duration = mean_duration;
+    c.speed_min = 0.0;
+    c.speed_max = 130.0;
+    c.heading_sigma = 6.0;
+    c.day_start = static_cast<int64_t>(day_number) * 86400;
+    static const char kHeader[] = "Journey Id,Timestamp,Latitude,Longitude,Postal Code,Speed,Heading\n";
+    const unsigned workers = std::min<unsigned>(
+        n_threads ? n_threads : std::max(1u, std::thread::hardware_concurrency()), n_shards);
+    std::atomic<uint32_t> next{0};
+    std::atomic<uint64_t> rows{0}, bytes{0};
+    std::atomic<bool> bad{false};
+    std::vector<std::thread> pool;
+    for (unsigned w = 0; w < workers; ++w)
+        pool.emplace_back([&] {
+            std::string buf;
+            buf.reserve(72u << 20);
+            for (uint32_t s = next.fetch_add(1); s < n_shards && !bad; s = next.fetch_add(1)) {
+                char path[4096];
+                std::snprintf(path, sizeof(path), "%s/shard_%04u.csv", out_dir, s);
+                std::FILE* f = std::fopen(path, "wb");
+                if (!f) {
+                    bad = true;
+                    break;
+                }
+                buf.assign(kHeader, sizeof(kHeader) - 1);
+                uint64_t r = 0, b = 0;
+                for (uint32_t j = s; j < n_journeys; j += n_shards) {
+                    r += gen_journey(j, c, buf);
+                    if (buf.size() > (64u << 20)) {
+                        if (std::fwrite(buf.data(), 1, buf.size(), f) != buf.size()) bad = true;
+                        b += buf.size();
+                        buf.clear();
+                    }
+                }
+                if (std::fwrite(buf.data(), 1, buf.size(), f) != buf.size()) bad = true;
+                b += buf.size();
+                if (std::fclose(f) != 0) bad = true;
+                rows += r;
+                bytes += b;
+            }
+        });
+    for (auto& t : pool) t.join();
+    if (bad) return -3;
+    if (total_rows) *total_rows = rows.load();
+    return static_cast<int64_t>(bytes.load());
+}
+
 // Adversarial variant of a generated day: every data row of the input shards
 // (each shard = header line + rows) shuffled with a seeded Fisher-Yates permutation and dealt
 // round-robin to n_out shards, each starting with `header`. Returns bytes written, or < 0.

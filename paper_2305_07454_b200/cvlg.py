@@ -33,7 +33,7 @@ ERR_NAMES = [
 EXTRA_ERRS = {100: "Cuda", 101: "InvalidArgument", 102: "Unsupported", 103: "Internal"}
 REJECT_NAMES = ["BadTimestamp", "BadNumeric", "MissingField", "RangeViolation", "BadHeader"]
 FILTER_NAMES = ["OutOfGrid", "SpeedCeiling", "MissingField"]
-STAGE_NAMES = ["decode", "dictionary+order", "fold", "finalize"]
+STAGE_NAMES = ["parse", "dedup+filter+accumulate", "merge", "finalize"]  # aggregate.cpp:370-383, 449
 
 
 class CvlError(RuntimeError):
@@ -102,6 +102,7 @@ def _load() -> ctypes.CDLL:
     lib.cvlg_write_container.argtypes = [vp, ctypes.POINTER(_Grid), ctypes.c_int32,
                                          ctypes.c_char_p, u64p]
     lib.cvlg_last_stage_ms.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int]
+    lib.cvlg_context_input.argtypes = [vp, ctypes.POINTER(vp), u64p]
     lib.cvlg_pin_host.argtypes = [vp, ctypes.c_size_t]
     lib.cvlg_unpin_host.argtypes = [vp]
     lib.cvlg_launch_count.restype = ctypes.c_uint64
@@ -125,7 +126,7 @@ EXPORTED_SYMBOLS = [
     "cvlg_context_destroy", "cvlg_run_pipeline", "cvlg_run_pipeline_host",
     "cvlg_run_pipeline_device", "cvlg_write_container", "cvlg_last_stage_ms", "cvlg_pin_host",
     "cvlg_unpin_host", "cvlg_launch_count", "cvlg_last_error", "cvlg_journey_features_host",
-    "cvlg_journey_features_device", "cvlg_features_copy",
+    "cvlg_journey_features_device", "cvlg_features_copy", "cvlg_context_input",
 ]
 
 
@@ -303,9 +304,17 @@ class Context:
         except Exception:
             pass
 
+    def input(self) -> tuple[int, int]:
+        """(device pointer, bytes) of the input the last file/host run left resident in HBM."""
+        p = ctypes.c_void_p()
+        n = ctypes.c_uint64()
+        _check(_lib.cvlg_context_input(self._h, ctypes.byref(p), ctypes.byref(n)))
+        return int(p.value or 0), int(n.value)
+
     def stage_ms(self) -> list[float]:
-        arr = (ctypes.c_float * 5)()
-        _lib.cvlg_last_stage_ms(self._h, arr, 5)
+        """[parse, dedup+filter+accumulate, merge, finalize, decode kernel, dictionary+order]"""
+        arr = (ctypes.c_float * 6)()
+        _lib.cvlg_last_stage_ms(self._h, arr, 6)
         return list(arr)
 
 
@@ -328,14 +337,16 @@ def _paths(manifest) -> list[str]:
 def run_pipeline(manifest, spec: GridSpec | None = None, rules: FilterRules | None = None,
                  n_partitions: int = 1, n_threads: int = 0,
                  stats: PipelineStats | None = None, ctx: Context | None = None,
-                 raw: bool = True) -> Lattice:
-    """cvl::run_pipeline (aggregate.hpp:125-127): shard files -> lattice, on the GPU."""
+                 raw: bool = True, out: tuple | None = None) -> Lattice:
+    """cvl::run_pipeline (aggregate.hpp:125-127): shard files -> lattice, on the GPU. The files
+    stream through a bounded pinned ring (n_threads reader threads) into HBM while decode runs.
+    `out` = (planes, raw) host arrays to fill (e.g. pinned) instead of fresh ones."""
     spec = spec or GridSpec()
     rules = rules or FilterRules()
     ctx = ctx or default_context()
     paths = _paths(manifest)
     arr = (ctypes.c_char_p * max(len(paths), 1))(*[p.encode() for p in paths])
-    planes, rawa = _alloc(spec, raw)
+    planes, rawa = out if out is not None else _alloc(spec, raw)
     st = _Stats()
     _check(_lib.cvlg_run_pipeline(ctx.handle, arr, len(paths), ctypes.byref(spec._c()),
                                   ctypes.byref(rules._c()), n_partitions, n_threads,
@@ -522,6 +533,28 @@ def synth_day(seed: int = 0, journeys: int = 100, shards: int = 8, sample_period
     if n < 0:
         raise CvlError(101, f"synth_day failed ({n})")
     return out[:n], list(offs), rows.value
+
+
+def synth_write_day(out_dir, seed: int = 0, journeys: int = 100, shards: int = 8,
+                    sample_period: float = 1.0, mean_duration: float = 300.0,
+                    day: str = "2021-05-09", threads: int = 0) -> tuple[int, int]:
+    """Writes the reference generate_day's shard files (byte-identical, synth.cpp:145-181) to
+    out_dir with one host thread per file. Returns (bytes, rows)."""
+    import datetime
+    d = datetime.date.fromisoformat(day)
+    day_number = (d - datetime.date(1970, 1, 1)).days
+    os.makedirs(out_dir, exist_ok=True)
+    rows = ctypes.c_uint64()
+    fn = _lib.cvlg_synth_write_day
+    fn.restype = ctypes.c_int64
+    fn.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_double,
+                   ctypes.c_double, ctypes.c_int32, ctypes.c_uint32, ctypes.c_char_p,
+                   ctypes.POINTER(ctypes.c_uint64)]
+    n = fn(seed, journeys, shards, sample_period, mean_duration, day_number, threads,
+           str(out_dir).encode(), ctypes.byref(rows))
+    if n < 0:
+        raise CvlError(11 if n == -3 else 101, f"synth_write_day failed ({n})")
+    return int(n), rows.value
 
 
 def shuffle_rows(blob: np.ndarray, offs: Sequence[int], n_out: int, seed: int = 7,

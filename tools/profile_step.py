@@ -18,11 +18,18 @@ ap.add_argument("--shuffle", action="store_true")
 ap.add_argument("--days", type=int, default=1)
 ap.add_argument("--fine", action="store_true")
 a = ap.parse_args()
-if a.days > 1:  # c5 shape: the bench's multi-day generator
-    sys.argv = sys.argv[:1]
-    import bench
-    blob, offs, rows = bench.generate(a.journeys, a.shards, 500.0, seed=1, days=a.days)
-    offs = list(offs)
+if a.days > 1:  # c5 shape: day k uses seed 1 + k and date + k; its shards follow day k-1's
+    import datetime
+    import numpy as np
+    blobs, offs, rows = [], [0], 0
+    for k in range(a.days):
+        d = (datetime.date(2021, 5, 9) + datetime.timedelta(days=k)).isoformat()
+        b, o, r = cvlg.synth_day(seed=1 + k, journeys=a.journeys, shards=a.shards,
+                                 mean_duration=500.0, day=d)
+        offs.extend(offs[-1] + int(x) for x in o[1:])
+        blobs.append(b)
+        rows += r
+    blob = np.concatenate(blobs)
 else:
     blob, offs, rows = cvlg.synth_day(seed=1, journeys=a.journeys, shards=a.shards,
                                       mean_duration=500.0)
