@@ -150,6 +150,61 @@ int cvlg_finalize_pairs(cvlg_context* ctx, const uint64_t* d_cell, const uint64_
                         uint64_t n, const cvlg_grid_spec* spec, uint32_t* d_planes,
                         uint32_t* d_raw_count, void* stream);
 
+/* ---- multi-GPU pipeline, one host thread ---------------------------
+ * cvl::run_pipeline over n_gpus GPUs: journeys are sharded by journey_hash(id) % n_gpus
+ * (FNV-1a 64, ingest.cpp:287-291), like the reference's partitions (aggregate.cpp:414-443). Each
+ * GPU streams a 1/n_gpus byte range of the shards (cut at line boundaries) into HBM, routes every
+ * data line to the GPU owning its journey (stores into the peer's HBM over NVLink), aggregates its
+ * journeys, and sends (cell, journey key, sum, count) tuples to the GPU owning the cell's time
+ * slab, which folds them in the reference's (cell, journey) order. Output and stats are
+ * byte-identical to cvlg_run_pipeline for every n_gpus. `devices` lists the CUDA devices (NULL:
+ * 0..n_gpus-1); a device may repeat (several shards on one GPU). Journey ids must be <= 15 bytes
+ * when n_gpus > 1 (exact inline keys across GPUs), else CVLG_E_UNSUPPORTED. */
+typedef struct cvlg_multi cvlg_multi;
+cvlg_multi* cvlg_multi_create(const int* devices, uint32_t n_gpus);
+void cvlg_multi_destroy(cvlg_multi* m);
+uint32_t cvlg_multi_size(const cvlg_multi* m);
+cvlg_context* cvlg_multi_context(cvlg_multi* m, uint32_t gpu);  /* borrowed */
+int cvlg_run_pipeline_multi(cvlg_multi* m, const char* const* shard_paths, size_t n_shards,
+                            const cvlg_grid_spec* spec, const cvlg_filter_rules* rules,
+                            uint32_t n_partitions, uint32_t n_threads, uint32_t* planes,
+                            uint32_t* raw_count, cvlg_stats* stats);
+
+/* The same steps for one process per GPU (the caller moves bytes, e.g. NCCL all-to-all):
+ *  1. cvlg_route_stage: rank the paths, cut the data lines into n_parts ranges, stream range
+ *     `part` into this context's HBM and count the bytes each owner (0..n_parts-1) receives.
+ *  2. cvlg_route_plan: bytes of the stream for `owner` and the offsets (within it) of its
+ *     n_pieces virtual shards (header line + the piece's lines routed to `owner`).
+ *  3. cvlg_route_scatter: writes the streams to d_dst[owner] (device pointers on this device).
+ *     The owner concatenates the streams of parts 0..n_parts-1 in order and runs
+ *     cvlg_partial_device over them with the virtual shard offsets as shard_offsets; the BadHeader
+ *     count (bad_headers, identical on every part) is added once.
+ *  4. cvlg_tuples_export: the subtotals of that run as 40-byte (u64 cell, u64 key0, u64 key1,
+ *     f64 sum, u64 count) tuples, counted per slab owner (counts[n_owners], owner of a tuple =
+ *     t * n_owners / T for its time bin t; cvlg_slab_rows gives each owner's rows [t0, t1)).
+ *  5. cvlg_tuples_scatter: writes them to d_dst[owner] (device pointers on this device).
+ *  6. cvlg_finalize_tuples: folds received tuples into a lattice (rows of the owner's slab). */
+int cvlg_route_stage(cvlg_context* ctx, const char* const* shard_paths, size_t n_shards,
+                     uint32_t n_parts, uint32_t part, uint32_t n_threads, uint64_t* n_pieces,
+                     uint64_t* bad_headers);
+/* Re-runs the count of step 1 on the range already in HBM (device-resident measurements). */
+int cvlg_route_count(cvlg_context* ctx);
+int cvlg_route_plan(cvlg_context* ctx, uint32_t owner, uint64_t* vshard_off, uint64_t* stream_len);
+int cvlg_route_scatter(cvlg_context* ctx, uint8_t* const* d_dst, void* stream);
+int cvlg_tuples_export(cvlg_context* ctx, const cvlg_grid_spec* spec, uint32_t n_owners,
+                       uint64_t* counts, uint64_t* n_tuples);
+int cvlg_tuples_scatter(cvlg_context* ctx, const cvlg_grid_spec* spec, uint32_t n_owners,
+                        void* const* d_dst, void* stream);
+int cvlg_finalize_tuples(cvlg_context* ctx, const void* d_tuples, uint64_t n,
+                         const cvlg_grid_spec* spec, uint32_t* d_planes, uint32_t* d_raw_count,
+                         void* stream);
+int cvlg_slab_rows(uint32_t n_batches, uint32_t n_owners, uint32_t owner, uint32_t* t0, uint32_t* t1);
+/* Host only (no GPU needed): the pieces of part `part` of n_parts, as cvlg_route_stage cuts them:
+ * (rank of the file in lexicographic path order, byte offset, length), at most `cap` written. */
+int cvlg_split_manifest(const char* const* shard_paths, size_t n_shards, uint32_t n_parts,
+                        uint32_t part, uint32_t* piece_file, uint64_t* piece_off, uint64_t* piece_len,
+                        size_t cap, size_t* n_pieces);
+
 /* ---- per-journey feature table (north_star extension) -----------------
  * NOT IN THE REFERENCE (proj/ has no such function): parity is against this repository's CPU
  * restatement (tests/test_features.py), never against cvl::run_pipeline. Runs the pipeline (the

@@ -4,7 +4,7 @@ The product is the C-ABI library ``lib/libcvlg.so`` (CUDA kernels in ``csrc/``);
 is the Python host mirror of the reference pipeline API on top of it (see cvlg.py).
 """
 from .cvlg import (  # noqa: F401
-    BatchFrame, Context, CvlError, FilterRules, GridSpec, Lattice, PipelineStats,
+    BatchFrame, Context, CvlError, FilterRules, GridSpec, Lattice, MultiGPU, PipelineStats,
     journey_features_device, journey_features_host, journey_ids, launch_count, pin_host, run_pipeline, run_pipeline_device,
     run_pipeline_host, synth_day, unpin_host, write_container,
 )

@@ -170,11 +170,12 @@ void launch_rank_slot(const uint32_t* uslot, const uint32_t* perm, uint64_t n, u
 void launch_export_pairs(const uint64_t* pkey, const double* psum, const uint32_t* pcnt, uint64_t n,
                          int rbits, const uint32_t* rank_slot, const unsigned long long* table,
                          uint64_t* cell, uint64_t* k0, uint64_t* k1, double* sum, uint64_t* cnt,
-                         uint32_t* bad, cudaStream_t s);
-void launch_gather_u64(const uint64_t* src, const uint32_t* idx, uint64_t n, uint64_t* dst,
-                       cudaStream_t s);
-void launch_import_pairs(const double* sum, const uint64_t* cnt, uint64_t n, double* psum,
-                         uint32_t* pcnt, cudaStream_t s);
+                         uint64_t stride, uint32_t* bad, cudaStream_t s);
+// dst[i] = src[(idx ? idx[i] : i) * stride]  (stride in u64 words: 1 = SoA column, 5 = PairTuple)
+void launch_gather_u64(const uint64_t* src, uint64_t stride, const uint32_t* idx, uint64_t n,
+                       uint64_t* dst, cudaStream_t s);
+void launch_import_pairs(const double* sum, const uint64_t* cnt, uint64_t stride, uint64_t n,
+                         double* psum, uint32_t* pcnt, cudaStream_t s);
 void launch_finalize(const uint64_t* keys, const uint32_t* vals, uint64_t n, int rank_bits,
                      const double* pair_sum, const uint32_t* pair_cnt, uint32_t D, uint64_t RC,
                      uint32_t* planes, uint32_t* raw, cudaStream_t s);

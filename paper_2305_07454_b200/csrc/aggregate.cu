@@ -973,7 +973,8 @@ __global__ void rank_slot_kernel(const uint32_t* uslot, const uint32_t* perm, ui
 __global__ void export_pairs_kernel(const uint64_t* pkey, const double* psum, const uint32_t* pcnt,
                                     uint64_t n, int rbits, const uint32_t* rank_slot,
                                     const unsigned long long* table, uint64_t* cell, uint64_t* k0,
-                                    uint64_t* k1, double* sum, uint64_t* cnt, uint32_t* bad) {
+                                    uint64_t* k1, double* sum, uint64_t* cnt, uint64_t stride,
+                                    uint32_t* bad) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (i >= n) return;
     const uint64_t key = pkey[i];
@@ -981,25 +982,26 @@ __global__ void export_pairs_kernel(const uint64_t* pkey, const double* psum, co
     const uint32_t slot = rank_slot[r];
     const uint64_t e0 = table[2 * slot], e1 = table[2 * slot + 1];
     if ((e1 & 0xFF) == 0xFF) *bad = 1u;  // id longer than 15 bytes: no exact inline key
-    cell[i] = key >> rbits;
-    k0[i] = e0;
-    k1[i] = e1;
-    sum[i] = psum[i];
-    cnt[i] = pcnt[i];
+    const uint64_t o = i * stride;
+    cell[o] = key >> rbits;
+    k0[o] = e0;
+    k1[o] = e1;
+    sum[o] = psum[i];
+    cnt[o] = pcnt[i];
 }
 
-__global__ void gather_u64_kernel(const uint64_t* src, const uint32_t* idx, uint64_t n,
-                                  uint64_t* dst) {
+__global__ void gather_u64_kernel(const uint64_t* src, uint64_t stride, const uint32_t* idx,
+                                  uint64_t n, uint64_t* dst) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    if (i < n) dst[i] = src[idx[i]];
+    if (i < n) dst[i] = src[(idx ? idx[i] : i) * stride];
 }
 
-__global__ void import_pairs_kernel(const double* sum, const uint64_t* cnt, uint64_t n,
-                                    double* psum, uint32_t* pcnt) {
+__global__ void import_pairs_kernel(const double* sum, const uint64_t* cnt, uint64_t stride,
+                                    uint64_t n, double* psum, uint32_t* pcnt) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (i >= n) return;
-    psum[i] = sum[i];
-    pcnt[i] = static_cast<uint32_t>(cnt[i]);
+    psum[i] = sum[i * stride];
+    pcnt[i] = static_cast<uint32_t>(cnt[i * stride]);
 }
 
 inline unsigned grid_for(uint64_t n, int bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
@@ -1199,24 +1201,24 @@ void launch_rank_slot(const uint32_t* uslot, const uint32_t* perm, uint64_t n, u
 void launch_export_pairs(const uint64_t* pkey, const double* psum, const uint32_t* pcnt, uint64_t n,
                          int rbits, const uint32_t* rank_slot, const unsigned long long* table,
                          uint64_t* cell, uint64_t* k0, uint64_t* k1, double* sum, uint64_t* cnt,
-                         uint32_t* bad, cudaStream_t s) {
+                         uint64_t stride, uint32_t* bad, cudaStream_t s) {
     if (!n) return;
     export_pairs_kernel<<<grid_for(n, 256), 256, 0, s>>>(pkey, psum, pcnt, n, rbits, rank_slot,
-                                                         table, cell, k0, k1, sum, cnt, bad);
+                                                         table, cell, k0, k1, sum, cnt, stride, bad);
     count_launch();
 }
 
-void launch_gather_u64(const uint64_t* src, const uint32_t* idx, uint64_t n, uint64_t* dst,
-                       cudaStream_t s) {
+void launch_gather_u64(const uint64_t* src, uint64_t stride, const uint32_t* idx, uint64_t n,
+                       uint64_t* dst, cudaStream_t s) {
     if (!n) return;
-    gather_u64_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, idx, n, dst);
+    gather_u64_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, stride, idx, n, dst);
     count_launch();
 }
 
-void launch_import_pairs(const double* sum, const uint64_t* cnt, uint64_t n, double* psum,
-                         uint32_t* pcnt, cudaStream_t s) {
+void launch_import_pairs(const double* sum, const uint64_t* cnt, uint64_t stride, uint64_t n,
+                         double* psum, uint32_t* pcnt, cudaStream_t s) {
     if (!n) return;
-    import_pairs_kernel<<<grid_for(n, 256), 256, 0, s>>>(sum, cnt, n, psum, pcnt);
+    import_pairs_kernel<<<grid_for(n, 256), 256, 0, s>>>(sum, cnt, stride, n, psum, pcnt);
     count_launch();
 }
 

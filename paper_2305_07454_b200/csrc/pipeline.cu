@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "../../include/cvlg.h"
+#include "pipeline_internal.cuh"
 #include "agg_api.cuh"
 #include "kernels.cuh"
 #include "sort_api.cuh"
@@ -54,64 +55,46 @@ int per_device(int key, int (*compute)()) {
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
-namespace {
-
 thread_local std::string t_last_error;
-
-struct Error {
-    int code;
-    std::string msg;
-};
 
 [[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
 
 void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(CVLG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
-#define CK(x) cuda_check((x), #x)
 
-struct DevBuf {
-    void* p = nullptr;
-    size_t cap = 0;
-    bool ensure(size_t bytes) {  // true when (re)allocated: contents undefined
-        if (bytes <= cap && p) return false;
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-        const size_t want = std::max<size_t>(bytes, 256);
-        CK(cudaMalloc(&p, want));
-        cap = want;
-        return true;
-    }
-    template <typename T>
-    T* as() const { return static_cast<T*>(p); }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-    }
-};
+bool DevBuf::ensure(size_t bytes) {
+    if (bytes <= cap && p) return false;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(bytes, 256);
+    CK(cudaMalloc(&p, want));
+    cap = want;
+    return true;
+}
+void DevBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+}
 
-struct HostPinned {
-    void* p = nullptr;
-    size_t cap = 0;
-    void ensure(size_t bytes) {
-        if (bytes <= cap && p) return;
-        if (p) cudaFreeHost(p);
-        p = nullptr;
-        cap = 0;
-        const size_t want = std::max<size_t>(bytes, 4096);
-        CK(cudaHostAlloc(&p, want, cudaHostAllocDefault));
-        cap = want;
-    }
-    void release() {
-        if (p) cudaFreeHost(p);
-        p = nullptr;
-        cap = 0;
-    }
-};
+void HostPinned::ensure(size_t bytes) {
+    if (bytes <= cap && p) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(bytes, 4096);
+    CK(cudaHostAlloc(&p, want, cudaHostAllocDefault));
+    cap = want;
+}
+void HostPinned::release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+}
 
-int bits_for(uint64_t v) {  // bits needed to represent values 0..v
+int bits_for(uint64_t v) {
     int b = 0;
     while (b < 64 && (v >> b)) ++b;
     return b;
@@ -122,11 +105,6 @@ uint64_t pow2_at_least(uint64_t v) {
     while (p < v) p <<= 1;
     return p;
 }
-
-struct Dims {
-    uint32_t T, D, R, C;
-    uint64_t RC, cells;
-};
 
 Dims validate_grid(const cvlg_grid_spec* s) {
     if (!s) fail(CVLG_E_INVALID_ARG, "grid spec is NULL");
@@ -155,6 +133,17 @@ Dims validate_grid(const cvlg_grid_spec* s) {
         fail(CVLG_E_UNSUPPORTED, "grid has >= 2^31-16 cells; the device cell code is 31-bit");
     return d;
 }
+
+MarkSource marks_of(std::vector<ChunkMark> v) {
+    auto st = std::make_shared<std::pair<std::vector<ChunkMark>, size_t>>(std::move(v), 0);
+    return [st](ChunkMark& m) {
+        if (st->second >= st->first.size()) return false;
+        m = st->first[st->second++];
+        return true;
+    };
+}
+
+namespace {
 
 GridParams make_params(const cvlg_grid_spec* s, const cvlg_filter_rules* r, const Dims& d) {
     GridParams g;
@@ -197,63 +186,9 @@ __global__ void init_run_kernel(uint64_t* stats) {
 
 unsigned blocks_for(uint64_t n, int bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
 
+uint64_t* h_small64(cvlg_context* c) { return static_cast<uint64_t*>(c->h_small.p); }
+
 }  // namespace
-
-// A chunk of CSV bytes that became resident: decode every tile whose lines are complete.
-struct ChunkMark {
-    uint64_t avail_end;  // bytes [0, avail_end) resident
-    uint64_t safe_end;   // every line starting before safe_end ends before it
-    cudaEvent_t ready;   // recorded on the copy stream (nullptr: already resident)
-};
-
-// Yields the marks of a run in order (blocking until the next chunk's copy is enqueued); false
-// once the input is complete. The last mark yielded covers every byte.
-using MarkSource = std::function<bool(ChunkMark&)>;
-
-MarkSource marks_of(std::vector<ChunkMark> v) {
-    auto st = std::make_shared<std::pair<std::vector<ChunkMark>, size_t>>(std::move(v), 0);
-    return [st](ChunkMark& m) {
-        if (st->second >= st->first.size()) return false;
-        m = st->first[st->second++];
-        return true;
-    };
-}
-
-}  // namespace cvlg
-
-using namespace cvlg;
-
-struct cvlg_context {
-    int device = 0;
-    cudaStream_t stream = nullptr, copy_stream = nullptr;
-    bool own_stream = true;
-    DevBuf csv, shard_off, cmap, good, counter, stats;
-    DevBuf ts, speed, code, loff, hslot, hscr, hend, tiles, thpos, hid_scr, hid, runs;
-    DevBuf ts2, speed2, code2, loff2;  // dense copies for the slow (full-sort) path
-    // per-journey features (cvlg_journey_features_*): lat/lon per slot, outputs per journey / cell
-    DevBuf lat, lon, lat2, lon2, f_points, f_tfirst, f_tlast, f_len, f_step, f_vmax, f_acc, f_dwell,
-        f_stops, f_id, f_first, f_cmin, f_cmax;
-    uint64_t f_J = 0, f_cells = 0;
-    DevBuf dict, hdict, flags, pos, uslot, rank_of_slot, hrank, scal;
-    DevBuf keys, vals, keys_alt, vals_alt, sort_tmp, scan_tmp, srank, jstart;
-    DevBuf pair_key, pair_sum, pair_cnt, spill_key, spill_sum, spill_cnt, fold_dir, dead;
-    uint32_t fold_epoch = 0;
-    bool slow_key_ts = false;
-    DevBuf planes, raw, rank_slot, x_keys, x_sum, x_cnt;
-    HostPinned h_small, h_ring;
-    std::vector<cudaEvent_t> ring_events;  // one per ring slot: its last H2D copy
-    // last cvlg_partial_device run: pairs kept in pair_key/pair_sum/pair_cnt
-    uint64_t part_pairs = 0, part_J = 0, last_slots = 0;
-    uint64_t input_bytes = 0;  // bytes of c->csv staged by the last host/file run
-    int part_rbits = 0;
-    bool part_long_ids = false;
-    std::vector<cudaEvent_t> chunk_events;
-    cudaEvent_t ev[6] = {};
-    cudaEvent_t ev_dec0 = nullptr, ev_dec1 = nullptr;
-    float stage_ms[6] = {0, 0, 0, 0, 0, 0};
-};
-
-namespace {
 
 cvlg_context* default_context() {
     thread_local cvlg_context* ctx = nullptr;
@@ -261,9 +196,9 @@ cvlg_context* default_context() {
     return ctx;
 }
 
-uint64_t* h_small64(cvlg_context* c) { return static_cast<uint64_t*>(c->h_small.p); }
-
 void sync(cvlg_context* c) { CK(cudaStreamSynchronize(c->stream)); }
+
+namespace {
 
 // CVLG_TRACE=1: host timestamps of the pipeline phases on stderr (diagnostics only)
 struct Tracer {
@@ -276,13 +211,15 @@ struct Tracer {
     }
 };
 
+}  // namespace
+
 // The pipeline proper over CSV bytes in HBM. `marks` drive incremental decode while the bytes
 // stream in; the last mark must cover everything.
 void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>& shard_off,
               const ColumnMap* h_cmap, const uint8_t* h_good, uint64_t bad_headers,
               const cvlg_grid_spec* spec, const cvlg_filter_rules* rules, uint32_t* d_planes,
               uint32_t* d_raw, cvlg_stats* out_stats, const MarkSource& next_mark,
-              bool partial = false, const double* feat_stop_speed = nullptr) {
+              bool partial, const double* feat_stop_speed) {
     const bool feat = feat_stop_speed != nullptr;
     const Dims dims = validate_grid(spec);
     const GridParams gp = make_params(spec, rules, dims);
@@ -889,6 +826,8 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
              "OutOfBounds: a kept record lies outside the grid (require_in_grid = false)");
 }
 
+namespace {
+
 // Host-side header map for shards whose bytes are in host memory.
 void host_headers(const uint8_t* const* bufs, const uint64_t* lens, size_t n,
                   std::vector<ColumnMap>& cmap, std::vector<uint8_t>& good, uint64_t& bad) {
@@ -985,76 +924,28 @@ void run_host(cvlg_context* c, const uint8_t* const* bufs, const uint64_t* lens,
     sync(c);
 }
 
-// Shard files in rank order -> HBM through a bounded pinned ring (read_shard's I/O half,
-// ingest.cpp:195-201, threaded like aggregate.cpp:414-443): reader threads fill ring slots with
-// file chunks in any order, this thread enqueues each chunk's H2D copy in input order as soon as
-// it is complete, and run_core decodes every tile whose lines are resident while later chunks are
-// still on disk / in flight. A slot is refilled only after its previous copy completed (event).
+// Shard files in rank order -> HBM through the bounded pinned ring (read_shard's I/O half,
+// ingest.cpp:195-201, threaded like aggregate.cpp:414-443): run_core decodes every tile whose
+// lines are resident while later chunks are still on disk / in flight.
 void run_files(cvlg_context* c, const char* const* paths, size_t n, const cvlg_grid_spec* spec,
                const cvlg_filter_rules* rules, uint32_t n_threads, uint32_t* planes, uint32_t* raw,
                cvlg_stats* stats) {
     const Dims dims = validate_grid(spec);
+    // sizes and header lines (parse_header, ingest.cpp:204-221) before anything streams
+    const std::vector<ShardHead> heads = read_shard_heads(paths, n);
     std::vector<uint64_t> off(n + 1, 0);
     std::vector<ColumnMap> cmap(n);
     std::vector<uint8_t> good(n, 0);
     uint64_t bad = 0;
-    // sizes and header lines (parse_header, ingest.cpp:204-221) before anything streams
+    std::vector<FileRange> ranges;
     for (size_t r = 0; r < n; ++r) {
-        const int fd = ::open(paths[r], O_RDONLY);
-        struct stat st;
-        if (fd < 0 || ::fstat(fd, &st) != 0 || !S_ISREG(st.st_mode)) {
-            if (fd >= 0) ::close(fd);
-            fail(CVLG_E_IO, std::string("Io: cannot open shard ") + paths[r]);
-        }
-        const uint64_t len = static_cast<uint64_t>(st.st_size);
-        off[r + 1] = off[r] + len;
-        ColumnMap m;
-        std::memset(&m, 0xFF, sizeof(m));
-        m.n_columns = 0;
-        if (len) {
-            std::string head;
-            char buf[4096];
-            uint64_t at = 0;
-            size_t nl = std::string::npos;
-            while (at < len) {
-                const ssize_t k = ::pread(fd, buf, sizeof(buf), static_cast<off_t>(at));
-                if (k <= 0) break;
-                head.append(buf, static_cast<size_t>(k));
-                at += static_cast<uint64_t>(k);
-                if ((nl = head.find('\n')) != std::string::npos) break;
-            }
-            size_t hl = nl == std::string::npos ? head.size() : nl;
-            if (hl > 0 && head[hl - 1] == '\r') --hl;
-            good[r] = parse_header(reinterpret_cast<const uint8_t*>(head.data()), static_cast<int64_t>(hl), m) ? 1 : 0;
-            if (!good[r]) ++bad;
-        }
-        cmap[r] = m;
-        ::close(fd);
+        off[r + 1] = off[r] + heads[r].len;
+        cmap[r] = heads[r].cmap;
+        good[r] = heads[r].good ? 1 : 0;
+        if (heads[r].bad_header) ++bad;
+        if (heads[r].len) ranges.push_back(FileRange{static_cast<uint32_t>(r), 0, heads[r].len, off[r]});
     }
     const uint64_t total = off[n];
-
-    // ring geometry (CVLG_RING_MB / CVLG_RING_SLOTS override: tuning only)
-    uint64_t chunk = 32ull << 20;
-    int slots = 16;
-    if (const char* e = std::getenv("CVLG_RING_MB")) chunk = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
-    if (const char* e = std::getenv("CVLG_RING_SLOTS")) slots = std::max(2, std::atoi(e));
-    struct Chunk {
-        uint32_t r;
-        uint64_t a, len;
-    };
-    std::vector<Chunk> chunks;
-    for (size_t r = 0; r < n; ++r)
-        for (uint64_t a = 0; a < off[r + 1] - off[r]; a += chunk)
-            chunks.push_back(Chunk{static_cast<uint32_t>(r), a, std::min(chunk, off[r + 1] - off[r] - a)});
-    const size_t n_chunks = chunks.size();
-    slots = static_cast<int>(std::min<size_t>(slots, std::max<size_t>(n_chunks, 2)));
-    c->h_ring.ensure(static_cast<uint64_t>(slots) * chunk);
-    while (c->ring_events.size() < static_cast<size_t>(slots)) {
-        cudaEvent_t e;
-        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        c->ring_events.push_back(e);
-    }
-    uint8_t* ring = static_cast<uint8_t*>(c->h_ring.p);
     c->csv.ensure(total + 16);
     c->input_bytes = total;
     uint8_t* d_csv = c->csv.as<uint8_t>();
@@ -1067,81 +958,8 @@ void run_files(cvlg_context* c, const char* const* paths, size_t n, const cvlg_g
         c->raw.ensure(raw_words * 4);
         d_raw = c->raw.as<uint32_t>();
     }
-    // the copies must not start before the previous run finished with the device buffer, and
-    // no slot may be refilled before its last copy (from a previous run) completed
-    cudaEvent_t start_ev = c->ring_events[0];
-    CK(cudaEventRecord(start_ev, c->stream));
-    CK(cudaStreamWaitEvent(c->copy_stream, start_ev, 0));
-    for (int k = 0; k < slots; ++k) CK(cudaEventRecord(c->ring_events[k], c->copy_stream));
-
-    struct Shared {
-        std::mutex mu;
-        std::condition_variable cv;
-        std::vector<uint8_t> ready;
-        size_t enqueued = 0;  // chunks [0, enqueued) have their copy enqueued
-        bool stop = false;
-        std::string err;
-    } sh;
-    sh.ready.assign(n_chunks, 0);
-    std::atomic<size_t> next{0};
-    const int dev = c->device;
-    unsigned workers = n_threads ? n_threads : std::max(1u, std::thread::hardware_concurrency());
-    workers = static_cast<unsigned>(std::min<size_t>({workers, static_cast<size_t>(slots), std::max<size_t>(n_chunks, 1)}));
-    auto reader = [&]() {
-        cudaSetDevice(dev);
-        int fd = -1;
-        uint32_t fd_r = 0xFFFFFFFFu;
-        for (size_t k = next.fetch_add(1); k < n_chunks; k = next.fetch_add(1)) {
-            const Chunk& ch = chunks[k];
-            const int slot = static_cast<int>(k % slots);
-            {
-                std::unique_lock<std::mutex> lk(sh.mu);
-                sh.cv.wait(lk, [&] { return sh.stop || k < static_cast<size_t>(slots) || sh.enqueued > k - slots; });
-                if (sh.stop) break;
-            }
-            if (cudaEventSynchronize(c->ring_events[slot]) != cudaSuccess) {
-                std::lock_guard<std::mutex> lk(sh.mu);
-                sh.err = "cudaEventSynchronize failed on the ingest ring";
-                sh.stop = true;
-                sh.cv.notify_all();
-                break;
-            }
-            if (ch.r != fd_r) {
-                if (fd >= 0) ::close(fd);
-                fd = ::open(paths[ch.r], O_RDONLY);
-                fd_r = ch.r;
-            }
-            uint8_t* dst = ring + static_cast<uint64_t>(slot) * chunk;
-            uint64_t got = 0;
-            while (fd >= 0 && got < ch.len) {
-                const ssize_t rd = ::pread(fd, dst + got, ch.len - got, static_cast<off_t>(ch.a + got));
-                if (rd <= 0) break;
-                got += static_cast<uint64_t>(rd);
-            }
-            std::lock_guard<std::mutex> lk(sh.mu);
-            if (got != ch.len) {
-                sh.err = std::string("Io: read failure on ") + paths[ch.r];
-                sh.stop = true;
-            } else {
-                sh.ready[k] = 1;
-            }
-            sh.cv.notify_all();
-            if (sh.stop) break;
-        }
-        if (fd >= 0) ::close(fd);
-    };
-    std::vector<std::thread> pool;
-    for (unsigned w = 0; w < workers; ++w) pool.emplace_back(reader);
-    auto join_all = [&]() {
-        {
-            std::lock_guard<std::mutex> lk(sh.mu);
-            sh.stop = true;
-            sh.cv.notify_all();
-        }
-        for (auto& t : pool)
-            if (t.joinable()) t.join();
-    };
-
+    RingIngest ring(c, paths, std::move(ranges), d_csv, n_threads);
+    const size_t n_chunks = ring.chunks();
     uint64_t safe = 0;
     size_t k_next = 0;
     MarkSource src = [&](ChunkMark& m) -> bool {
@@ -1153,47 +971,287 @@ void run_files(cvlg_context* c, const char* const* paths, size_t n, const cvlg_g
             }
             return false;
         }
-        const size_t k = k_next++;
-        {
-            std::unique_lock<std::mutex> lk(sh.mu);
-            sh.cv.wait(lk, [&] { return sh.ready[k] || !sh.err.empty(); });
-            if (!sh.err.empty()) fail(sh.err.rfind("Io:", 0) == 0 ? CVLG_E_IO : CVLG_E_CUDA, sh.err);
-        }
-        const Chunk& ch = chunks[k];
-        const int slot = static_cast<int>(k % slots);
-        const uint8_t* src_p = ring + static_cast<uint64_t>(slot) * chunk;
-        const uint64_t g0 = off[ch.r] + ch.a, g1 = g0 + ch.len;
-        CK(cudaMemcpyAsync(d_csv + g0, src_p, ch.len, cudaMemcpyHostToDevice, c->copy_stream));
-        CK(cudaEventRecord(c->ring_events[slot], c->copy_stream));
-        if (ch.a + ch.len == off[ch.r + 1] - off[ch.r]) {
+        RingChunk ch;
+        if (!ring.next(ch)) fail(CVLG_E_INTERNAL, "ingest ring ended early");
+        ++k_next;
+        const uint64_t g0 = ch.dst, g1 = g0 + ch.len;
+        const uint32_t r = static_cast<uint32_t>(std::upper_bound(off.begin(), off.end(), g0) - off.begin() - 1);
+        if (g1 == off[r + 1]) {
             safe = g1;  // lines never cross a shard end
-        } else {
-            const void* nl = memrchr(src_p, '\n', ch.len);
-            if (nl) safe = g0 + static_cast<uint64_t>(static_cast<const uint8_t*>(nl) - src_p) + 1;
+        } else if (ch.nl_end) {
+            safe = g0 + ch.nl_end;
         }
-        {
-            std::lock_guard<std::mutex> lk(sh.mu);
-            sh.enqueued = k + 1;
-            sh.cv.notify_all();
-        }
-        m = ChunkMark{g1, safe, c->ring_events[slot]};
+        m = ChunkMark{g1, safe, ch.copied};
         // the final mark must cover the whole input even when trailing shards are empty
-        if (k + 1 == n_chunks) m.avail_end = total;
+        if (k_next == n_chunks) m.avail_end = total;
         return true;
     };
-    try {
-        run_core(c, d_csv, off, cmap.data(), good.data(), bad, spec, rules, d_planes, d_raw, stats,
-                 src, false, nullptr);
-    } catch (...) {
-        join_all();
-        cudaStreamSynchronize(c->copy_stream);
-        throw;
-    }
-    join_all();
+    run_core(c, d_csv, off, cmap.data(), good.data(), bad, spec, rules, d_planes, d_raw, stats, src,
+             false, nullptr);
+    ring.stop();
     if (planes)
         CK(cudaMemcpyAsync(planes, d_planes, lattice_words * 4, cudaMemcpyDeviceToHost, c->stream));
     if (raw) CK(cudaMemcpyAsync(raw, d_raw, raw_words * 4, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
+}
+
+}  // namespace
+
+std::vector<ShardHead> read_shard_heads(const char* const* paths, size_t n) {
+    std::vector<ShardHead> heads(n);
+    for (size_t r = 0; r < n; ++r) {
+        ShardHead& h = heads[r];
+        const int fd = ::open(paths[r], O_RDONLY);
+        struct stat st;
+        if (fd < 0 || ::fstat(fd, &st) != 0 || !S_ISREG(st.st_mode)) {
+            if (fd >= 0) ::close(fd);
+            fail(CVLG_E_IO, std::string("Io: cannot open shard ") + paths[r]);
+        }
+        h.len = static_cast<uint64_t>(st.st_size);
+        std::memset(&h.cmap, 0xFF, sizeof(h.cmap));
+        h.cmap.n_columns = 0;
+        h.data_begin = h.len;
+        if (h.len) {
+            std::string head;
+            char buf[4096];
+            uint64_t at = 0;
+            size_t nl = std::string::npos;
+            while (at < h.len) {
+                const ssize_t k = ::pread(fd, buf, sizeof(buf), static_cast<off_t>(at));
+                if (k <= 0) break;
+                head.append(buf, static_cast<size_t>(k));
+                at += static_cast<uint64_t>(k);
+                if ((nl = head.find('\n', at - static_cast<uint64_t>(k))) != std::string::npos) break;
+            }
+            size_t hl = nl == std::string::npos ? head.size() : nl;
+            if (nl != std::string::npos) {
+                h.data_begin = nl + 1;
+                h.header = head.substr(0, nl + 1);
+            } else {
+                h.header = head + "\n";
+            }
+            if (hl > 0 && head[hl - 1] == '\r') --hl;
+            h.good = parse_header(reinterpret_cast<const uint8_t*>(head.data()), static_cast<int64_t>(hl), h.cmap);
+            h.bad_header = !h.good;
+        }
+        ::close(fd);
+    }
+    return heads;
+}
+
+// ---- RingIngest -------------------------------------------------------------------------------
+struct RingIngest::Impl {
+    cvlg_context* c;
+    const char* const* paths;
+    std::vector<FileRange> ranges;
+    uint8_t* d_dst;
+    uint64_t chunk = 32ull << 20;
+    int slots = 16;
+    struct Chunk {
+        size_t range;
+        uint64_t off, len, dst;
+    };
+    std::vector<Chunk> chunks;
+    uint8_t* ring = nullptr;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<uint8_t> ready;
+    size_t enqueued = 0;  // chunks [0, enqueued) have their copy enqueued
+    bool stopping = false;
+    std::string err;
+    std::atomic<size_t> next_read{0};
+    std::vector<std::thread> pool;
+    size_t k_next = 0;
+
+    void reader() {
+        cudaSetDevice(c->device);
+        int fd = -1;
+        uint32_t fd_file = 0xFFFFFFFFu;
+        for (size_t k = next_read.fetch_add(1); k < chunks.size(); k = next_read.fetch_add(1)) {
+            const Chunk& ch = chunks[k];
+            const int slot = static_cast<int>(k % slots);
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return stopping || k < static_cast<size_t>(slots) || enqueued > k - slots; });
+                if (stopping) break;
+            }
+            if (cudaEventSynchronize(c->ring_events[slot]) != cudaSuccess) {
+                std::lock_guard<std::mutex> lk(mu);
+                err = "cudaEventSynchronize failed on the ingest ring";
+                stopping = true;
+                cv.notify_all();
+                break;
+            }
+            const uint32_t file = ranges[ch.range].file;
+            if (file != fd_file) {
+                if (fd >= 0) ::close(fd);
+                fd = ::open(paths[file], O_RDONLY);
+                fd_file = file;
+            }
+            uint8_t* dst = ring + static_cast<uint64_t>(slot) * chunk;
+            uint64_t got = 0;
+            while (fd >= 0 && got < ch.len) {
+                const ssize_t rd = ::pread(fd, dst + got, ch.len - got, static_cast<off_t>(ch.off + got));
+                if (rd <= 0) break;
+                got += static_cast<uint64_t>(rd);
+            }
+            std::lock_guard<std::mutex> lk(mu);
+            if (got != ch.len) {
+                err = std::string("Io: read failure on ") + paths[file];
+                stopping = true;
+            } else {
+                ready[k] = 1;
+            }
+            cv.notify_all();
+            if (stopping) break;
+        }
+        if (fd >= 0) ::close(fd);
+    }
+};
+
+RingIngest::RingIngest(cvlg_context* c, const char* const* paths, std::vector<FileRange> ranges,
+                       uint8_t* d_dst, unsigned n_threads)
+    : impl_(new Impl) {
+    Impl& I = *impl_;
+    I.c = c;
+    I.paths = paths;
+    I.ranges = std::move(ranges);
+    I.d_dst = d_dst;
+    // ring geometry (CVLG_RING_MB / CVLG_RING_SLOTS override: tuning only)
+    if (const char* e = std::getenv("CVLG_RING_MB")) I.chunk = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
+    if (const char* e = std::getenv("CVLG_RING_SLOTS")) I.slots = std::max(2, std::atoi(e));
+    for (size_t i = 0; i < I.ranges.size(); ++i) {
+        const FileRange& r = I.ranges[i];
+        for (uint64_t a = 0; a < r.len; a += I.chunk)
+            I.chunks.push_back(Impl::Chunk{i, r.off + a, std::min(I.chunk, r.len - a), r.dst + a});
+    }
+    const size_t n_chunks = I.chunks.size();
+    I.slots = static_cast<int>(std::min<size_t>(I.slots, std::max<size_t>(n_chunks, 2)));
+    c->h_ring.ensure(static_cast<uint64_t>(I.slots) * I.chunk);
+    while (c->ring_events.size() < static_cast<size_t>(I.slots)) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ring_events.push_back(e);
+    }
+    I.ring = static_cast<uint8_t*>(c->h_ring.p);
+    // the copies must not start before the previous run finished with the device buffer, and
+    // no slot may be refilled before its last copy (from a previous run) completed
+    cudaEvent_t start_ev = c->ring_events[0];
+    CK(cudaEventRecord(start_ev, c->stream));
+    CK(cudaStreamWaitEvent(c->copy_stream, start_ev, 0));
+    for (int k = 0; k < I.slots; ++k) CK(cudaEventRecord(c->ring_events[k], c->copy_stream));
+    I.ready.assign(n_chunks, 0);
+    unsigned workers = n_threads ? n_threads : std::max(1u, std::thread::hardware_concurrency());
+    workers = static_cast<unsigned>(std::min<size_t>({workers, static_cast<size_t>(I.slots), std::max<size_t>(n_chunks, 1)}));
+    for (unsigned w = 0; w < workers && n_chunks; ++w) I.pool.emplace_back([&I] { I.reader(); });
+}
+
+size_t RingIngest::chunks() const { return impl_->chunks.size(); }
+
+bool RingIngest::next(RingChunk& out) {
+    Impl& I = *impl_;
+    if (I.k_next >= I.chunks.size()) return false;
+    const size_t k = I.k_next++;
+    {
+        std::unique_lock<std::mutex> lk(I.mu);
+        I.cv.wait(lk, [&] { return I.ready[k] || !I.err.empty(); });
+        if (!I.err.empty()) fail(I.err.rfind("Io:", 0) == 0 ? CVLG_E_IO : CVLG_E_CUDA, I.err);
+    }
+    const Impl::Chunk& ch = I.chunks[k];
+    const int slot = static_cast<int>(k % I.slots);
+    const uint8_t* src = I.ring + static_cast<uint64_t>(slot) * I.chunk;
+    CK(cudaMemcpyAsync(I.d_dst + ch.dst, src, ch.len, cudaMemcpyHostToDevice, I.c->copy_stream));
+    CK(cudaEventRecord(I.c->ring_events[slot], I.c->copy_stream));
+    // (before the slot is released for refilling)
+    const void* nl = memrchr(src, '\n', ch.len);
+    const uint64_t nl_end = nl ? static_cast<uint64_t>(static_cast<const uint8_t*>(nl) - src) + 1 : 0;
+    {
+        std::lock_guard<std::mutex> lk(I.mu);
+        I.enqueued = k + 1;
+        I.cv.notify_all();
+    }
+    out = RingChunk{ch.range, ch.off, ch.len, ch.dst, nl_end, I.c->ring_events[slot]};
+    return true;
+}
+
+void RingIngest::stop() {
+    Impl& I = *impl_;
+    {
+        std::lock_guard<std::mutex> lk(I.mu);
+        I.stopping = true;
+        I.cv.notify_all();
+    }
+    for (auto& t : I.pool)
+        if (t.joinable()) t.join();
+    I.pool.clear();
+}
+
+RingIngest::~RingIngest() {
+    stop();
+    cudaStreamSynchronize(impl_->c->copy_stream);
+    delete impl_;
+}
+
+void export_tuples(cvlg_context* c, uint64_t* d_cell, uint64_t* d_key0, uint64_t* d_key1,
+                   double* d_sum, uint64_t* d_count, uint64_t stride, cudaStream_t s) {
+    if (c->part_long_ids)
+        fail(CVLG_E_UNSUPPORTED, "multi-GPU combine needs journey ids <= 15 bytes (exact inline keys)");
+    const uint64_t n = c->part_pairs;
+    if (!n) return;
+    c->h_small.ensure(4096);
+    uint32_t* d_bad = c->scal.as<uint32_t>() + 15;
+    CK(cudaMemsetAsync(d_bad, 0, 4, s));
+    launch_export_pairs(c->pair_key.as<uint64_t>(), c->pair_sum.as<double>(), c->pair_cnt.as<uint32_t>(),
+                        n, c->part_rbits, c->rank_slot.as<uint32_t>(), c->dict.as<unsigned long long>(),
+                        d_cell, d_key0, d_key1, d_sum, d_count, stride, d_bad, s);
+    uint32_t* hb = static_cast<uint32_t*>(c->h_small.p) + 200;
+    CK(cudaMemcpyAsync(hb, d_bad, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    if (*hb) fail(CVLG_E_UNSUPPORTED, "multi-GPU combine needs journey ids <= 15 bytes (exact inline keys)");
+}
+
+void finalize_tuples(cvlg_context* c, const uint64_t* d_cell, const uint64_t* d_key0,
+                     const uint64_t* d_key1, const double* d_sum, const uint64_t* d_count,
+                     uint64_t stride, uint64_t n, const Dims& dims, uint32_t* d_planes,
+                     uint32_t* d_raw, cudaStream_t s) {
+    const uint64_t lattice_words = static_cast<uint64_t>(dims.T) * 8 * dims.RC;
+    const uint64_t raw_words = static_cast<uint64_t>(dims.T) * 4 * dims.RC;
+    CK(cudaMemsetAsync(d_planes, 0, lattice_words * 4, s));
+    if (d_raw) CK(cudaMemsetAsync(d_raw, 0, raw_words * 4, s));
+    if (n) {
+        if (n >= (1ull << 32)) fail(CVLG_E_UNSUPPORTED, ">= 2^32 (cell, journey) tuples on one device");
+        c->h_small.ensure(4096);
+        c->scal.ensure(128);
+        unsigned long long* d_orand = c->scal.as<unsigned long long>() + 4;
+        unsigned long long* h_orand = reinterpret_cast<unsigned long long*>(h_small64(c) + 40);
+        c->x_keys.ensure(n * 8);
+        c->keys_alt.ensure(n * 8);
+        c->vals.ensure(n * 4);
+        c->vals_alt.ensure(n * 4);
+        c->sort_tmp.ensure(radix_temp_bytes(n));
+        c->x_sum.ensure(n * 8);
+        c->x_cnt.ensure(n * 4);
+        uint64_t* keys = c->x_keys.as<uint64_t>();
+        uint32_t* vals = c->vals.as<uint32_t>();
+        // stable LSD over (cell, key0, key1): least significant word first; (cell, key) is unique,
+        // so the order is the reference's (g, journey) finalize order (aggregate.cpp:161-204)
+        launch_gather_u64(d_key1, stride, nullptr, n, keys, s);
+        launch_pair_vals(vals, n, s);
+        radix_sort_pairs(keys, vals, c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), n, 0, 64,
+                         c->sort_tmp.p, s, d_orand, h_orand);
+        launch_gather_u64(d_key0, stride, vals, n, keys, s);
+        radix_sort_pairs(keys, vals, c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), n, 0, 64,
+                         c->sort_tmp.p, s, d_orand, h_orand);
+        launch_gather_u64(d_cell, stride, vals, n, keys, s);
+        radix_sort_pairs(keys, vals, c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), n, 0,
+                         bits_for(dims.cells - 1), c->sort_tmp.p, s, d_orand, h_orand);
+        launch_import_pairs(d_sum, d_count, stride, n, c->x_sum.as<double>(), c->x_cnt.as<uint32_t>(), s);
+        launch_finalize(keys, vals, n, 0, c->x_sum.as<double>(), c->x_cnt.as<uint32_t>(), dims.D, dims.RC,
+                        d_planes, d_raw, s);
+    }
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
 }
 
 int guard(const std::function<void()>& fn) {
@@ -1212,7 +1270,9 @@ int guard(const std::function<void()>& fn) {
     }
 }
 
-}  // namespace
+}  // namespace cvlg
+
+using namespace cvlg;
 
 // ==================================== C ABI =====================================================
 extern "C" {
@@ -1287,7 +1347,11 @@ void cvlg_context_destroy(cvlg_context* c) {
                       &c->scal,   &c->keys,      &c->vals,     &c->keys_alt, &c->vals_alt,
                       &c->sort_tmp, &c->scan_tmp, &c->srank,   &c->jstart,   &c->pair_key,
                       &c->pair_sum, &c->pair_cnt, &c->planes,  &c->raw, &c->rank_slot,
-                      &c->x_keys, &c->x_sum, &c->x_cnt};
+                      &c->x_keys, &c->x_sum, &c->x_cnt, &c->fold_dir, &c->dead,
+                      &c->slice, &c->r_tbytes, &c->r_tbase, &c->r_pobase, &c->r_total, &c->r_lines,
+                      &c->r_idcol, &c->r_poff, &c->r_tfirst, &c->r_hdr, &c->r_hoff, &c->r_dst,
+                      &c->r_err, &c->r_send, &c->tuples, &c->tuples_in, &c->tuples_send,
+                      &c->t_counts, &c->t_dst};
     for (DevBuf* b : bufs) b->release();
     c->h_small.release();
     c->h_ring.release();
@@ -1471,21 +1535,10 @@ int cvlg_export_pairs(cvlg_context* ctx, uint64_t* d_cell, uint64_t* d_key0, uin
         cvlg_context* c = ctx ? ctx : default_context();
         if (!c) fail(CVLG_E_CUDA, "no CUDA context");
         CK(cudaSetDevice(c->device));
-        if (c->part_long_ids)
-            fail(CVLG_E_UNSUPPORTED,
-                 "multi-GPU combine needs journey ids <= 15 bytes (exact inline keys)");
-        const uint64_t n = c->part_pairs;
-        if (!n) return;
-        if (!d_cell || !d_key0 || !d_key1 || !d_sum || !d_count) fail(CVLG_E_INVALID_ARG, "NULL argument");
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
-        uint32_t* d_bad = c->scal.as<uint32_t>() + 15;
-        CK(cudaMemsetAsync(d_bad, 0, 4, s));
-        launch_export_pairs(c->pair_key.as<uint64_t>(), c->pair_sum.as<double>(),
-                            c->pair_cnt.as<uint32_t>(), n, c->part_rbits, c->rank_slot.as<uint32_t>(),
-                            c->dict.as<unsigned long long>(), d_cell, d_key0, d_key1, d_sum, d_count,
-                            d_bad, s);
-        CK(cudaStreamSynchronize(s));
-        CK(cudaGetLastError());
+        if (c->part_pairs && (!d_cell || !d_key0 || !d_key1 || !d_sum || !d_count))
+            fail(CVLG_E_INVALID_ARG, "NULL argument");
+        export_tuples(c, d_cell, d_key0, d_key1, d_sum, d_count, 1,
+                      stream ? static_cast<cudaStream_t>(stream) : c->stream);
     });
 }
 
@@ -1499,42 +1552,8 @@ int cvlg_finalize_pairs(cvlg_context* ctx, const uint64_t* d_cell, const uint64_
         if (!c) fail(CVLG_E_CUDA, "no CUDA context");
         if (!d_planes) fail(CVLG_E_INVALID_ARG, "NULL planes");
         CK(cudaSetDevice(c->device));
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
-        const uint64_t lattice_words = static_cast<uint64_t>(dims.T) * 8 * dims.RC;
-        const uint64_t raw_words = static_cast<uint64_t>(dims.T) * 4 * dims.RC;
-        CK(cudaMemsetAsync(d_planes, 0, lattice_words * 4, s));
-        if (d_raw_count) CK(cudaMemsetAsync(d_raw_count, 0, raw_words * 4, s));
-        if (n) {
-            c->h_small.ensure(4096);
-            c->scal.ensure(64);
-            unsigned long long* d_orand = c->scal.as<unsigned long long>() + 4;
-            unsigned long long* h_orand = reinterpret_cast<unsigned long long*>(h_small64(c) + 40);
-            c->x_keys.ensure(n * 8);
-            c->keys_alt.ensure(n * 8);
-            c->vals.ensure(n * 4);
-            c->vals_alt.ensure(n * 4);
-            c->sort_tmp.ensure(radix_temp_bytes(n));
-            c->x_sum.ensure(n * 8);
-            c->x_cnt.ensure(n * 4);
-            uint64_t* keys = c->x_keys.as<uint64_t>();
-            uint32_t* vals = c->vals.as<uint32_t>();
-            // stable LSD over (cell, key0, key1): least significant word first
-            CK(cudaMemcpyAsync(keys, d_key1, n * 8, cudaMemcpyDeviceToDevice, s));
-            launch_pair_vals(vals, n, s);
-            radix_sort_pairs(keys, vals, c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), n,
-                             0, 64, c->sort_tmp.p, s, d_orand, h_orand);
-            launch_gather_u64(d_key0, vals, n, keys, s);
-            radix_sort_pairs(keys, vals, c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), n,
-                             0, 64, c->sort_tmp.p, s, d_orand, h_orand);
-            launch_gather_u64(d_cell, vals, n, keys, s);
-            radix_sort_pairs(keys, vals, c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), n,
-                             0, bits_for(dims.cells - 1), c->sort_tmp.p, s, d_orand, h_orand);
-            launch_import_pairs(d_sum, d_count, n, c->x_sum.as<double>(), c->x_cnt.as<uint32_t>(), s);
-            launch_finalize(keys, vals, n, 0, c->x_sum.as<double>(), c->x_cnt.as<uint32_t>(), dims.D,
-                            dims.RC, d_planes, d_raw_count, s);
-        }
-        CK(cudaStreamSynchronize(s));
-        CK(cudaGetLastError());
+        finalize_tuples(c, d_cell, d_key0, d_key1, d_sum, d_count, 1, n, dims, d_planes, d_raw_count,
+                        stream ? static_cast<cudaStream_t>(stream) : c->stream);
     });
 }
 

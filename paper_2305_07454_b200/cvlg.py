@@ -116,6 +116,34 @@ def _load() -> ctypes.CDLL:
                                                  ctypes.c_double, vp, vp, ctypes.POINTER(_Stats),
                                                  u64p, vp]
     lib.cvlg_features_copy.argtypes = [vp, ctypes.POINTER(_Features)]
+    # multi-GPU (include/cvlg.h, multi.cu)
+    lib.cvlg_multi_create.restype = vp
+    lib.cvlg_multi_create.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.c_uint32]
+    lib.cvlg_multi_destroy.argtypes = [vp]
+    lib.cvlg_multi_size.restype = ctypes.c_uint32
+    lib.cvlg_multi_size.argtypes = [vp]
+    lib.cvlg_multi_context.restype = vp
+    lib.cvlg_multi_context.argtypes = [vp, ctypes.c_uint32]
+    lib.cvlg_run_pipeline_multi.argtypes = [vp, ctypes.POINTER(ctypes.c_char_p), ctypes.c_size_t,
+                                            ctypes.POINTER(_Grid), ctypes.POINTER(_Rules),
+                                            ctypes.c_uint32, ctypes.c_uint32, vp, vp,
+                                            ctypes.POINTER(_Stats)]
+    lib.cvlg_route_stage.argtypes = [vp, ctypes.POINTER(ctypes.c_char_p), ctypes.c_size_t,
+                                     ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, u64p, u64p]
+    lib.cvlg_route_count.argtypes = [vp]
+    lib.cvlg_route_plan.argtypes = [vp, ctypes.c_uint32, u64p, u64p]
+    lib.cvlg_route_scatter.argtypes = [vp, ctypes.POINTER(vp), vp]
+    lib.cvlg_tuples_export.argtypes = [vp, ctypes.POINTER(_Grid), ctypes.c_uint32, u64p, u64p]
+    lib.cvlg_tuples_scatter.argtypes = [vp, ctypes.POINTER(_Grid), ctypes.c_uint32,
+                                        ctypes.POINTER(vp), vp]
+    lib.cvlg_finalize_tuples.argtypes = [vp, vp, ctypes.c_uint64, ctypes.POINTER(_Grid), vp, vp,
+                                         vp]
+    lib.cvlg_slab_rows.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, u32p, u32p]
+    lib.cvlg_split_manifest.argtypes = [ctypes.POINTER(ctypes.c_char_p), ctypes.c_size_t,
+                                        ctypes.c_uint32, ctypes.c_uint32, u32p, u64p, u64p,
+                                        ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
+    lib.cvlg_partial_device.argtypes = [vp, vp, u64p, ctypes.c_size_t, ctypes.POINTER(_Grid),
+                                        ctypes.POINTER(_Rules), u64p, ctypes.POINTER(_Stats), vp]
     return lib
 
 
@@ -127,6 +155,10 @@ EXPORTED_SYMBOLS = [
     "cvlg_run_pipeline_device", "cvlg_write_container", "cvlg_last_stage_ms", "cvlg_pin_host",
     "cvlg_unpin_host", "cvlg_launch_count", "cvlg_last_error", "cvlg_journey_features_host",
     "cvlg_journey_features_device", "cvlg_features_copy", "cvlg_context_input",
+    "cvlg_multi_create", "cvlg_multi_destroy", "cvlg_multi_size", "cvlg_multi_context",
+    "cvlg_run_pipeline_multi", "cvlg_route_stage", "cvlg_route_count", "cvlg_route_plan",
+    "cvlg_route_scatter", "cvlg_tuples_export", "cvlg_tuples_scatter", "cvlg_finalize_tuples",
+    "cvlg_slab_rows", "cvlg_split_manifest", "cvlg_partial_device",
 ]
 
 
@@ -354,6 +386,80 @@ def run_pipeline(manifest, spec: GridSpec | None = None, rules: FilterRules | No
     if stats is not None:
         stats._fill(st)
     return Lattice(planes, rawa)
+
+
+class MultiGPU:
+    """Several GPUs driven from one host thread (cvlg_multi_*): journeys sharded by
+    journey_hash(id) % n like the reference's partitions (aggregate.cpp:414-443). `devices` may
+    repeat a device (several shards on one GPU)."""
+
+    def __init__(self, devices: Sequence[int]):
+        arr = (ctypes.c_int * len(devices))(*devices)
+        self._h = _lib.cvlg_multi_create(arr, len(devices))
+        if not self._h:
+            buf = ctypes.create_string_buffer(1024)
+            _lib.cvlg_last_error(buf, 1024)
+            raise CvlError(100, buf.value.decode() or "cvlg_multi_create failed")
+        self.devices = list(devices)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __len__(self) -> int:
+        return len(self.devices)
+
+    def close(self) -> None:
+        if self._h:
+            _lib.cvlg_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def run_pipeline(self, manifest, spec: GridSpec | None = None, rules: FilterRules | None = None,
+                     n_partitions: int = 1, n_threads: int = 0, stats: PipelineStats | None = None,
+                     raw: bool = True, out: tuple | None = None) -> Lattice:
+        """cvl::run_pipeline over the group's GPUs (cvlg_run_pipeline_multi): same result as
+        run_pipeline on one GPU, byte for byte."""
+        spec = spec or GridSpec()
+        rules = rules or FilterRules()
+        paths = _paths(manifest)
+        arr = (ctypes.c_char_p * max(len(paths), 1))(*[p.encode() for p in paths])
+        planes, rawa = out if out is not None else _alloc(spec, raw)
+        st = _Stats()
+        _check(_lib.cvlg_run_pipeline_multi(self._h, arr, len(paths), ctypes.byref(spec._c()),
+                                            ctypes.byref(rules._c()), n_partitions, n_threads,
+                                            _ptr(planes), _ptr(rawa), ctypes.byref(st)))
+        if stats is not None:
+            stats._fill(st)
+        return Lattice(planes, rawa)
+
+
+def split_manifest(manifest, n_parts: int, part: int) -> list[tuple[int, int, int]]:
+    """Host only: the (file rank, byte offset, length) pieces of part `part` of `n_parts` as the
+    multi-GPU ingest cuts the shards' data lines (cvlg_split_manifest)."""
+    paths = _paths(manifest)
+    arr = (ctypes.c_char_p * max(len(paths), 1))(*[p.encode() for p in paths])
+    n = ctypes.c_size_t()
+    _check(_lib.cvlg_split_manifest(arr, len(paths), n_parts, part, None, None, None, 0,
+                                    ctypes.byref(n)))
+    k = n.value
+    f = (ctypes.c_uint32 * max(k, 1))()
+    o = (ctypes.c_uint64 * max(k, 1))()
+    ln = (ctypes.c_uint64 * max(k, 1))()
+    _check(_lib.cvlg_split_manifest(arr, len(paths), n_parts, part, f, o, ln, k, ctypes.byref(n)))
+    return [(int(f[i]), int(o[i]), int(ln[i])) for i in range(k)]
+
+
+def slab_rows(n_batches: int, n_owners: int, owner: int) -> tuple[int, int]:
+    """Rows [t0, t1) of the lattice folded by slab owner `owner` (cvlg_slab_rows)."""
+    t0, t1 = ctypes.c_uint32(), ctypes.c_uint32()
+    _check(_lib.cvlg_slab_rows(n_batches, n_owners, owner, ctypes.byref(t0), ctypes.byref(t1)))
+    return t0.value, t1.value
 
 
 def run_pipeline_host(buffers: Iterable, spec: GridSpec | None = None,

@@ -79,3 +79,28 @@ def commuter_days(n_journeys, days, cells, seed):
                     j, 9 + d, sec // 60, sec % 60, la, lo, rng.uniform(0, 80), rng.uniform(0, hmax)))
         out.append(HEADER + b"\n" + b"\n".join(lines) + b"\n")
     return out
+
+
+def malformed_contents(seed: int = 5) -> list[bytes]:
+    """Shards exercising read_shard / parse_record_impl edge cases (ingest.cpp:119-157, 195-239):
+    CRLF, blank lines, no trailing newline, an empty shard, a BadHeader shard, a permuted header,
+    a header-only shard, plus the malformed-line corpus mixed with good lines."""
+    import corpus
+    rng = random.Random(seed)
+    body = corpus.line_corpus(rng, 3000)
+    good = [b"jj%03d,2021-05-09 %02d:%02d:%02d,%.6f,%.6f,65101,%.2f,%.2f" % (
+        i % 17, (i // 3600) % 24, (i // 60) % 60, i % 60, 36.1 + (i % 400) * 0.01,
+        -95.7 + (i % 600) * 0.011, (i * 7.3) % 140, (i * 13.7) % 360) for i in range(4000)]
+    mixed = body + good
+    rng.shuffle(mixed)
+    return [
+        HEADER + b"\r\n" + b"\r\n".join(mixed[:1500]) + b"\r\n",
+        HEADER + b"\n" + b"\n\n".join(mixed[1500:4000]),  # blank lines, no trailing newline
+        b"",  # empty shard: no header, no rows
+        b"nope,nope\n1,2\n",  # BadHeader
+        b"heading,speed,zip code,longitude,latitude,timestamp,journey-id\n" + b"\n".join(
+            b"%s,%s,%s,%s,%s,%s,%s" % tuple(reversed(l.split(b",")[:7])) for l in good[:800]
+            if len(l.split(b",")) == 7),
+        HEADER,  # header only, no newline
+        HEADER + b"\n" + b"\n".join(mixed[4000:]) + b"\n",
+    ]

@@ -1,7 +1,7 @@
 """Multi-GPU combine logic.
 
-CPU (gloo, world_size 2): the slab partition + all-to-all exchange + per-rank fold + all-reduce
-of paper_2305_07454_b200.distributed reproduces a single-process fold of the union of tuples
+CPU (gloo, world_size 2): the slab partition + all-to-all exchange (distributed.all_to_all_bytes)
++ per-rank fold + slab gather reproduces a single-process fold of the union of tuples
 (the fold here is a numpy restatement of the reference finalize, aggregate.cpp:161-204 — test
 code only). GPU (1 device): the C-ABI building blocks (partial -> export -> finalize) over two
 journey-hash shards give the lattice of the single-shard pipeline bit for bit.
@@ -66,22 +66,31 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2305_07454_b200.distributed import exchange_tuples, slab_owner
+    from paper_2305_07454_b200.distributed import all_gather_obj, all_to_all_bytes, slab_rows
     T, D, R, C = 24, 4, 3, 5
-    mine = torch.from_numpy(make_tuples(rank, T, D, R, C))
-    owner = slab_owner(mine[:, 0], D * R * C, T, world)
-    recv = exchange_tuples(mine, owner, world)
-    # every received tuple belongs to this rank's slab
-    assert bool((slab_owner(recv[:, 0], D * R * C, T, world) == rank).all())
-    planes, raw = np_finalize(recv.numpy(), T, D, R, C)
-    p = torch.from_numpy(planes.view(np.int32).copy())
-    r = torch.from_numpy(raw.view(np.int32).copy())
-    dist.all_reduce(p, op=dist.ReduceOp.SUM)
-    dist.all_reduce(r, op=dist.ReduceOp.SUM)
+    mine = make_tuples(rank, T, D, R, C)
+    # partition by time-slab owner (owner(t) = t * world // T, route.cu tuple_owner)
+    owner = (mine[:, 0] // (D * R * C)) * world // T
+    order = np.argsort(owner, kind="stable")
+    send = np.ascontiguousarray(mine[order])
+    counts = np.bincount(owner, minlength=world).tolist()
+    all_counts = all_gather_obj(counts)
+    recv = all_to_all_bytes(torch.from_numpy(send.view(np.uint8).reshape(-1).copy()),
+                            [c * 40 for c in counts], [c[rank] * 40 for c in all_counts])
+    got = recv.numpy().view(np.int64).reshape(-1, 5)
+    t0, t1 = slab_rows(T, world, rank)
+    ts = got[:, 0] // (D * R * C)
+    assert bool(((ts >= t0) & (ts < t1)).all())
+    planes, raw = np_finalize(got, T, D, R, C)
+    slabs = all_gather_obj((t0, t1, planes[t0:t1], raw[t0:t1]))
+    p = np.zeros_like(planes)
+    r = np.zeros_like(raw)
+    for a, b, sp, sr in slabs:
+        p[a:b] = sp
+        r[a:b] = sr
     allc = np.concatenate([make_tuples(k, T, D, R, C) for k in range(world)])
     ep, er = np_finalize(allc, T, D, R, C)
-    q.put((rank, bool(np.array_equal(p.numpy().view(np.uint32), ep)),
-           bool(np.array_equal(r.numpy().view(np.uint32), er)), int(recv.shape[0])))
+    q.put((rank, bool(np.array_equal(p, ep)), bool(np.array_equal(r, er)), int(got.shape[0])))
     dist.destroy_process_group()
 
 
@@ -109,21 +118,11 @@ def test_gloo_exchange_matches_single_process():
     assert sum(n for *_, n in res) > 0
 
 
-def test_slab_owner_partition():
-    from paper_2305_07454_b200.distributed import slab_owner
-    T, per_t = 288, 100
-    cell = torch.arange(T * per_t)
-    for world in (1, 2, 3, 8):
-        o = slab_owner(cell, per_t, T, world)
-        assert int(o.min()) == 0 and int(o.max()) == world - 1
-        # contiguous, non-decreasing slabs
-        assert bool((o[1:] >= o[:-1]).all())
-
-
 @pytest.mark.gpu
+@pytest.mark.parametrize("shards", [2, 4, 8])
 @pytest.mark.parametrize("case", ["coarse", "fine_multiday"])
-def test_partial_export_finalize_two_shards_on_one_gpu(ref, day_cache, tmp_path, case):
-    """Journey-hash sharding into 2 'ranks' on one GPU: union of exported tuples finalized =
+def test_partial_export_finalize_shards_on_one_gpu(ref, day_cache, tmp_path, case, shards):
+    """Journey-hash sharding into 2/4/8 'ranks' on one GPU: union of exported tuples finalized =
     the single pipeline = the reference (fine_multiday: the fold's time-bin window reloads and
     the vacated-pair compaction run inside each rank's partial)."""
     import ctypes
@@ -150,8 +149,8 @@ def test_partial_export_finalize_two_shards_on_one_gpu(ref, day_cache, tmp_path,
 
     T, Dn, R, C = spec.dims()
     tuples = []
-    for rank in range(2):
-        mine = [l for l in rows if fnv(l.split(b",")[0]) % 2 == rank]
+    for rank in range(shards):
+        mine = [l for l in rows if fnv(l.split(b",")[0]) % shards == rank]
         blob = HEADER + b"\n" + b"\n".join(mine) + b"\n"
         d_csv = torch.frombuffer(bytearray(blob), dtype=torch.uint8).cuda()
         ctx = cvlg.Context()

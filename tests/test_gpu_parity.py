@@ -124,26 +124,8 @@ def test_table1_rows(ref, tmp_path):
 
 
 def test_malformed_and_edge_inputs(ref, tmp_path):
-    import corpus
-    rng = random.Random(5)
-    body = corpus.line_corpus(rng, 3000)
-    good = [b"jj%03d,2021-05-09 %02d:%02d:%02d,%.6f,%.6f,65101,%.2f,%.2f" % (
-        i % 17, (i // 3600) % 24, (i // 60) % 60, i % 60, 36.1 + (i % 400) * 0.01,
-        -95.7 + (i % 600) * 0.011, (i * 7.3) % 140, (i * 13.7) % 360) for i in range(4000)]
-    mixed = body + good
-    rng.shuffle(mixed)
-    contents = [
-        HEADER + b"\r\n" + b"\r\n".join(mixed[:1500]) + b"\r\n",
-        HEADER + b"\n" + b"\n\n".join(mixed[1500:4000]),  # blank lines, no trailing newline
-        b"",  # empty shard: no header, no rows
-        b"nope,nope\n1,2\n",  # BadHeader
-        b"heading,speed,zip code,longitude,latitude,timestamp,journey-id\n" + b"\n".join(
-            b"%s,%s,%s,%s,%s,%s,%s" % tuple(reversed(l.split(b",")[:7])) for l in good[:800]
-            if len(l.split(b",")) == 7),
-        HEADER,  # header only, no newline
-        HEADER + b"\n" + b"\n".join(mixed[4000:]) + b"\n",
-    ]
-    paths = write_shards(tmp_path, contents)
+    from helpers import malformed_contents
+    paths = write_shards(tmp_path, malformed_contents(5))
     for spec in (spec_default(), spec_degenerate()):
         est = assert_parity(ref, paths, spec)
     assert est["rejected"].get("BadHeader") == 1
