@@ -158,8 +158,9 @@ int cvlg_finalize_pairs(cvlg_context* ctx, const uint64_t* d_cell, const uint64_
  * journeys, and sends (cell, journey key, sum, count) tuples to the GPU owning the cell's time
  * slab, which folds them in the reference's (cell, journey) order. Output and stats are
  * byte-identical to cvlg_run_pipeline for every n_gpus. `devices` lists the CUDA devices (NULL:
- * 0..n_gpus-1); a device may repeat (several shards on one GPU). Journey ids must be <= 15 bytes
- * when n_gpus > 1 (exact inline keys across GPUs), else CVLG_E_UNSUPPORTED. */
+ * 0..n_gpus-1); a device may repeat (several shards on one GPU). Journey keys across GPUs are the
+ * exact inline ids when every id is <= 15 bytes, else global ranks from a host merge of the
+ * GPUs' sorted id lists. */
 typedef struct cvlg_multi cvlg_multi;
 cvlg_multi* cvlg_multi_create(const int* devices, uint32_t n_gpus);
 void cvlg_multi_destroy(cvlg_multi* m);
@@ -192,7 +193,17 @@ int cvlg_route_count(cvlg_context* ctx);
 int cvlg_route_plan(cvlg_context* ctx, uint32_t owner, uint64_t* vshard_off, uint64_t* stream_len);
 int cvlg_route_scatter(cvlg_context* ctx, uint8_t* const* d_dst, void* stream);
 int cvlg_tuples_export(cvlg_context* ctx, const cvlg_grid_spec* spec, uint32_t n_owners,
-                       uint64_t* counts, uint64_t* n_tuples);
+                       const uint32_t* global_rank, uint64_t* counts, uint64_t* n_tuples);
+/* Journey keys across GPUs: with every id <= 15 bytes (cvlg_partial_info long_ids == 0 on every
+ * rank) the tuples carry exact inline keys (global_rank NULL). Otherwise every rank exports its
+ * sorted ids (cvlg_journey_ids, local rank order; call with NULL buffers for the sizes), the
+ * lists are merged (cvlg_merge_id_ranks, host only: ranks[i][r] = global lexicographic rank of
+ * list i's id r) and each rank passes its global_rank (host array, one per local journey). */
+int cvlg_partial_info(cvlg_context* ctx, uint64_t* n_journeys, uint64_t* n_pairs, int32_t* long_ids);
+int cvlg_journey_ids(cvlg_context* ctx, uint8_t* blob, uint64_t blob_cap, uint64_t* offs,
+                     uint64_t offs_cap, uint64_t* n_journeys, uint64_t* blob_bytes);
+int cvlg_merge_id_ranks(uint32_t n_lists, const uint8_t* const* blobs, const uint64_t* const* offs,
+                        const uint64_t* n_ids, uint32_t* const* ranks);
 int cvlg_tuples_scatter(cvlg_context* ctx, const cvlg_grid_spec* spec, uint32_t n_owners,
                         void* const* d_dst, void* stream);
 int cvlg_finalize_tuples(cvlg_context* ctx, const void* d_tuples, uint64_t n,

@@ -170,7 +170,12 @@ void launch_rank_slot(const uint32_t* uslot, const uint32_t* perm, uint64_t n, u
 void launch_export_pairs(const uint64_t* pkey, const double* psum, const uint32_t* pcnt, uint64_t n,
                          int rbits, const uint32_t* rank_slot, const unsigned long long* table,
                          uint64_t* cell, uint64_t* k0, uint64_t* k1, double* sum, uint64_t* cnt,
-                         uint64_t stride, uint32_t* bad, cudaStream_t s);
+                         uint64_t stride, const uint32_t* grank, uint32_t* bad, cudaStream_t s);
+// journey ids by local rank: lengths, then the bytes at pos[r] (exclusive scan of the lengths)
+void launch_id_len(const uint32_t* rank_slot, const unsigned long long* table, uint64_t n,
+                   uint32_t* len, cudaStream_t s);
+void launch_id_copy(const uint32_t* rank_slot, const unsigned long long* table, const uint8_t* csv,
+                    uint64_t n, const uint32_t* pos, uint8_t* blob, cudaStream_t s);
 // dst[i] = src[(idx ? idx[i] : i) * stride]  (stride in u64 words: 1 = SoA column, 5 = PairTuple)
 void launch_gather_u64(const uint64_t* src, uint64_t stride, const uint32_t* idx, uint64_t n,
                        uint64_t* dst, cudaStream_t s);

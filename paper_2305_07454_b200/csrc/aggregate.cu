@@ -974,20 +974,57 @@ __global__ void export_pairs_kernel(const uint64_t* pkey, const double* psum, co
                                     uint64_t n, int rbits, const uint32_t* rank_slot,
                                     const unsigned long long* table, uint64_t* cell, uint64_t* k0,
                                     uint64_t* k1, double* sum, uint64_t* cnt, uint64_t stride,
-                                    uint32_t* bad) {
+                                    const uint32_t* grank, uint32_t* bad) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (i >= n) return;
     const uint64_t key = pkey[i];
     const uint64_t r = rbits ? (key & ((1ull << rbits) - 1)) : 0;
-    const uint32_t slot = rank_slot[r];
-    const uint64_t e0 = table[2 * slot], e1 = table[2 * slot + 1];
-    if ((e1 & 0xFF) == 0xFF) *bad = 1u;  // id longer than 15 bytes: no exact inline key
+    uint64_t e0, e1;
+    if (grank) {  // global lexicographic rank (any id length), merged across GPUs on the host
+        e0 = grank[r];
+        e1 = 0;
+    } else {
+        const uint32_t slot = rank_slot[r];
+        e0 = table[2 * slot];
+        e1 = table[2 * slot + 1];
+        if ((e1 & 0xFF) == 0xFF) *bad = 1u;  // id longer than 15 bytes: no exact inline key
+    }
     const uint64_t o = i * stride;
     cell[o] = key >> rbits;
     k0[o] = e0;
     k1[o] = e1;
     sum[o] = psum[i];
     cnt[o] = pcnt[i];
+}
+
+// Journey ids in local rank order (for the cross-GPU merge of long ids): lengths, then bytes.
+__device__ __forceinline__ uint32_t id_len_of(uint64_t e0, uint64_t e1) {
+    return (e1 & 0xFF) == 0xFF ? static_cast<uint32_t>(e0 & 0xFFFFFF) : static_cast<uint32_t>(e1 & 0xFF);
+}
+
+__global__ void id_len_kernel(const uint32_t* rank_slot, const unsigned long long* table, uint64_t n,
+                              uint32_t* len) {
+    const uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (r >= n) return;
+    const uint32_t slot = rank_slot[r];
+    len[r] = id_len_of(table[2 * slot], table[2 * slot + 1]);
+}
+
+__global__ void id_copy_kernel(const uint32_t* rank_slot, const unsigned long long* table,
+                               const uint8_t* csv, uint64_t n, const uint32_t* pos, uint8_t* blob) {
+    const uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (r >= n) return;
+    const uint32_t slot = rank_slot[r];
+    const uint64_t e0 = table[2 * slot], e1 = table[2 * slot + 1];
+    const uint32_t len = id_len_of(e0, e1);
+    uint8_t* d = blob + pos[r];
+    if ((e1 & 0xFF) == 0xFF) {
+        const uint8_t* p = csv + (e1 >> 8);
+        for (uint32_t k = 0; k < len; ++k) d[k] = p[k];
+    } else {
+        for (uint32_t k = 0; k < len; ++k)
+            d[k] = static_cast<uint8_t>(k < 8 ? e0 >> (56 - 8 * k) : e1 >> (64 - 8 * (k - 8)));
+    }
 }
 
 __global__ void gather_u64_kernel(const uint64_t* src, uint64_t stride, const uint32_t* idx,
@@ -1201,10 +1238,25 @@ void launch_rank_slot(const uint32_t* uslot, const uint32_t* perm, uint64_t n, u
 void launch_export_pairs(const uint64_t* pkey, const double* psum, const uint32_t* pcnt, uint64_t n,
                          int rbits, const uint32_t* rank_slot, const unsigned long long* table,
                          uint64_t* cell, uint64_t* k0, uint64_t* k1, double* sum, uint64_t* cnt,
-                         uint64_t stride, uint32_t* bad, cudaStream_t s) {
+                         uint64_t stride, const uint32_t* grank, uint32_t* bad, cudaStream_t s) {
     if (!n) return;
     export_pairs_kernel<<<grid_for(n, 256), 256, 0, s>>>(pkey, psum, pcnt, n, rbits, rank_slot,
-                                                         table, cell, k0, k1, sum, cnt, stride, bad);
+                                                         table, cell, k0, k1, sum, cnt, stride,
+                                                         grank, bad);
+    count_launch();
+}
+
+void launch_id_len(const uint32_t* rank_slot, const unsigned long long* table, uint64_t n,
+                   uint32_t* len, cudaStream_t s) {
+    if (!n) return;
+    id_len_kernel<<<grid_for(n, 256), 256, 0, s>>>(rank_slot, table, n, len);
+    count_launch();
+}
+
+void launch_id_copy(const uint32_t* rank_slot, const unsigned long long* table, const uint8_t* csv,
+                    uint64_t n, const uint32_t* pos, uint8_t* blob, cudaStream_t s) {
+    if (!n) return;
+    id_copy_kernel<<<grid_for(n, 256), 256, 0, s>>>(rank_slot, table, csv, n, pos, blob);
     count_launch();
 }
 

@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstring>
 #include <numeric>
+#include <string_view>
 #include <thread>
 #include <vector>
 
@@ -111,6 +112,43 @@ std::vector<std::vector<Piece>> split_manifest(const char* const* paths, const s
 }
 
 void route_count(cvlg_context* c);
+
+void merge_id_ranks(const std::vector<const std::vector<uint8_t>*>& blobs,
+                    const std::vector<const std::vector<uint64_t>*>& offs,
+                    std::vector<std::vector<uint32_t>>& ranks) {
+    const size_t n = blobs.size();
+    ranks.assign(n, {});
+    struct Cur {
+        size_t list;
+        uint64_t r;
+    };
+    auto view = [&](const Cur& c) {
+        const std::vector<uint64_t>& o = *offs[c.list];
+        return std::string_view(reinterpret_cast<const char*>(blobs[c.list]->data()) + o[c.r],
+                                o[c.r + 1] - o[c.r]);
+    };
+    // std::string order = lexicographic unsigned bytes, prefix first (string_view compare)
+    auto later = [&](const Cur& a, const Cur& b) { return view(a) > view(b); };
+    std::vector<Cur> heap;
+    for (size_t i = 0; i < n; ++i) {
+        const uint64_t J = offs[i]->size() - 1;
+        ranks[i].assign(J, 0);
+        if (J) heap.push_back(Cur{i, 0});
+    }
+    std::make_heap(heap.begin(), heap.end(), later);
+    uint64_t g = 0;
+    while (!heap.empty()) {
+        std::pop_heap(heap.begin(), heap.end(), later);
+        Cur c = heap.back();
+        heap.pop_back();
+        if (g >= 0xFFFFFFFFull) fail(CVLG_E_UNSUPPORTED, ">= 2^32 - 1 journeys");
+        ranks[c.list][c.r] = static_cast<uint32_t>(g++);
+        if (++c.r + 1 < offs[c.list]->size()) {
+            heap.push_back(c);
+            std::push_heap(heap.begin(), heap.end(), later);
+        }
+    }
+}
 
 // Step 2 + 3a: stream the pieces into c->slice, find every line's owner, count bytes per
 // (tile, owner), scan. The routing plan stays in the context.
@@ -244,13 +282,21 @@ void route_scatter(cvlg_context* c, uint8_t* const* dst, cudaStream_t s) {
 }
 
 // Step 5a: the context's subtotals as PairTuples (c->tuples), counted per slab owner.
-void tuples_export(cvlg_context* c, const Dims& dims, uint32_t n_owners, cudaStream_t s) {
+void tuples_export(cvlg_context* c, const Dims& dims, uint32_t n_owners, cudaStream_t s,
+                   const std::vector<uint32_t>* grank) {
     if (n_owners == 0 || n_owners > static_cast<uint32_t>(kMaxOwners))
         fail(CVLG_E_INVALID_ARG, "the combine supports 1.." + std::to_string(kMaxOwners) + " GPUs");
     const uint64_t n = c->part_pairs;
     c->tuples.ensure(n * sizeof(PairTuple) + 64);
     PairTuple* tu = c->tuples.as<PairTuple>();
-    export_tuples(c, &tu->cell, &tu->key0, &tu->key1, &tu->sum, &tu->count, 5, s);
+    const uint32_t* d_grank = nullptr;
+    if (grank) {
+        c->r_grank.ensure(grank->size() * 4 + 4);
+        if (!grank->empty())
+            CK(cudaMemcpy(c->r_grank.p, grank->data(), grank->size() * 4, cudaMemcpyHostToDevice));
+        d_grank = c->r_grank.as<uint32_t>();
+    }
+    export_tuples(c, &tu->cell, &tu->key0, &tu->key1, &tu->sum, &tu->count, 5, s, d_grank);
     c->t_n = n;
     c->t_counts.ensure(kMaxOwners * 8);
     CK(cudaMemsetAsync(c->t_counts.p, 0, kMaxOwners * 8, s));
@@ -381,7 +427,26 @@ void run_multi(cvlg_multi* m, const char* const* paths, size_t n, const cvlg_gri
         std::vector<uint8_t> good(vmap[o].size(), 1);
         run_core(c, c->csv.as<uint8_t>(), voff[o], vmap[o].data(), good.data(), 0, spec, rules, nullptr,
                  nullptr, &st[o], marks_of({ChunkMark{recv[o], recv[o], nullptr}}), true);
-        tuples_export(c, dims, N, c->stream);
+    });
+    // journey keys that order like the ids across GPUs: exact inline keys (ids <= 15 bytes), else
+    // global ranks from a merge of every owner's sorted ids
+    bool long_ids = false;
+    for (uint32_t o = 0; o < N; ++o) long_ids |= m->ctx[o]->part_long_ids;
+    std::vector<std::vector<uint32_t>> granks;
+    if (long_ids) {
+        std::vector<std::vector<uint8_t>> blobs(N);
+        std::vector<std::vector<uint64_t>> offs(N);
+        parallel(m, [&](uint32_t o) { journey_ids(m->ctx[o], blobs[o], offs[o]); });
+        std::vector<const std::vector<uint8_t>*> bp;
+        std::vector<const std::vector<uint64_t>*> op;
+        for (uint32_t o = 0; o < N; ++o) {
+            bp.push_back(&blobs[o]);
+            op.push_back(&offs[o]);
+        }
+        merge_id_ranks(bp, op, granks);
+    }
+    parallel(m, [&](uint32_t o) {
+        tuples_export(m->ctx[o], dims, N, m->ctx[o]->stream, granks.empty() ? nullptr : &granks[o]);
     });
     // 5: tuples to their slab owners, folded there
     std::vector<uint64_t> tin(N, 0);
@@ -576,13 +641,58 @@ int cvlg_route_scatter(cvlg_context* ctx, uint8_t* const* d_dst, void* stream) {
     });
 }
 
+int cvlg_partial_info(cvlg_context* ctx, uint64_t* n_journeys, uint64_t* n_pairs, int32_t* long_ids) {
+    if (!ctx) return CVLG_E_INVALID_ARG;
+    if (n_journeys) *n_journeys = ctx->part_J;
+    if (n_pairs) *n_pairs = ctx->part_pairs;
+    if (long_ids) *long_ids = ctx->part_long_ids ? 1 : 0;
+    return CVLG_OK;
+}
+
+int cvlg_journey_ids(cvlg_context* ctx, uint8_t* blob, uint64_t blob_cap, uint64_t* offs,
+                     uint64_t offs_cap, uint64_t* n_journeys, uint64_t* blob_bytes) {
+    return guard([&] {
+        if (!ctx) fail(CVLG_E_INVALID_ARG, "context is NULL");
+        CK(cudaSetDevice(ctx->device));
+        std::vector<uint8_t> b;
+        std::vector<uint64_t> o;
+        journey_ids(ctx, b, o);
+        if (n_journeys) *n_journeys = o.size() - 1;
+        if (blob_bytes) *blob_bytes = b.size();
+        if (blob && !b.empty()) std::memcpy(blob, b.data(), std::min<uint64_t>(blob_cap, b.size()));
+        if (offs) std::memcpy(offs, o.data(), std::min<uint64_t>(offs_cap, o.size()) * 8);
+    });
+}
+
+int cvlg_merge_id_ranks(uint32_t n_lists, const uint8_t* const* blobs, const uint64_t* const* offs,
+                        const uint64_t* n_ids, uint32_t* const* ranks) {
+    return guard([&] {
+        std::vector<std::vector<uint8_t>> bv(n_lists);
+        std::vector<std::vector<uint64_t>> ov(n_lists);
+        std::vector<const std::vector<uint8_t>*> bp;
+        std::vector<const std::vector<uint64_t>*> op;
+        for (uint32_t i = 0; i < n_lists; ++i) {
+            ov[i].assign(offs[i], offs[i] + n_ids[i] + 1);
+            bv[i].assign(blobs[i], blobs[i] + ov[i].back());
+            bp.push_back(&bv[i]);
+            op.push_back(&ov[i]);
+        }
+        std::vector<std::vector<uint32_t>> r;
+        merge_id_ranks(bp, op, r);
+        for (uint32_t i = 0; i < n_lists; ++i)
+            if (!r[i].empty()) std::memcpy(ranks[i], r[i].data(), r[i].size() * 4);
+    });
+}
+
 int cvlg_tuples_export(cvlg_context* ctx, const cvlg_grid_spec* spec, uint32_t n_owners,
-                       uint64_t* counts, uint64_t* n_tuples) {
+                       const uint32_t* global_rank, uint64_t* counts, uint64_t* n_tuples) {
     return guard([&] {
         const Dims dims = validate_grid(spec);
         if (!ctx) fail(CVLG_E_INVALID_ARG, "context is NULL");
         CK(cudaSetDevice(ctx->device));
-        tuples_export(ctx, dims, n_owners, ctx->stream);
+        std::vector<uint32_t> gr;
+        if (global_rank) gr.assign(global_rank, global_rank + ctx->part_J);
+        tuples_export(ctx, dims, n_owners, ctx->stream, global_rank ? &gr : nullptr);
         if (counts) std::memcpy(counts, ctx->t_h_counts.data(), n_owners * 8);
         if (n_tuples) *n_tuples = ctx->t_n;
     });

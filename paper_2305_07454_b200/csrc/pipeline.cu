@@ -222,6 +222,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
               bool partial, const double* feat_stop_speed) {
     const bool feat = feat_stop_speed != nullptr;
     const Dims dims = validate_grid(spec);
+    c->csv_in = d_csv;
     const GridParams gp = make_params(spec, rules, dims);
     cudaStream_t s = c->stream;
     const uint32_t n_shards = static_cast<uint32_t>(shard_off.size() - 1);
@@ -1193,8 +1194,9 @@ RingIngest::~RingIngest() {
 }
 
 void export_tuples(cvlg_context* c, uint64_t* d_cell, uint64_t* d_key0, uint64_t* d_key1,
-                   double* d_sum, uint64_t* d_count, uint64_t stride, cudaStream_t s) {
-    if (c->part_long_ids)
+                   double* d_sum, uint64_t* d_count, uint64_t stride, cudaStream_t s,
+                   const uint32_t* d_grank) {
+    if (c->part_long_ids && !d_grank)
         fail(CVLG_E_UNSUPPORTED, "multi-GPU combine needs journey ids <= 15 bytes (exact inline keys)");
     const uint64_t n = c->part_pairs;
     if (!n) return;
@@ -1203,12 +1205,41 @@ void export_tuples(cvlg_context* c, uint64_t* d_cell, uint64_t* d_key0, uint64_t
     CK(cudaMemsetAsync(d_bad, 0, 4, s));
     launch_export_pairs(c->pair_key.as<uint64_t>(), c->pair_sum.as<double>(), c->pair_cnt.as<uint32_t>(),
                         n, c->part_rbits, c->rank_slot.as<uint32_t>(), c->dict.as<unsigned long long>(),
-                        d_cell, d_key0, d_key1, d_sum, d_count, stride, d_bad, s);
+                        d_cell, d_key0, d_key1, d_sum, d_count, stride, d_grank, d_bad, s);
     uint32_t* hb = static_cast<uint32_t*>(c->h_small.p) + 200;
     CK(cudaMemcpyAsync(hb, d_bad, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
     if (*hb) fail(CVLG_E_UNSUPPORTED, "multi-GPU combine needs journey ids <= 15 bytes (exact inline keys)");
+}
+
+void journey_ids(cvlg_context* c, std::vector<uint8_t>& blob, std::vector<uint64_t>& offs) {
+    const uint64_t J = c->part_J;
+    offs.assign(J + 1, 0);
+    blob.clear();
+    if (!J) return;
+    cudaStream_t s = c->stream;
+    c->flags.ensure(J * 4 + 16);
+    c->pos.ensure(J * 4 + 16);
+    c->scan_tmp.ensure(scan_temp_words(J) * 4 + 64);
+    c->scal.ensure(128);
+    uint32_t* d_total = c->scal.as<uint32_t>() + 30;
+    launch_id_len(c->rank_slot.as<uint32_t>(), c->dict.as<unsigned long long>(), J, c->flags.as<uint32_t>(), s);
+    exclusive_scan_u32(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), J, d_total, c->scan_tmp.as<uint32_t>(), s);
+    uint32_t total = 0;
+    CK(cudaMemcpyAsync(&total, d_total, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    c->x_keys.ensure(static_cast<uint64_t>(total) + 16);
+    launch_id_copy(c->rank_slot.as<uint32_t>(), c->dict.as<unsigned long long>(), c->csv_in,
+                   J, c->pos.as<uint32_t>(), c->x_keys.as<uint8_t>(), s);
+    std::vector<uint32_t> pos(J);
+    blob.resize(total);
+    CK(cudaMemcpyAsync(pos.data(), c->pos.p, J * 4, cudaMemcpyDeviceToHost, s));
+    if (total) CK(cudaMemcpyAsync(blob.data(), c->x_keys.p, total, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    for (uint64_t r = 0; r < J; ++r) offs[r] = pos[r];
+    offs[J] = total;
 }
 
 void finalize_tuples(cvlg_context* c, const uint64_t* d_cell, const uint64_t* d_key0,
@@ -1538,7 +1569,7 @@ int cvlg_export_pairs(cvlg_context* ctx, uint64_t* d_cell, uint64_t* d_key0, uin
         if (c->part_pairs && (!d_cell || !d_key0 || !d_key1 || !d_sum || !d_count))
             fail(CVLG_E_INVALID_ARG, "NULL argument");
         export_tuples(c, d_cell, d_key0, d_key1, d_sum, d_count, 1,
-                      stream ? static_cast<cudaStream_t>(stream) : c->stream);
+                      stream ? static_cast<cudaStream_t>(stream) : c->stream, nullptr);
     });
 }
 

@@ -105,6 +105,8 @@ struct cvlg_context {
     // last cvlg_partial_device run: pairs kept in pair_key/pair_sum/pair_cnt
     uint64_t part_pairs = 0, part_J = 0, last_slots = 0;
     uint64_t input_bytes = 0;  // bytes of c->csv staged by the last host/file run
+    const uint8_t* csv_in = nullptr;  // CSV bytes of the last run (long journey ids point into it)
+    cvlg::DevBuf r_grank;             // global journey ranks (multi-GPU combine with long ids)
     int part_rbits = 0;
     bool part_long_ids = false;
     std::vector<cudaEvent_t> chunk_events;
@@ -129,8 +131,18 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
 
 // Per-(cell, journey) subtotals of the last partial run -> (cell, key0, key1, sum, count) with
 // exact global journey keys (stride in u64 words between consecutive tuples' fields).
+// With d_grank (device, one u32 per local journey rank: its rank in the global lexicographic
+// order of all GPUs' ids) the key is (grank, 0) and ids of any length are supported.
 void export_tuples(cvlg_context* c, uint64_t* d_cell, uint64_t* d_key0, uint64_t* d_key1,
-                   double* d_sum, uint64_t* d_count, uint64_t stride, cudaStream_t s);
+                   double* d_sum, uint64_t* d_count, uint64_t stride, cudaStream_t s,
+                   const uint32_t* d_grank);
+// The last partial run's journey ids in local rank order (host): bytes of rank r are
+// blob[offs[r], offs[r + 1]).
+void journey_ids(cvlg_context* c, std::vector<uint8_t>& blob, std::vector<uint64_t>& offs);
+// Global lexicographic ranks of the union of n sorted, pairwise disjoint id lists.
+void merge_id_ranks(const std::vector<const std::vector<uint8_t>*>& blobs,
+                    const std::vector<const std::vector<uint64_t>*>& offs,
+                    std::vector<std::vector<uint32_t>>& ranks);
 // Any union of such tuples -> dense lattice (cells without tuples are zero), synchronous.
 void finalize_tuples(cvlg_context* c, const uint64_t* d_cell, const uint64_t* d_key0,
                      const uint64_t* d_key1, const double* d_sum, const uint64_t* d_count,

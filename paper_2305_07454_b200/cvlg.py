@@ -133,7 +133,11 @@ def _load() -> ctypes.CDLL:
     lib.cvlg_route_count.argtypes = [vp]
     lib.cvlg_route_plan.argtypes = [vp, ctypes.c_uint32, u64p, u64p]
     lib.cvlg_route_scatter.argtypes = [vp, ctypes.POINTER(vp), vp]
-    lib.cvlg_tuples_export.argtypes = [vp, ctypes.POINTER(_Grid), ctypes.c_uint32, u64p, u64p]
+    lib.cvlg_tuples_export.argtypes = [vp, ctypes.POINTER(_Grid), ctypes.c_uint32, vp, u64p, u64p]
+    lib.cvlg_partial_info.argtypes = [vp, u64p, u64p, ctypes.POINTER(ctypes.c_int32)]
+    lib.cvlg_journey_ids.argtypes = [vp, vp, ctypes.c_uint64, u64p, ctypes.c_uint64, u64p, u64p]
+    lib.cvlg_merge_id_ranks.argtypes = [ctypes.c_uint32, ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                        u64p, ctypes.POINTER(vp)]
     lib.cvlg_tuples_scatter.argtypes = [vp, ctypes.POINTER(_Grid), ctypes.c_uint32,
                                         ctypes.POINTER(vp), vp]
     lib.cvlg_finalize_tuples.argtypes = [vp, vp, ctypes.c_uint64, ctypes.POINTER(_Grid), vp, vp,
@@ -158,7 +162,8 @@ EXPORTED_SYMBOLS = [
     "cvlg_multi_create", "cvlg_multi_destroy", "cvlg_multi_size", "cvlg_multi_context",
     "cvlg_run_pipeline_multi", "cvlg_route_stage", "cvlg_route_count", "cvlg_route_plan",
     "cvlg_route_scatter", "cvlg_tuples_export", "cvlg_tuples_scatter", "cvlg_finalize_tuples",
-    "cvlg_slab_rows", "cvlg_split_manifest", "cvlg_partial_device",
+    "cvlg_slab_rows", "cvlg_split_manifest", "cvlg_partial_device", "cvlg_partial_info",
+    "cvlg_journey_ids", "cvlg_merge_id_ranks",
 ]
 
 

@@ -185,15 +185,24 @@ class FileShardedPipeline:
         counts = (ctypes.c_uint64 * world)()
         n_t = ctypes.c_uint64()
 
+        long_ids = ctypes.c_int32()
+
         def local():
             _c._check(_lib.cvlg_partial_device(self.ctx.handle, _vp(buf.data_ptr()), carr,
                                                len(offs) - 1, ctypes.byref(spec._c()),
                                                ctypes.byref(self.rules._c()), ctypes.byref(n_pairs),
                                                ctypes.byref(st), None))
-            # 4. tuples by slab owner (ids > 15 bytes fail here, on every rank alike)
-            _c._check(_lib.cvlg_tuples_export(self.ctx.handle, ctypes.byref(spec._c()), world,
-                                              counts, ctypes.byref(n_t)))
+            _c._check(_lib.cvlg_partial_info(self.ctx.handle, None, None, ctypes.byref(long_ids)))
         agreed(local, g)
+        # 4. journey keys: exact inline ids, or global ranks when any rank has ids > 15 bytes
+        grank = None
+        if any(all_gather_obj(int(long_ids.value), g)):
+            lists = all_gather_obj(self._journey_ids(), g)
+            grank = self._merge(lists)[self.rank]
+        agreed(lambda: _c._check(_lib.cvlg_tuples_export(
+            self.ctx.handle, ctypes.byref(spec._c()), world,
+            grank.ctypes.data_as(_vp) if grank is not None and grank.size else None,
+            counts, ctypes.byref(n_t))), g)
         self.local_parsed = int(st.parsed)
         tcount = [int(counts[i]) for i in range(world)]
         toff = np.concatenate([[0], np.cumsum(tcount)]).astype(np.int64)
@@ -238,6 +247,31 @@ class FileShardedPipeline:
         out["rejected"] = {k: x for k, x in zip(_c.REJECT_NAMES, v[5:10]) if x}
         out["filtered"] = dict(zip(_c.FILTER_NAMES, v[10:13]))
         return out
+
+    def _journey_ids(self) -> tuple[bytes, np.ndarray]:
+        """This rank's journey ids in local rank order: (bytes, offsets[J + 1])."""
+        nj, nb = ctypes.c_uint64(), ctypes.c_uint64()
+        _c._check(_lib.cvlg_journey_ids(self.ctx.handle, None, 0, None, 0, ctypes.byref(nj),
+                                        ctypes.byref(nb)))
+        blob = np.empty(max(nb.value, 1), dtype=np.uint8)
+        offs = np.empty(nj.value + 1, dtype=np.uint64)
+        _c._check(_lib.cvlg_journey_ids(self.ctx.handle, blob.ctypes.data_as(_vp), blob.size,
+                                        offs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                        offs.size, None, None))
+        return blob[: nb.value].tobytes(), offs
+
+    @staticmethod
+    def _merge(lists) -> list[np.ndarray]:
+        """Global lexicographic ranks of every rank's ids (cvlg_merge_id_ranks, host code)."""
+        n = len(lists)
+        blobs = [np.frombuffer(b or b"\0", dtype=np.uint8) for b, _ in lists]
+        offs = [np.ascontiguousarray(o, dtype=np.uint64) for _, o in lists]
+        ranks = [np.empty(max(len(o) - 1, 1), dtype=np.uint32) for o in offs]
+        counts = (ctypes.c_uint64 * n)(*[len(o) - 1 for o in offs])
+        _c._check(_lib.cvlg_merge_id_ranks(
+            n, (_vp * n)(*[b.ctypes.data for b in blobs]), (_vp * n)(*[o.ctypes.data for o in offs]),
+            counts, (_vp * n)(*[r.ctypes.data for r in ranks])))
+        return [r[: len(o) - 1] for r, o in zip(ranks, offs)]
 
     def _all_gather(self, x: torch.Tensor) -> list[torch.Tensor]:
         g = self.group

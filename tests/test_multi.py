@@ -129,9 +129,12 @@ def _gloo_worker(rank, world, port, paths, out_dir, q):
         for i in range(len(offs) - 1):
             blob = recv[offs[i]:offs[i + 1]]
             (Path(out_dir) / f"o{rank}_{i:06d}.csv").write_bytes(blob)
-            for raw in blob.split(b"\n")[1:]:
+            lines = blob.split(b"\n")
+            cols = ref.parse_header(lines[0].rstrip(b"\r"))
+            for raw in lines[1:]:
                 if raw and raw != b"\r":
-                    owned.add(raw.split(b",")[0].strip(b" \t\r"))
+                    f = raw.rstrip(b"\r").split(b",")
+                    owned.add(f[cols[0]].strip(b" \t\r") if cols[0] < len(f) else b"")
         q.put((rank, sorted(owned), None))
     except Exception as e:  # pragma: no cover
         q.put((rank, None, repr(e)))
@@ -240,14 +243,29 @@ def test_multi_gpu_pipeline_matches_reference(ref, tmp_path, day_cache, n_gpus):
 
 
 @pytest.mark.gpu
-def test_multi_gpu_long_ids_unsupported(tmp_path):
+@pytest.mark.parametrize("n_gpus", [1, 2, 5])
+def test_multi_gpu_long_ids(ref, tmp_path, n_gpus):
+    """Ids longer than the 15-byte inline key: journeys keyed by global ranks (host merge of
+    every GPU's sorted ids), including ids that share a 15-byte prefix."""
+    import random
     import paper_2305_07454_b200 as cvlg
-    rows = [b"vehicle-%012d,2021-05-09 01:00:%02d,37.5,-93.5,65101,10.0,20.0" % (i, i) for i in range(40)]
-    paths = write_shards(tmp_path, [HEADER + b"\n" + b"\n".join(rows) + b"\n"])
-    m = cvlg.MultiGPU([0, 0])
-    with pytest.raises(cvlg.CvlError) as e:
-        m.run_pipeline(paths)
-    assert e.value.code == "Unsupported"
+    rng = random.Random(3)
+    ids = ([b"vehicle-%012d" % i for i in range(30)] + [b"x" * n for n in range(1, 25)]
+           + [b"prefix-shared-%d-tail" % i for i in range(12)] + [b"j%06d" % i for i in range(20)])
+    rows = []
+    for k in range(5000):
+        j = rng.choice(ids)
+        rows.append(b"%s,2021-05-09 %02d:%02d:%02d,%.6f,%.6f,65101,%.2f,%.2f" % (
+            j, rng.randrange(24), rng.randrange(60), rng.randrange(60), 36.2 + rng.random() * 0.5,
+            -95.5 + rng.random() * 0.5, rng.uniform(0, 120), rng.uniform(0, 360)))
+    paths = write_shards(tmp_path, [HEADER + b"\n" + b"\n".join(rows[i::3]) + b"\n" for i in range(3)])
+    spec = cvlg.GridSpec(lat_step=0.25, lon_step=0.25)
+    ep, er, est, _ = ref.run_pipeline(paths, spec)
+    m = cvlg.MultiGPU([0] * n_gpus)
+    st = cvlg.PipelineStats()
+    lat = m.run_pipeline(paths, spec, stats=st)
+    assert diff_lattice(ep, er, lat.planes, lat.raw) == ""
+    assert stats_dict(st) == est
     m.close()
 
 
