@@ -184,7 +184,8 @@ int cvlg_run_pipeline_multi(cvlg_multi* m, const char* const* shard_paths, size_
  *     f64 sum, u64 count) tuples, counted per slab owner (counts[n_owners], owner of a tuple =
  *     t * n_owners / T for its time bin t; cvlg_slab_rows gives each owner's rows [t0, t1)).
  *  5. cvlg_tuples_scatter: writes them to d_dst[owner] (device pointers on this device).
- *  6. cvlg_finalize_tuples: folds received tuples into a lattice (rows of the owner's slab). */
+ *  6. cvlg_finalize_tuples: folds received tuples into rows [t0, t1) of the lattice (the
+ *     owner's slab; d_planes / d_raw_count hold those rows only). */
 int cvlg_route_stage(cvlg_context* ctx, const char* const* shard_paths, size_t n_shards,
                      uint32_t n_parts, uint32_t part, uint32_t n_threads, uint64_t* n_pieces,
                      uint64_t* bad_headers);
@@ -207,8 +208,8 @@ int cvlg_merge_id_ranks(uint32_t n_lists, const uint8_t* const* blobs, const uin
 int cvlg_tuples_scatter(cvlg_context* ctx, const cvlg_grid_spec* spec, uint32_t n_owners,
                         void* const* d_dst, void* stream);
 int cvlg_finalize_tuples(cvlg_context* ctx, const void* d_tuples, uint64_t n,
-                         const cvlg_grid_spec* spec, uint32_t* d_planes, uint32_t* d_raw_count,
-                         void* stream);
+                         const cvlg_grid_spec* spec, uint32_t t0, uint32_t t1, uint32_t* d_planes,
+                         uint32_t* d_raw_count, void* stream);
 int cvlg_slab_rows(uint32_t n_batches, uint32_t n_owners, uint32_t owner, uint32_t* t0, uint32_t* t1);
 /* Host only (no GPU needed): the pieces of part `part` of n_parts, as cvlg_route_stage cuts them:
  * (rank of the file in lexicographic path order, byte offset, length), at most `cap` written. */

@@ -183,6 +183,7 @@ void launch_import_pairs(const double* sum, const uint64_t* cnt, uint64_t stride
                          double* psum, uint32_t* pcnt, cudaStream_t s);
 void launch_finalize(const uint64_t* keys, const uint32_t* vals, uint64_t n, int rank_bits,
                      const double* pair_sum, const uint32_t* pair_cnt, uint32_t D, uint64_t RC,
-                     uint32_t* planes, uint32_t* raw, cudaStream_t s);
+                     uint32_t t_base, uint32_t t_rows, uint32_t* planes, uint32_t* raw,
+                     cudaStream_t s);
 
 }  // namespace cvlg

@@ -939,10 +939,13 @@ __global__ void pair_vals_kernel(uint32_t* vals, uint64_t n) {
 // ---- Z: canonical per-cell fold (finalize_range, aggregate.cpp:161-187) ----------------------
 __global__ void finalize_kernel(const uint64_t* keys, const uint32_t* vals, uint64_t n,
                                 int rank_bits, const double* pair_sum, const uint32_t* pair_cnt,
-                                uint32_t D, uint64_t RC, uint32_t* planes, uint32_t* raw) {
+                                uint32_t D, uint64_t RC, uint32_t t_base, uint32_t t_rows,
+                                uint32_t* planes, uint32_t* raw) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (i >= n) return;
     const uint64_t g = keys[i] >> rank_bits;
+    const uint64_t tg = g / (D * RC);
+    if (tg < t_base || tg - t_base >= t_rows) return;  // outside the rows this lattice holds
     if (i > 0 && (keys[i - 1] >> rank_bits) == g) return;
     double sum = 0.0;
     uint64_t cnt = 0;
@@ -952,7 +955,7 @@ __global__ void finalize_kernel(const uint64_t* keys, const uint32_t* vals, uint
         cnt += pair_cnt[vals[k]];
         ++vol;
     }
-    const uint64_t t = g / (D * RC);
+    const uint64_t t = tg - t_base;
     const uint64_t d = (g / RC) % D;
     const uint64_t rc = g % RC;
     const float mean = __double2float_rn(__ddiv_rn(sum, static_cast<double>(cnt)));
@@ -1282,10 +1285,11 @@ void launch_pair_vals(uint32_t* vals, uint64_t n, cudaStream_t s) {
 
 void launch_finalize(const uint64_t* keys, const uint32_t* vals, uint64_t n, int rank_bits,
                      const double* pair_sum, const uint32_t* pair_cnt, uint32_t D, uint64_t RC,
-                     uint32_t* planes, uint32_t* raw, cudaStream_t s) {
+                     uint32_t t_base, uint32_t t_rows, uint32_t* planes, uint32_t* raw,
+                     cudaStream_t s) {
     if (!n) return;
     finalize_kernel<<<grid_for(n, 256), 256, 0, s>>>(keys, vals, n, rank_bits, pair_sum, pair_cnt,
-                                                     D, RC, planes, raw);
+                                                     D, RC, t_base, t_rows, planes, raw);
     count_launch();
 }
 

@@ -479,21 +479,20 @@ void run_multi(cvlg_multi* m, const char* const* paths, size_t n, const cvlg_gri
     const uint64_t rc4 = 4 * dims.RC;
     parallel(m, [&](uint32_t s) {
         cvlg_context* c = m->ctx[s];
-        const uint64_t lattice_words = static_cast<uint64_t>(dims.T) * 8 * dims.RC;
-        const uint64_t raw_words = static_cast<uint64_t>(dims.T) * 4 * dims.RC;
-        c->planes.ensure(lattice_words * 4);
-        if (raw) c->raw.ensure(raw_words * 4);
-        PairTuple* tu = c->tuples_in.as<PairTuple>();
-        finalize_tuples(c, &tu->cell, &tu->key0, &tu->key1, &tu->sum, &tu->count, 5, tin[s], dims,
-                        c->planes.as<uint32_t>(), raw ? c->raw.as<uint32_t>() : nullptr, c->stream);
         uint32_t t0, t1;
         slab_rows(dims.T, N, s, t0, t1);
-        if (t1 > t0) {
+        const uint64_t rows = t1 - t0;
+        c->planes.ensure(rows * 2 * rc4 * 4 + 4);
+        if (raw) c->raw.ensure(rows * rc4 * 4 + 4);
+        PairTuple* tu = c->tuples_in.as<PairTuple>();
+        finalize_tuples(c, &tu->cell, &tu->key0, &tu->key1, &tu->sum, &tu->count, 5, tin[s], dims, t0, t1,
+                        c->planes.as<uint32_t>(), raw ? c->raw.as<uint32_t>() : nullptr, c->stream);
+        if (rows) {
             if (planes)
-                CK(cudaMemcpyAsync(planes + t0 * 2 * rc4, c->planes.as<uint32_t>() + t0 * 2 * rc4,
-                                   (t1 - t0) * 2 * rc4 * 4, cudaMemcpyDeviceToHost, c->stream));
+                CK(cudaMemcpyAsync(planes + t0 * 2 * rc4, c->planes.as<uint32_t>(), rows * 2 * rc4 * 4,
+                                   cudaMemcpyDeviceToHost, c->stream));
             if (raw)
-                CK(cudaMemcpyAsync(raw + t0 * rc4, c->raw.as<uint32_t>() + t0 * rc4, (t1 - t0) * rc4 * 4,
+                CK(cudaMemcpyAsync(raw + t0 * rc4, c->raw.as<uint32_t>(), rows * rc4 * 4,
                                    cudaMemcpyDeviceToHost, c->stream));
         }
         CK(cudaStreamSynchronize(c->stream));
@@ -712,16 +711,17 @@ int cvlg_tuples_scatter(cvlg_context* ctx, const cvlg_grid_spec* spec, uint32_t 
 }
 
 int cvlg_finalize_tuples(cvlg_context* ctx, const void* d_tuples, uint64_t n,
-                         const cvlg_grid_spec* spec, uint32_t* d_planes, uint32_t* d_raw_count,
-                         void* stream) {
+                         const cvlg_grid_spec* spec, uint32_t t0, uint32_t t1, uint32_t* d_planes,
+                         uint32_t* d_raw_count, void* stream) {
     return guard([&] {
         const Dims dims = validate_grid(spec);
         if (!ctx) fail(CVLG_E_INVALID_ARG, "context is NULL");
         if (!d_planes || (n && !d_tuples)) fail(CVLG_E_INVALID_ARG, "NULL argument");
         CK(cudaSetDevice(ctx->device));
         const PairTuple* tu = static_cast<const PairTuple*>(d_tuples);
-        finalize_tuples(ctx, &tu->cell, &tu->key0, &tu->key1, &tu->sum, &tu->count, 5, n, dims, d_planes,
-                        d_raw_count, stream ? static_cast<cudaStream_t>(stream) : ctx->stream);
+        if (t0 > t1 || t1 > dims.T) fail(CVLG_E_INVALID_ARG, "rows [t0, t1) outside the lattice");
+        finalize_tuples(ctx, &tu->cell, &tu->key0, &tu->key1, &tu->sum, &tu->count, 5, n, dims, t0, t1,
+                        d_planes, d_raw_count, stream ? static_cast<cudaStream_t>(stream) : ctx->stream);
     });
 }
 

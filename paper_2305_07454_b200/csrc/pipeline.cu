@@ -771,7 +771,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         CK(cudaEventRecord(c->ev[4], s));
         launch_finalize(c->pair_key.as<uint64_t>(), c->vals.as<uint32_t>(), n_pairs, rbits,
                         c->pair_sum.as<double>(), c->pair_cnt.as<uint32_t>(), dims.D, dims.RC,
-                        d_planes, d_raw, s);
+                        0, dims.T, d_planes, d_raw, s);
         } else {
             CK(cudaEventRecord(c->ev[4], s));
         }
@@ -1244,10 +1244,10 @@ void journey_ids(cvlg_context* c, std::vector<uint8_t>& blob, std::vector<uint64
 
 void finalize_tuples(cvlg_context* c, const uint64_t* d_cell, const uint64_t* d_key0,
                      const uint64_t* d_key1, const double* d_sum, const uint64_t* d_count,
-                     uint64_t stride, uint64_t n, const Dims& dims, uint32_t* d_planes,
-                     uint32_t* d_raw, cudaStream_t s) {
-    const uint64_t lattice_words = static_cast<uint64_t>(dims.T) * 8 * dims.RC;
-    const uint64_t raw_words = static_cast<uint64_t>(dims.T) * 4 * dims.RC;
+                     uint64_t stride, uint64_t n, const Dims& dims, uint32_t t0, uint32_t t1,
+                     uint32_t* d_planes, uint32_t* d_raw, cudaStream_t s) {
+    const uint64_t lattice_words = static_cast<uint64_t>(t1 - t0) * 8 * dims.RC;
+    const uint64_t raw_words = static_cast<uint64_t>(t1 - t0) * 4 * dims.RC;
     CK(cudaMemsetAsync(d_planes, 0, lattice_words * 4, s));
     if (d_raw) CK(cudaMemsetAsync(d_raw, 0, raw_words * 4, s));
     if (n) {
@@ -1279,7 +1279,7 @@ void finalize_tuples(cvlg_context* c, const uint64_t* d_cell, const uint64_t* d_
                          bits_for(dims.cells - 1), c->sort_tmp.p, s, d_orand, h_orand);
         launch_import_pairs(d_sum, d_count, stride, n, c->x_sum.as<double>(), c->x_cnt.as<uint32_t>(), s);
         launch_finalize(keys, vals, n, 0, c->x_sum.as<double>(), c->x_cnt.as<uint32_t>(), dims.D, dims.RC,
-                        d_planes, d_raw, s);
+                        t0, t1 - t0, d_planes, d_raw, s);
     }
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
@@ -1583,8 +1583,8 @@ int cvlg_finalize_pairs(cvlg_context* ctx, const uint64_t* d_cell, const uint64_
         if (!c) fail(CVLG_E_CUDA, "no CUDA context");
         if (!d_planes) fail(CVLG_E_INVALID_ARG, "NULL planes");
         CK(cudaSetDevice(c->device));
-        finalize_tuples(c, d_cell, d_key0, d_key1, d_sum, d_count, 1, n, dims, d_planes, d_raw_count,
-                        stream ? static_cast<cudaStream_t>(stream) : c->stream);
+        finalize_tuples(c, d_cell, d_key0, d_key1, d_sum, d_count, 1, n, dims, 0, dims.T, d_planes,
+                        d_raw_count, stream ? static_cast<cudaStream_t>(stream) : c->stream);
     });
 }
 

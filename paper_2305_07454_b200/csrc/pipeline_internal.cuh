@@ -143,11 +143,12 @@ void journey_ids(cvlg_context* c, std::vector<uint8_t>& blob, std::vector<uint64
 void merge_id_ranks(const std::vector<const std::vector<uint8_t>*>& blobs,
                     const std::vector<const std::vector<uint64_t>*>& offs,
                     std::vector<std::vector<uint32_t>>& ranks);
-// Any union of such tuples -> dense lattice (cells without tuples are zero), synchronous.
+// Any union of such tuples -> rows [t0, t1) of the dense lattice (d_planes / d_raw hold only
+// those rows; cells without tuples are zero, tuples of other rows are ignored), synchronous.
 void finalize_tuples(cvlg_context* c, const uint64_t* d_cell, const uint64_t* d_key0,
                      const uint64_t* d_key1, const double* d_sum, const uint64_t* d_count,
-                     uint64_t stride, uint64_t n, const Dims& dims, uint32_t* d_planes,
-                     uint32_t* d_raw, cudaStream_t s);
+                     uint64_t stride, uint64_t n, const Dims& dims, uint32_t t0, uint32_t t1,
+                     uint32_t* d_planes, uint32_t* d_raw, cudaStream_t s);
 
 // Byte ranges of files streamed into device memory through the context's bounded pinned ring:
 // reader threads pread chunks into ring slots in any order, next() enqueues each chunk's H2D

@@ -140,14 +140,17 @@ def _load() -> ctypes.CDLL:
                                         u64p, ctypes.POINTER(vp)]
     lib.cvlg_tuples_scatter.argtypes = [vp, ctypes.POINTER(_Grid), ctypes.c_uint32,
                                         ctypes.POINTER(vp), vp]
-    lib.cvlg_finalize_tuples.argtypes = [vp, vp, ctypes.c_uint64, ctypes.POINTER(_Grid), vp, vp,
-                                         vp]
+    lib.cvlg_finalize_tuples.argtypes = [vp, vp, ctypes.c_uint64, ctypes.POINTER(_Grid),
+                                         ctypes.c_uint32, ctypes.c_uint32, vp, vp, vp]
     lib.cvlg_slab_rows.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, u32p, u32p]
     lib.cvlg_split_manifest.argtypes = [ctypes.POINTER(ctypes.c_char_p), ctypes.c_size_t,
                                         ctypes.c_uint32, ctypes.c_uint32, u32p, u64p, u64p,
                                         ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
     lib.cvlg_partial_device.argtypes = [vp, vp, u64p, ctypes.c_size_t, ctypes.POINTER(_Grid),
                                         ctypes.POINTER(_Rules), u64p, ctypes.POINTER(_Stats), vp]
+    lib.cvlg_export_pairs.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    lib.cvlg_finalize_pairs.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_uint64,
+                                        ctypes.POINTER(_Grid), vp, vp, vp]
     return lib
 
 
@@ -163,7 +166,7 @@ EXPORTED_SYMBOLS = [
     "cvlg_run_pipeline_multi", "cvlg_route_stage", "cvlg_route_count", "cvlg_route_plan",
     "cvlg_route_scatter", "cvlg_tuples_export", "cvlg_tuples_scatter", "cvlg_finalize_tuples",
     "cvlg_slab_rows", "cvlg_split_manifest", "cvlg_partial_device", "cvlg_partial_info",
-    "cvlg_journey_ids", "cvlg_merge_id_ranks",
+    "cvlg_journey_ids", "cvlg_merge_id_ranks", "cvlg_export_pairs", "cvlg_finalize_pairs",
 ]
 
 

@@ -216,17 +216,19 @@ class FileShardedPipeline:
                                  [c * TUPLE_BYTES for c in tcount], trecv_splits, g)
         # 5. fold this rank's slab, all-gather the slabs
         n_in = trecv.numel() // TUPLE_BYTES
-        full_p = torch.empty((T, 8, R, C), dtype=torch.int32, device=dev)
-        full_r = torch.empty((T, 4, R, C), dtype=torch.int32, device=dev)
-        _c._check(_lib.cvlg_finalize_tuples(self.ctx.handle, _vp(trecv.data_ptr()) if n_in else None,
-                                            n_in, ctypes.byref(spec._c()), _vp(full_p.data_ptr()),
-                                            _vp(full_r.data_ptr()), _vp(stream)))
         rows = max(slab_rows(T, world, r)[1] - slab_rows(T, world, r)[0] for r in range(world))
         t0, t1 = slab_rows(T, world, self.rank)
+        # this rank's slab rows, planes then raw counts per row (one buffer for the gather)
         mine = torch.zeros((max(rows, 1), 12, R, C), dtype=torch.int32, device=dev)
+        slab_p = torch.empty((max(t1 - t0, 1), 8, R, C), dtype=torch.int32, device=dev)
+        slab_r = torch.empty((max(t1 - t0, 1), 4, R, C), dtype=torch.int32, device=dev)
+        _c._check(_lib.cvlg_finalize_tuples(self.ctx.handle, _vp(trecv.data_ptr()) if n_in else None,
+                                            n_in, ctypes.byref(spec._c()), t0, t1,
+                                            _vp(slab_p.data_ptr()), _vp(slab_r.data_ptr()),
+                                            _vp(stream)))
         if t1 > t0:
-            mine[: t1 - t0, :8].copy_(full_p[t0:t1])
-            mine[: t1 - t0, 8:].copy_(full_r[t0:t1])
+            mine[: t1 - t0, :8].copy_(slab_p[: t1 - t0])
+            mine[: t1 - t0, 8:].copy_(slab_r[: t1 - t0])
         gathered = self._all_gather(mine)
         for r in range(world):
             a, b = slab_rows(T, world, r)
