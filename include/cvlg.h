@@ -269,6 +269,14 @@ int cvlg_last_stage_ms(cvlg_context* ctx, float* ms, int n);
  * cvlg_run_pipeline_device (the device-resident measurement of the same input). */
 int cvlg_context_input(cvlg_context* ctx, const uint8_t** d_csv, uint64_t* n_bytes);
 
+/* Test hook: the decode output of the context's last run, one entry per data line in provenance
+ * order (slot order; "\r\n" lines hold an inert slot): epoch seconds, speed (f64), cell code
+ * (grid.cuh: cell index, or 0x7FFFFFFB rejected by parse, 0x7FFFFFFF OutOfGrid, 0x7FFFFFFE
+ * SpeedCeiling, 0x7FFFFFFC off-grid with require_in_grid = false; bit 31 = run head) and the
+ * line's byte offset in the concatenated input. *n = number of entries, at most cap written. */
+int cvlg_debug_slots(cvlg_context* ctx, int64_t* ts, double* speed, uint32_t* code, uint64_t* loff,
+                     uint64_t cap, uint64_t* n);
+
 /* Pins / unpins caller memory for faster H2D (cudaHostRegister). */
 int cvlg_pin_host(void* ptr, size_t bytes);
 int cvlg_unpin_host(void* ptr);

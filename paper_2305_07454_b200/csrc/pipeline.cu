@@ -348,6 +348,8 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
     const uint64_t n_parsed = hs[kStParsed];
     const uint64_t hs_inert = hs[kStInert];
     c->last_slots = 0;  // the slot space is sparse (see cvlg_debug_slots)
+    c->dbg_tiles = n_tiles;
+    c->dbg_lines = N + hs_inert;
     const uint64_t transitions = hs[kStGTransitions];
     const uint64_t H = hs[kStHeads];
     // Order keys use the biased epoch (ts - INT64_MIN: signed order as unsigned); the radix sort
@@ -1594,13 +1596,32 @@ int cvlg_debug_slots(cvlg_context* ctx, int64_t* ts, double* speed, uint32_t* co
         cvlg_context* c = ctx ? ctx : default_context();
         if (!c) fail(CVLG_E_CUDA, "no CUDA context");
         CK(cudaSetDevice(c->device));
-        const uint64_t m = std::min<uint64_t>(cap, c->last_slots);
-        if (n) *n = c->last_slots;
-        if (!m) return;
-        if (ts) CK(cudaMemcpy(ts, c->ts.p, m * 8, cudaMemcpyDeviceToHost));
-        if (speed) CK(cudaMemcpy(speed, c->speed.p, m * 8, cudaMemcpyDeviceToHost));
-        if (code) CK(cudaMemcpy(code, c->code.p, m * 4, cudaMemcpyDeviceToHost));
-        if (loff) CK(cudaMemcpy(loff, c->loff.p, m * 8, cudaMemcpyDeviceToHost));
+        CK(cudaStreamSynchronize(c->stream));
+        if (c->last_slots) {  // dense (full-sort path): slots 0..NS-1 in provenance order
+            const uint64_t m = std::min<uint64_t>(cap, c->last_slots);
+            if (n) *n = c->last_slots;
+            if (!m) return;
+            if (ts) CK(cudaMemcpy(ts, c->ts.p, m * 8, cudaMemcpyDeviceToHost));
+            if (speed) CK(cudaMemcpy(speed, c->speed.p, m * 8, cudaMemcpyDeviceToHost));
+            if (code) CK(cudaMemcpy(code, c->code.p, m * 4, cudaMemcpyDeviceToHost));
+            if (loff) CK(cudaMemcpy(loff, c->loff.p, m * 8, cudaMemcpyDeviceToHost));
+            return;
+        }
+        // sparse (run-merge path): tile t's lines are slots [tiles[t].x, + tiles[t].y)
+        if (n) *n = c->dbg_lines;
+        if (!cap || !c->dbg_tiles) return;
+        std::vector<uint4> tiles(c->dbg_tiles);
+        CK(cudaMemcpy(tiles.data(), c->tiles.p, c->dbg_tiles * 16, cudaMemcpyDeviceToHost));
+        uint64_t at = 0;
+        for (const uint4& t : tiles) {
+            const uint64_t k = std::min<uint64_t>(t.y, cap > at ? cap - at : 0);
+            if (!k) continue;
+            if (ts) CK(cudaMemcpy(ts + at, c->ts.as<int64_t>() + t.x, k * 8, cudaMemcpyDeviceToHost));
+            if (speed) CK(cudaMemcpy(speed + at, c->speed.as<double>() + t.x, k * 8, cudaMemcpyDeviceToHost));
+            if (code) CK(cudaMemcpy(code + at, c->code.as<uint32_t>() + t.x, k * 4, cudaMemcpyDeviceToHost));
+            if (loff) CK(cudaMemcpy(loff + at, c->loff.as<uint64_t>() + t.x, k * 8, cudaMemcpyDeviceToHost));
+            at += k;
+        }
     });
 }
 

@@ -104,6 +104,7 @@ struct cvlg_context {
     std::vector<cudaEvent_t> ring_events;  // one per ring slot: its last H2D copy
     // last cvlg_partial_device run: pairs kept in pair_key/pair_sum/pair_cnt
     uint64_t part_pairs = 0, part_J = 0, last_slots = 0;
+    uint64_t dbg_tiles = 0, dbg_lines = 0;  // decode geometry of the last run (cvlg_debug_slots)
     uint64_t input_bytes = 0;  // bytes of c->csv staged by the last host/file run
     const uint8_t* csv_in = nullptr;  // CSV bytes of the last run (long journey ids point into it)
     cvlg::DevBuf r_grank;             // global journey ranks (multi-GPU combine with long ids)
