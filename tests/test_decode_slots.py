@@ -83,7 +83,8 @@ def check(ref, paths, spec):
         assert int(ts[i]) == rec.epoch_sec, (line, int(ts[i]), rec.epoch_sec)
         assert struct.pack("<d", float(sp[i])) == struct.pack("<d", rec.speed), (line, sp[i], rec.speed)
         assert got == expected_code(ref, spec, rec), (line, hex(got), hex(expected_code(ref, spec, rec)))
-    rows = sum(1 for p in paths for l in Path(p).read_bytes().split(b"\n")[1:] if l.rstrip(b"\r"))
+    rows = sum(1 for p in paths for l in Path(p).read_bytes().split(b"\n")[1:]
+               if (l[:-1] if l.endswith(b"\r") else l))  # one '\r' stripped (ingest.cpp:208)
     assert n_lines == rows
     ctx.close()
     return n_lines
