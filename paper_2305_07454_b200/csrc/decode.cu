@@ -83,23 +83,37 @@ struct LineOut {
 constexpr uint32_t kNoMinute = 0xFFFFFFFFu;
 constexpr uint8_t kNeedGeneral = 255;
 
-// Per-thread fast-path state carried across lines: the last validated date, per numeric column the
-// decimal point position of the previous line, and the comma layout of the previous line's fixed
-// prefix (journey id, timestamp, latitude, longitude[, postal code]): lines of a trace share it, so
-// the first K comma positions usually come from the cache after one 64-bit compare.
+// Per-thread fast-path state carried across lines: the last validated date and, per numeric
+// column, the decimal point position of the previous line.
 struct FastState {
     DateCache dc;
-    uint32_t qc = 0xFFFFu;                // 4-bit point positions per number column (15: none)
-                                          // | (c4 | last << 8) << 16 of the comma prefix
-    uint32_t cmask_lo = 0, cmask_hi = 0;  // bits of the cached prefix commas (line-relative)
-    uint32_t cpos_a = 0;                  // prefix comma positions c0..c3 (bytes)
+    int q[4] = {-1, -1, -1, -1};
 };
 static_assert(sizeof(FastState) % 8 == 4, "odd word stride: conflict-free per-thread state");
 
-// First 7 comma positions of a line (relative to its start; len when absent) from its 96-bit comma
-// window. Out of line: runs only when the cached prefix layout does not match.
-__device__ __noinline__ void comma_positions(uint32_t m0, uint32_t m1, uint32_t m2, uint32_t len,
-                                             uint32_t* cpos) {
+// Fast path of parse_record_impl for a line [p, e) (tile-relative) entirely staged in shared
+// memory whose header is canonical: journey, timestamp, latitude, longitude as fields 0..3, then
+// speed, heading as 5, 6 (`postal` = 1: any column at 4) or 4, 5. Returns kAccepted or
+// kRangeViolation, or kNeedGeneral whenever the general restatement has to decide.
+__device__ __forceinline__ uint8_t fast_parse(const uint8_t* __restrict__ buf, const uint32_t* __restrict__ cm,
+                                              uint32_t p, uint32_t e, int postal, FastState& fs, LineOut& o) {
+    const uint32_t len = e - p;
+    if (len > 95) return kNeedGeneral;
+    // 96-bit comma window starting at bit p
+    const uint32_t wi = p >> 5, sh = p & 31;
+    const uint32_t a = cm[wi], b = cm[wi + 1], c = cm[wi + 2], d = cm[wi + 3];
+    uint32_t m0 = __funnelshift_r(a, b, sh), m1 = __funnelshift_r(b, c, sh), m2 = __funnelshift_r(c, d, sh);
+    if (len < 32) {
+        m0 &= (1u << len) - 1u;
+        m1 = m2 = 0;
+    } else if (len < 64) {
+        m1 &= (1u << (len - 32)) - 1u;
+        m2 = 0;
+    } else {
+        m2 &= (1u << (len - 64)) - 1u;
+    }
+    // first 7 comma positions (relative to p); len when absent
+    uint32_t cpos[7];
 #pragma unroll
     for (int k = 0; k < 7; ++k) {
         uint32_t pos = len;
@@ -115,86 +129,6 @@ __device__ __noinline__ void comma_positions(uint32_t m0, uint32_t m1, uint32_t 
         }
         cpos[k] = pos;
     }
-}
-
-// next set bit of a 96-bit mask (lo 64 + hi 32), cleared; len when none
-__device__ __forceinline__ uint32_t pop96(uint64_t& lo, uint32_t& hi, uint32_t len) {
-    if (lo) {
-        const uint32_t pos = __ffsll(static_cast<long long>(lo)) - 1;
-        lo &= lo - 1;
-        return pos;
-    }
-    if (hi) {
-        const uint32_t pos = 64 + __ffs(hi) - 1;
-        hi &= hi - 1;
-        return pos;
-    }
-    return len;
-}
-
-// Fast path of parse_record_impl for a line [p, e) (tile-relative) entirely staged in shared
-// memory whose header is canonical: journey, timestamp, latitude, longitude as fields 0..3, then
-// speed, heading as 5, 6 (`postal` = 1: any column at 4) or 4, 5. Returns kAccepted or
-// kRangeViolation, or kNeedGeneral whenever the general restatement has to decide.
-__device__ __forceinline__ uint8_t fast_parse(const uint8_t* __restrict__ buf, const uint32_t* __restrict__ cm,
-                                              uint32_t p, uint32_t e, int postal, FastState& fs, LineOut& o) {
-    const uint32_t len = e - p;
-    if (len > 95) return kNeedGeneral;
-    // 96-bit comma window starting at bit p, bits >= len cleared
-    const uint32_t wi = p >> 5, sh = p & 31;
-    const uint32_t a = cm[wi], b = cm[wi + 1], c = cm[wi + 2], d = cm[wi + 3];
-    uint32_t m0 = __funnelshift_r(a, b, sh), m1 = __funnelshift_r(b, c, sh), m2 = __funnelshift_r(c, d, sh);
-    if (len < 32) {
-        m0 &= (1u << len) - 1u;
-        m1 = m2 = 0;
-    } else if (len < 64) {
-        m1 &= (1u << (len - 32)) - 1u;
-        m2 = 0;
-    } else {
-        m2 &= (1u << (len - 64)) - 1u;
-    }
-    // the K prefix commas: the cached layout when this line has exactly those commas up to the
-    // last of them, else extracted (and cached for the next line)
-    uint64_t lo = (static_cast<uint64_t>(m1) << 32) | m0;
-    uint32_t hi = m2;
-    const uint32_t K = postal ? 5u : 4u;
-    const uint64_t pm = (static_cast<uint64_t>(fs.cmask_hi) << 32) | fs.cmask_lo;
-    const uint32_t qc = fs.qc;
-    const uint32_t pa = fs.cpos_a, pb = qc >> 16;
-    const uint32_t plast = pb >> 8;  // position of the K-th cached comma (< 63)
-    const uint64_t below = (2ull << plast) - 1ull;
-    // (the K-th cached comma is c4 for a cache made by a line with a postal column, else c3)
-    const uint32_t kth = postal ? (pb & 0xFF) : (pa >> 24);
-    uint32_t cpos[7];
-    uint32_t qc_new = qc;  // == fs.qc throughout
-    if (pm != 0 && plast == kth && (lo & below) == pm) {
-        cpos[0] = pa & 0xFF;
-        cpos[1] = (pa >> 8) & 0xFF;
-        cpos[2] = (pa >> 16) & 0xFF;
-        cpos[3] = pa >> 24;
-        lo &= ~below;
-        if (postal) {
-            cpos[4] = pb & 0xFF;
-            cpos[5] = pop96(lo, hi, len);
-            cpos[6] = pop96(lo, hi, len);
-        } else {
-            cpos[4] = pop96(lo, hi, len);
-            cpos[5] = pop96(lo, hi, len);
-            cpos[6] = len;
-        }
-    } else {
-        comma_positions(m0, m1, m2, len, cpos);
-        const uint32_t last = cpos[K - 1];
-        if (last < 63) {
-            const uint64_t bl = (2ull << last) - 1ull;
-            const uint64_t pmask = ((static_cast<uint64_t>(m1) << 32) | m0) & bl;
-            fs.cmask_lo = static_cast<uint32_t>(pmask);
-            fs.cmask_hi = static_cast<uint32_t>(pmask >> 32);
-            fs.cpos_a = cpos[0] | (cpos[1] << 8) | (cpos[2] << 16) | (cpos[3] << 24);
-            qc_new = (qc & 0xFFFFu) | (((postal ? cpos[4] : 0u) | (last << 8)) << 16);
-            fs.qc = qc_new;  // the prefix cache words change together
-        }
-    }
     const uint32_t fe_id = cpos[0];
     const uint32_t fb_ts = cpos[0] + 1, fe_ts = cpos[1];
     const uint32_t fb_la = cpos[1] + 1, fe_la = cpos[2];
@@ -208,23 +142,13 @@ __device__ __forceinline__ uint8_t fast_parse(const uint8_t* __restrict__ buf, c
         return kNeedGeneral;
     const uint32_t base = p + kPre;  // buffer offset of the line
     const uint32_t* w = reinterpret_cast<const uint32_t*>(buf);
-    // trim bytes (' ', '\t', '\r') are all <= 0x20: a conservative test, general decides
-    if (buf[base] <= 0x20 || buf[base + fe_id - 1] <= 0x20) return kNeedGeneral;
+    if (is_trim(buf[base]) || is_trim(buf[base + fe_id - 1])) return kNeedGeneral;
     if (fe_ts - fb_ts != 19 || !fast_timestamp(w, base + fb_ts, fs.dc, o.ts, o.minute)) return kNeedGeneral;
-    auto qget = [&](int k) {
-        const int v = static_cast<int>((qc_new >> (4 * k)) & 0xFu);
-        return v == 15 ? -1 : v;
-    };
-    int q0 = qget(0), q1 = qget(1), q2 = qget(2), q3 = qget(3);
-    const bool ok = fast_number(w, buf, base + fb_la, base + fe_la, q0, o.lat) &&
-                    fast_number(w, buf, base + fb_lo, base + fe_lo, q1, o.lon) &&
-                    fast_number(w, buf, base + fb_sp, base + fe_sp, q2, o.speed) &&
-                    fast_number(w, buf, base + fb_hd, base + fe_hd, q3, o.heading);
-    const uint32_t qn = (qc_new & 0xFFFF0000u) | (static_cast<uint32_t>(q0) & 0xFu) |
-                        ((static_cast<uint32_t>(q1) & 0xFu) << 4) | ((static_cast<uint32_t>(q2) & 0xFu) << 8) |
-                        ((static_cast<uint32_t>(q3) & 0xFu) << 12);
-    if (qn != qc_new) fs.qc = qn;
-    if (!ok) return kNeedGeneral;
+    if (!fast_number(w, buf, base + fb_la, base + fe_la, fs.q[0], o.lat) ||
+        !fast_number(w, buf, base + fb_lo, base + fe_lo, fs.q[1], o.lon) ||
+        !fast_number(w, buf, base + fb_sp, base + fe_sp, fs.q[2], o.speed) ||
+        !fast_number(w, buf, base + fb_hd, base + fe_hd, fs.q[3], o.heading))
+        return kNeedGeneral;
     if (o.heading == 360.0) o.heading = 0.0;
     o.id_rel = p;
     o.id_len = fe_id;

@@ -142,8 +142,8 @@ CVLG_HD double div_pow10(double x, int k) {
 //   long path (<= 11 digits): bytes after the point move down one position ('0' enters at 11),
 //     so the three words read V = 10 M; x = V / 10^(F+1). Without a point nothing moves.
 // Both divide an exact integer by an exact power of ten with correct rounding (div_pow10).
-CVLG_HD_NOINLINE bool fast_number_full(const uint32_t* w, const uint8_t* buf, uint32_t b, uint32_t e,
-                                        int& qguess, double& v) {
+CVLG_HD bool fast_number(const uint32_t* w, const uint8_t* buf, uint32_t b, uint32_t e, int& qguess,
+                         double& v) {
     const uint32_t n = e - b;
     if (n - 1u > 11u) return false;  // 1..12 bytes
     const bool neg = buf[b] == '-';
@@ -192,40 +192,6 @@ CVLG_HD_NOINLINE bool fast_number_full(const uint32_t* w, const uint8_t* buf, ui
     const double x = div_pow10(static_cast<double>(V), 12 - qe);  // V exact: < 10^12
     v = neg ? -x : x;
     return true;
-}
-
-// fast_number: the common case inline — the point at this column's cached window position q
-// (4..11: the field's last 8 bytes), at most 8 digits — and everything else (a new point position,
-// longer numbers, no point) out of line in fast_number_full, so the rare branches are real branches
-// instead of predicated code every line pays for. Same results as fast_number_full.
-CVLG_HD bool fast_number(const uint32_t* w, const uint8_t* buf, uint32_t b, uint32_t e, int& qguess,
-                         double& v) {
-    const int q = qguess;
-    const uint32_t n = e - b;
-    const uint32_t o = e - 12;
-    if (q >= 4 && q <= 11 && n - 2u <= 8u && buf[o + q] == '.') {
-        const bool neg = buf[b] == '-';
-        const int s = 12 - static_cast<int>(n) + (neg ? 1 : 0);
-        const int D = static_cast<int>(n) - 1 - (neg ? 1 : 0);
-        if (s <= q && D >= 1 && D <= 8) {
-            const uint32_t i = o >> 2, sh = (o & 3) * 8;
-            const uint32_t x0 = w[i], x1 = w[i + 1], x2 = w[i + 2], x3 = w[i + 3];
-            const uint32_t a0 = fs_r(x0, x1, sh), a1 = fs_r(x1, x2, sh), a2 = fs_r(x2, x3, sh);
-            const uint64_t a = (static_cast<uint64_t>(a2) << 32) | a1;
-            const uint64_t sft = (a << 8) | (a0 >> 24);  // every byte takes the byte below it
-            const uint64_t keep_hi = q >= 11 ? 0ull : (~0ull << (8 * (q - 3)));  // positions > q stay
-            uint64_t r = (a & keep_hi) | (sft & ~keep_hi);
-            const uint64_t dig = ~0ull << (8 * (8 - D));  // digits occupy [12 - D, 12)
-            r = (r & dig) | (0x3030303030303030ull & ~dig);
-            const uint32_t r1 = static_cast<uint32_t>(r), r2 = static_cast<uint32_t>(r >> 32);
-            if (digits3(r1, r2, 0x30303030u)) {
-                const double x = div_pow10(static_cast<double>(swar4(r1) * 10000u + swar4(r2)), 11 - q);
-                v = neg ? -x : x;
-                return true;
-            }
-        }
-    }
-    return fast_number_full(w, buf, b, e, qguess, v);
 }
 
 // '\n' and ',' flags of 32 staged bytes (words x[0..7], little endian) -> two 32-bit masks, bit i

@@ -85,17 +85,13 @@ CVLG_HD uint32_t extent_bins(double lo, double hi, double step) {
 // exact quotient and snap_to_integer (tolerance 1e-9 * max(1, |r|)) leaves the quotient alone:
 // floor(qa) is the exact bin. Otherwise (near a bin edge, or huge quotients) the exact division
 // and snap of grid.cpp decide.
-CVLG_HD_NOINLINE double snapped_floor_exact(double d, double step) {  // rare: out of line
-    return floor(snap_to_integer(d_div(d, step)));
-}
-
 CVLG_HD double snapped_floor(double d, double step, double inv) {
     const double qa = d_mul(d, inv);
     const double r = d_rint(qa);
     const double ar = d_abs(r);
     const double m = ar > 1.0 ? ar : 1.0;
     if (qa < 1e6 && d_abs(d_sub(qa, r)) > d_mul(4e-9, m)) return floor(qa);
-    return snapped_floor_exact(d, step);
+    return floor(snap_to_integer(d_div(d, step)));
 }
 
 // precondition: lo <= x <= hi (checked by the caller)

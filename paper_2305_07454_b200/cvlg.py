@@ -23,6 +23,8 @@ import numpy as np
 
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "lib" / "libcvlg.so"
+if os.environ.get("CVLG_LIB_VARIANT"):  # A/B builds of the same sources (tools/, never the default)
+    LIB_PATH = _HERE / "lib" / f"libcvlg.{os.environ['CVLG_LIB_VARIANT']}.so"
 
 ERR_NAMES = [
     "MissingRoot", "BadConfig", "BadGrid", "ZeroPartitions", "OutOfBounds",
