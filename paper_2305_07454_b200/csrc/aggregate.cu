@@ -753,30 +753,60 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
             }
         }
         __syncwarp();
-        // ---- sequential walk of this lane's chunk ---------------------------------------------
-        for (uint32_t k = 0; k < avail; ++k) {
-            const uint32_t code = s_code[warp][lane][k] & kCodeMask;
-            if (kSlow) {
-                const uint32_t slot = s_slot[warp][lane][k];
-                const int64_t t = s_ts[warp][lane][kSlow ? k : 0];
-                if (have_prev && t == prev_ts) {  // duplicate key: dropped before filtering
-                    ++c_dup;
-                    if (!payload_equal(P, P.loff[slot], P.loff[surv])) ++c_conf;
-                    continue;
+        // ---- pass 1: this lane's chunk in (rank, ts) order: dedup (slow path), filters, and the
+        // positions where the accepted records' cell changes (segment starts) -------------------
+        uint32_t use = 0, segs = 0;
+        {
+            uint32_t prev = cur_g;
+            for (uint32_t k = 0; k < avail; ++k) {
+                const uint32_t code = s_code[warp][lane][k] & kCodeMask;
+                if (kSlow) {
+                    const uint32_t slot = s_slot[warp][lane][k];
+                    const int64_t t = s_ts[warp][lane][kSlow ? k : 0];
+                    if (have_prev && t == prev_ts) {  // duplicate key: dropped before filtering
+                        ++c_dup;
+                        if (!payload_equal(P, P.loff[slot], P.loff[surv])) ++c_conf;
+                        continue;
+                    }
+                    have_prev = true;
+                    prev_ts = t;
+                    surv = slot;
                 }
-                have_prev = true;
-                prev_ts = t;
-                surv = slot;
+                if (code >= kCodeFirstSpecial) {
+                    if (code == kCodeOutOfGrid) ++c_oog;
+                    else if (code == kCodeSpeedCeiling) ++c_spd;
+                    else if (code == kCodeMissingField) ++c_miss;
+                    else if (code == kCodeUnbinnable) ++c_unb;
+                    continue;  // kCodeRejected: counted by decode
+                }
+                ++c_acc;
+                use |= 1u << k;
+                if (code != prev) {
+                    segs |= 1u << k;
+                    prev = code;
+                }
             }
-            if (code >= kCodeFirstSpecial) {
-                if (code == kCodeOutOfGrid) ++c_oog;
-                else if (code == kCodeSpeedCeiling) ++c_spd;
-                else if (code == kCodeMissingField) ++c_miss;
-                else if (code == kCodeUnbinnable) ++c_unb;
-                continue;  // kCodeRejected: counted by decode
+        }
+        // ---- pass 2: the left fold (aggregate.cpp:349-356). Records before the first segment
+        // start continue the current cell; then one warp-wide round per segment index, so every
+        // lane's cell switch of that round runs together instead of the warp serializing on each
+        // record where any lane switches.
+        auto accumulate = [&](uint32_t from, uint32_t to) {
+            uint32_t m = use & ((to >= 32 ? 0xFFFFFFFFu : ((1u << to) - 1u)) & ~((1u << from) - 1u));
+            while (m) {
+                const uint32_t k = __ffs(m) - 1;
+                m &= m - 1;
+                cur_sum = __dadd_rn(cur_sum, s_speed[warp][lane][k]);  // aggregate.cpp:354
+                ++cur_cnt;
             }
-            ++c_acc;
-            if (code != cur_g) {
+        };
+        accumulate(0, segs ? static_cast<uint32_t>(__ffs(segs) - 1) : avail);
+        while (__any_sync(0xFFFFFFFFu, segs != 0)) {
+            if (segs) {
+                const uint32_t k0 = __ffs(segs) - 1;
+                segs &= segs - 1;
+                const uint32_t k1 = segs ? static_cast<uint32_t>(__ffs(segs) - 1) : avail;
+                const uint32_t code = s_code[warp][lane][k0] & kCodeMask;
                 if (cur_g != kNone) {  // park the current subtotal in its table entry
                     t_s[warp][cur][lane] = cur_sum;
                     t_c[warp][cur][lane] = cur_cnt;
@@ -844,9 +874,8 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
                 }
                 cur = e;
                 cur_g = code;
+                accumulate(k0, k1);
             }
-            cur_sum = __dadd_rn(cur_sum, s_speed[warp][lane][k]);  // aggregate.cpp:354
-            ++cur_cnt;
         }
         __syncwarp();
         // ---- flush closed windows of nearly full tables, one pair-list reservation per warp ------
