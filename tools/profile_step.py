@@ -26,7 +26,8 @@ if a.days > 1:  # c5 shape: day k uses seed 1 + k and date + k; its shards follo
         d = (datetime.date(2021, 5, 9) + datetime.timedelta(days=k)).isoformat()
         b, o, r = cvlg.synth_day(seed=1 + k, journeys=a.journeys, shards=a.shards,
                                  mean_duration=500.0, day=d)
-        offs.extend(offs[-1] + int(x) for x in o[1:])
+        b0 = offs[-1]
+        offs.extend(b0 + int(x) for x in o[1:])
         blobs.append(b)
         rows += r
     blob = np.concatenate(blobs)
