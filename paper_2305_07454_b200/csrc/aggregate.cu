@@ -397,13 +397,12 @@ __global__ void run_keys_kernel(const uint32_t* hslot, const uint32_t* hrank, ui
     for (uint64_t i = hslot[h]; i < end; ++i) put(i, r);
 }
 
-__global__ void slot_jstart_kernel(const uint32_t* perm, const uint32_t* srank, uint64_t n,
-                                   uint32_t reject_rank, uint32_t* jstart) {
+// journey starts from the sorted keys: the rank is key >> rank_shift (no gather through perm)
+__global__ void slot_jstart_kernel(const uint64_t* keys, int rank_shift, uint64_t n, uint32_t* jstart) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (i >= n) return;
-    const uint32_t r = srank[perm[i]];
-    if (i == 0 || srank[perm[i - 1]] != r) jstart[r] = static_cast<uint32_t>(i);
-    (void)reject_rank;  // jstart[reject_rank] marks the end of the last journey
+    const uint32_t r = static_cast<uint32_t>(keys[i] >> rank_shift);
+    if (i == 0 || static_cast<uint32_t>(keys[i - 1] >> rank_shift) != r) jstart[r] = static_cast<uint32_t>(i);
 }
 
 // ---- payload re-parse for the duplicate-conflict check (aggregate.cpp:286) -------------------
@@ -739,8 +738,13 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
                 const int src = it * kPer + lane / kCh;
                 const uint32_t a = __shfl_sync(0xFFFFFFFFu, avail, src);
                 const bool in = static_cast<uint32_t>(k) < a;
-                cv[it] = in ? __ldg(&P.code[slv[it]]) : 0u;
-                sv[it] = in ? __ldg(&P.speed[slv[it]]) : 0.0;
+                if (P.code_s) {  // sorted columns: sequential loads
+                    cv[it] = in ? __ldg(&P.code_s[p0s[it] + k]) : 0u;
+                    sv[it] = in ? __ldg(&P.speed_s[p0s[it] + k]) : 0.0;
+                } else {
+                    cv[it] = in ? __ldg(&P.code[slv[it]]) : 0u;
+                    sv[it] = in ? __ldg(&P.speed[slv[it]]) : 0.0;
+                }
                 tv[it] = !in ? 0 : P.skey ? static_cast<long long>(P.skey[p0s[it] + k]) : __ldg(&P.ts[slv[it]]);
             }
 #pragma unroll
@@ -933,6 +937,28 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
         const unsigned long long s = warp_sum(vals[k]);
         if (lane == 0 && s) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[idx[k]]), s);
     }
+}
+
+// slow path: the fold's columns in sorted order, one pass with every load of a thread in flight
+__global__ void gather_sorted_kernel(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ code,
+                                     const double* __restrict__ speed, uint64_t n, uint32_t* code_out,
+                                     double* speed_out) {
+    const uint64_t i0 = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) * 4;
+    uint32_t p[4], c[4];
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) p[u] = i0 + u < n ? __ldg(&perm[i0 + u]) : 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        c[u] = i0 + u < n ? __ldg(&code[p[u]]) : 0u;
+        v[u] = i0 + u < n ? __ldg(&speed[p[u]]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        if (i0 + u < n) {
+            code_out[i0 + u] = c[u];
+            speed_out[i0 + u] = v[u];
+        }
 }
 
 // fast path: the runs in perm order as (start, end) slot pairs (one load per run switch)
@@ -1182,9 +1208,10 @@ void launch_slot_keys(const uint32_t* hslot, const uint32_t* hrank, uint64_t n_h
     count_launch();
 }
 
-void launch_slot_jstart(const uint32_t* perm, const uint32_t* srank, uint64_t n,
-                        uint32_t reject_rank, uint32_t* jstart, cudaStream_t s) {
-    slot_jstart_kernel<<<grid_for(n, 256), 256, 0, s>>>(perm, srank, n, reject_rank, jstart);
+void launch_slot_jstart(const uint64_t* keys, int rank_shift, uint64_t n, uint32_t* jstart,
+                        cudaStream_t s) {
+    if (!n) return;
+    slot_jstart_kernel<<<grid_for(n, 256), 256, 0, s>>>(keys, rank_shift, n, jstart);
     count_launch();
 }
 
@@ -1303,6 +1330,13 @@ void launch_import_pairs(const double* sum, const uint64_t* cnt, uint64_t stride
                          double* psum, uint32_t* pcnt, cudaStream_t s) {
     if (!n) return;
     import_pairs_kernel<<<grid_for(n, 256), 256, 0, s>>>(sum, cnt, stride, n, psum, pcnt);
+    count_launch();
+}
+
+void launch_gather_sorted(const uint32_t* perm, const uint32_t* code, const double* speed, uint64_t n,
+                          uint32_t* code_out, double* speed_out, cudaStream_t s) {
+    if (!n) return;
+    gather_sorted_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(perm, code, speed, n, code_out, speed_out);
     count_launch();
 }
 

@@ -226,7 +226,10 @@ constexpr int kStage = kPre + kTile + kHalo;
 constexpr int kStageAlloc = kStage + 32;  // word over-read padding, keeps 16 B alignment
 constexpr int kWords = (kTile + kHalo) / 32;
 constexpr int kMaxShardsInTile = 32;
-constexpr int kDecodeCtasPerSm = 4 * 16384 / kTile;  // 1024 threads per SM at 64 registers
+#ifndef CVLG_DECODE_MINB
+#define CVLG_DECODE_MINB (4 * 16384 / kTile)
+#endif
+constexpr int kDecodeCtasPerSm = CVLG_DECODE_MINB;  // 1024 threads per SM at 64 registers
 constexpr int kNW = kDecodeThreads / 32;
 constexpr int kRounds = (kLineCap + kDecodeThreads - 1) / kDecodeThreads;
 constexpr int kHeadWords = kRounds * kNW;  // one ballot word per (round, warp)

@@ -375,7 +375,8 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         uint32_t* d_invalid = c->scal.as<uint32_t>() + 12;
         // dictionary capacity: 2x the distinct ids, which are at most H (and usually far fewer:
         // every run head inserts its journey); start at <= 8M entries, grow if a probe chain fills
-        uint64_t dcap = pow2_at_least(2 * std::min<uint64_t>(H, 1ull << 22));
+        // (<= 2M entries = 32 MB first: L2-resident probes; row-shuffled input has a head per line)
+        uint64_t dcap = pow2_at_least(2 * std::min<uint64_t>(H, 1ull << 20));
         const uint64_t flag_n = std::max<uint64_t>({pow2_at_least(2 * H), n_tiles + 1, N + 1});
         c->flags.ensure(flag_n * 4 + 16);
         c->pos.ensure(flag_n * 4 + 16);
@@ -591,8 +592,8 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
                                  rbits, c->sort_tmp.p, s, d_orand, h_orand);
             }
             c->slow_key_ts = mode == 0;  // keys hold (rank, ts - lo): the fold's dedup reads them
-            launch_slot_jstart(c->vals.as<uint32_t>(), c->srank.as<uint32_t>(), NS,
-                               static_cast<uint32_t>(J), jstart, s);
+            // the sorted keys hold (rank << key_tsbits | ts) (mode 0) or the rank (mode 1)
+            launch_slot_jstart(c->keys.as<uint64_t>(), mode == 0 ? key_tsbits : 0, NS, jstart, s);
             set_u32_kernel<<<1, 1, 0, s>>>(jstart + J, static_cast<uint32_t>(n_parsed));
             count_launch();
         }
@@ -623,6 +624,17 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         F.code = c->code.as<uint32_t>();
         F.loff = c->loff.as<uint64_t>();
         F.skey = (slow && c->slow_key_ts) ? c->keys.as<uint64_t>() : nullptr;
+        F.code_s = nullptr;
+        F.speed_s = nullptr;
+        if (slow && !feat) {  // sorted copies of code / speed: the fold reads them sequentially
+            const uint64_t NSS = c->last_slots;
+            c->code2.ensure(NSS * 4 + 4);
+            c->speed2.ensure(NSS * 8 + 8);
+            launch_gather_sorted(c->vals.as<uint32_t>(), c->code.as<uint32_t>(), c->speed.as<double>(), NSS,
+                                 c->code2.as<uint32_t>(), c->speed2.as<double>(), s);
+            F.code_s = c->code2.as<uint32_t>();
+            F.speed_s = c->speed2.as<double>();
+        }
         F.pair_key = c->pair_key.as<uint64_t>();
         F.pair_sum = c->pair_sum.as<double>();
         F.pair_cnt = c->pair_cnt.as<uint32_t>();
