@@ -42,8 +42,6 @@ struct FoldParams {
     // slow path: the sorted (rank << span | ts - lo) keys, aligned with perm (nullable): equal keys
     // within a journey = equal timestamps, read in order instead of gathering ts per slot
     const uint64_t* skey;
-    const uint32_t* code_s;  // slow path: code / speed already in sorted (perm) order, or null
-    const double* speed_s;
     // (cell, journey) subtotals out: key = cell << rank_bits | rank
     uint64_t* pair_key;
     double* pair_sum;
@@ -161,9 +159,6 @@ void launch_slot_keys(const uint32_t* hslot, const uint32_t* hrank, uint64_t n_h
 void launch_slot_jstart(const uint64_t* keys, int rank_shift, uint64_t n, uint32_t* jstart,
                         cudaStream_t s);
 void launch_fold(const FoldParams& p, bool slow, cudaStream_t s);
-// code_out[i] = code[perm[i]], speed_out[i] = speed[perm[i]] (the slow path's sorted columns)
-void launch_gather_sorted(const uint32_t* perm, const uint32_t* code, const double* speed, uint64_t n,
-                          uint32_t* code_out, double* speed_out, cudaStream_t s);
 // CTAs of the (persistent) fold launch: the directory holds one row per lane of this grid
 unsigned fold_grid(uint64_t n_journeys, bool slow);
 // moves the live pairs of [0, n) over the `dead` vacated slots: the first n - dead stay live

@@ -738,13 +738,8 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
                 const int src = it * kPer + lane / kCh;
                 const uint32_t a = __shfl_sync(0xFFFFFFFFu, avail, src);
                 const bool in = static_cast<uint32_t>(k) < a;
-                if (P.code_s) {  // sorted columns: sequential loads
-                    cv[it] = in ? __ldg(&P.code_s[p0s[it] + k]) : 0u;
-                    sv[it] = in ? __ldg(&P.speed_s[p0s[it] + k]) : 0.0;
-                } else {
-                    cv[it] = in ? __ldg(&P.code[slv[it]]) : 0u;
-                    sv[it] = in ? __ldg(&P.speed[slv[it]]) : 0.0;
-                }
+                cv[it] = in ? __ldg(&P.code[slv[it]]) : 0u;
+                sv[it] = in ? __ldg(&P.speed[slv[it]]) : 0.0;
                 tv[it] = !in ? 0 : P.skey ? static_cast<long long>(P.skey[p0s[it] + k]) : __ldg(&P.ts[slv[it]]);
             }
 #pragma unroll
@@ -937,28 +932,6 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
         const unsigned long long s = warp_sum(vals[k]);
         if (lane == 0 && s) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[idx[k]]), s);
     }
-}
-
-// slow path: the fold's columns in sorted order, one pass with every load of a thread in flight
-__global__ void gather_sorted_kernel(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ code,
-                                     const double* __restrict__ speed, uint64_t n, uint32_t* code_out,
-                                     double* speed_out) {
-    const uint64_t i0 = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) * 4;
-    uint32_t p[4], c[4];
-    double v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) p[u] = i0 + u < n ? __ldg(&perm[i0 + u]) : 0u;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        c[u] = i0 + u < n ? __ldg(&code[p[u]]) : 0u;
-        v[u] = i0 + u < n ? __ldg(&speed[p[u]]) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-        if (i0 + u < n) {
-            code_out[i0 + u] = c[u];
-            speed_out[i0 + u] = v[u];
-        }
 }
 
 // fast path: the runs in perm order as (start, end) slot pairs (one load per run switch)
@@ -1330,13 +1303,6 @@ void launch_import_pairs(const double* sum, const uint64_t* cnt, uint64_t stride
                          double* psum, uint32_t* pcnt, cudaStream_t s) {
     if (!n) return;
     import_pairs_kernel<<<grid_for(n, 256), 256, 0, s>>>(sum, cnt, stride, n, psum, pcnt);
-    count_launch();
-}
-
-void launch_gather_sorted(const uint32_t* perm, const uint32_t* code, const double* speed, uint64_t n,
-                          uint32_t* code_out, double* speed_out, cudaStream_t s) {
-    if (!n) return;
-    gather_sorted_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(perm, code, speed, n, code_out, speed_out);
     count_launch();
 }
 

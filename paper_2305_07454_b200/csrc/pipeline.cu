@@ -624,17 +624,6 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         F.code = c->code.as<uint32_t>();
         F.loff = c->loff.as<uint64_t>();
         F.skey = (slow && c->slow_key_ts) ? c->keys.as<uint64_t>() : nullptr;
-        F.code_s = nullptr;
-        F.speed_s = nullptr;
-        if (slow && !feat) {  // sorted copies of code / speed: the fold reads them sequentially
-            const uint64_t NSS = c->last_slots;
-            c->code2.ensure(NSS * 4 + 4);
-            c->speed2.ensure(NSS * 8 + 8);
-            launch_gather_sorted(c->vals.as<uint32_t>(), c->code.as<uint32_t>(), c->speed.as<double>(), NSS,
-                                 c->code2.as<uint32_t>(), c->speed2.as<double>(), s);
-            F.code_s = c->code2.as<uint32_t>();
-            F.speed_s = c->speed2.as<double>();
-        }
         F.pair_key = c->pair_key.as<uint64_t>();
         F.pair_sum = c->pair_sum.as<double>();
         F.pair_cnt = c->pair_cnt.as<uint32_t>();
