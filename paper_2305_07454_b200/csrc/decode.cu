@@ -91,71 +91,59 @@ struct FastState {
 };
 static_assert(sizeof(FastState) % 8 == 4, "odd word stride: conflict-free per-thread state");
 
+// First ',' at or after tile-relative byte x within the next 32 bytes (comma bitmap `cm`, bit i =
+// tile byte i): its position, or x - 1 when there is none (every caller then fails a length test).
+__device__ __forceinline__ uint32_t next_comma(const uint32_t* __restrict__ cm, uint32_t x) {
+    const uint32_t m = __funnelshift_r(cm[x >> 5], cm[(x >> 5) + 1], x & 31);
+    return x + __ffs(m) - 1;
+}
+
 // Fast path of parse_record_impl for a line [p, e) (tile-relative) entirely staged in shared
 // memory whose header is canonical: journey, timestamp, latitude, longitude as fields 0..3, then
-// speed, heading as 5, 6 (`postal` = 1: any column at 4) or 4, 5. Returns kAccepted or
-// kRangeViolation, or kNeedGeneral whenever the general restatement has to decide.
-__device__ __forceinline__ uint8_t fast_parse(const uint8_t* __restrict__ buf, const uint32_t* __restrict__ cm,
-                                              uint32_t p, uint32_t e, int postal, FastState& fs, LineOut& o) {
-    const uint32_t len = e - p;
-    if (len > 95) return kNeedGeneral;
-    // 96-bit comma window starting at bit p
-    const uint32_t wi = p >> 5, sh = p & 31;
-    const uint32_t a = cm[wi], b = cm[wi + 1], c = cm[wi + 2], d = cm[wi + 3];
-    uint32_t m0 = __funnelshift_r(a, b, sh), m1 = __funnelshift_r(b, c, sh), m2 = __funnelshift_r(c, d, sh);
-    if (len < 32) {
-        m0 &= (1u << len) - 1u;
-        m1 = m2 = 0;
-    } else if (len < 64) {
-        m1 &= (1u << (len - 32)) - 1u;
-        m2 = 0;
-    } else {
-        m2 &= (1u << (len - 64)) - 1u;
-    }
-    // first 7 comma positions (relative to p); len when absent
-    uint32_t cpos[7];
-#pragma unroll
-    for (int k = 0; k < 7; ++k) {
-        uint32_t pos = len;
-        if (m0) {
-            pos = __ffs(m0) - 1;
-            m0 &= m0 - 1;
-        } else if (m1) {
-            pos = 32 + __ffs(m1) - 1;
-            m1 &= m1 - 1;
-        } else if (m2) {
-            pos = 64 + __ffs(m2) - 1;
-            m2 &= m2 - 1;
-        }
-        cpos[k] = pos;
-    }
-    const uint32_t fe_id = cpos[0];
-    const uint32_t fb_ts = cpos[0] + 1, fe_ts = cpos[1];
-    const uint32_t fb_la = cpos[1] + 1, fe_la = cpos[2];
-    const uint32_t fb_lo = cpos[2] + 1, fe_lo = cpos[3];
-    const uint32_t fb_sp = postal ? cpos[4] + 1 : cpos[3] + 1;
-    const uint32_t fe_sp = postal ? cpos[5] : cpos[4];
-    const uint32_t fb_hd = postal ? cpos[5] + 1 : cpos[4] + 1;
-    const uint32_t fe_hd = postal ? cpos[6] : cpos[5];
-    // every required field must exist and be non-empty (else: general decides MissingField)
-    if (fb_hd >= fe_hd || fe_id == 0 || fb_la >= fe_la || fb_lo >= fe_lo || fb_sp >= fe_sp)
-        return kNeedGeneral;
-    const uint32_t base = p + kPre;  // buffer offset of the line
+// speed, heading as 5, 6 (`postal` = 1: any column at 4) or 4, 5. True iff every field has the
+// canonical shape and the record is in range (then `o` holds the accepted record); false ->
+// the general restatement decides (including every rejection). Field ends come from the comma
+// bitmap one field at a time (the timestamp is exactly 19 bytes, its separator checked in
+// registers); the checks of all fields are combined without branches.
+__device__ __forceinline__ bool fast_parse(const uint8_t* __restrict__ buf, const uint32_t* __restrict__ cm,
+                                           uint32_t p, uint32_t e, int postal, FastState& fs, LineOut& o) {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(buf);
-    if (is_trim(buf[base]) || is_trim(buf[base + fe_id - 1])) return kNeedGeneral;
-    if (fe_ts - fb_ts != 19 || !fast_timestamp(w, base + fb_ts, fs.dc, o.ts, o.minute)) return kNeedGeneral;
-    if (!fast_number(w, buf, base + fb_la, base + fe_la, fs.q[0], o.lat) ||
-        !fast_number(w, buf, base + fb_lo, base + fe_lo, fs.q[1], o.lon) ||
-        !fast_number(w, buf, base + fb_sp, base + fe_sp, fs.q[2], o.speed) ||
-        !fast_number(w, buf, base + fb_hd, base + fe_hd, fs.q[3], o.heading))
-        return kNeedGeneral;
+    const uint32_t c0 = next_comma(cm, p);  // journey id [p, c0)
+    const uint32_t c1 = c0 + 20;            // timestamp [c0 + 1, c1)
+    const uint32_t c2 = next_comma(cm, c1 + 1);
+    const uint32_t c3 = next_comma(cm, c2 + 1);
+    const uint32_t c4 = next_comma(cm, c3 + 1);
+    uint32_t sp_b = c3 + 1, sp_e = c4;
+    if (postal) {
+        sp_b = c4 + 1;
+        sp_e = next_comma(cm, sp_b);
+    }
+    const uint32_t hd_b = sp_e + 1;
+    uint32_t hd_e;
+    {
+        const uint32_t m = __funnelshift_r(cm[hd_b >> 5], cm[(hd_b >> 5) + 1], hd_b & 31);
+        hd_e = m ? min(hd_b + __ffs(m) - 1, e) : e;
+    }
+    uint32_t sep;
+    bool ok = fast_timestamp(w, kPre + c0 + 1, fs.dc, o.ts, o.minute, sep);
+    const uint32_t idl = c0 - p;
+    ok &= (idl - 1u < 31u) & (sep == 0x2Cu) & (sp_e < e) & (c4 > c3) &
+          !trim_byte(buf[kPre + p]) & !trim_byte(buf[kPre + c0 - 1]);
+    bool num = fast_number_hit(w, buf, kPre + c1 + 1, kPre + c2, fs.q[0], o.lat);
+    num &= fast_number_hit(w, buf, kPre + c2 + 1, kPre + c3, fs.q[1], o.lon);
+    num &= fast_number_hit(w, buf, kPre + sp_b, kPre + sp_e, fs.q[2], o.speed);
+    num &= fast_number_hit(w, buf, kPre + hd_b, kPre + hd_e, fs.q[3], o.heading);
+    if (!num && ok) {  // a column changed shape: fast_number re-learns the point positions
+        num = fast_number(w, buf, kPre + c1 + 1, kPre + c2, fs.q[0], o.lat) &&
+              fast_number(w, buf, kPre + c2 + 1, kPre + c3, fs.q[1], o.lon) &&
+              fast_number(w, buf, kPre + sp_b, kPre + sp_e, fs.q[2], o.speed) &&
+              fast_number(w, buf, kPre + hd_b, kPre + hd_e, fs.q[3], o.heading);
+    }
     if (o.heading == 360.0) o.heading = 0.0;
     o.id_rel = p;
-    o.id_len = fe_id;
-    if (!(o.lat >= -90.0 && o.lat <= 90.0) || !(o.lon >= -180.0 && o.lon <= 180.0) ||
-        !(o.speed >= 0.0) || !(o.heading >= 0.0 && o.heading < 360.0))
-        return kRangeViolation;  // fast numbers are always finite
-    return kAccepted;
+    o.id_len = idl;
+    return ok & num & (o.lat >= -90.0) & (o.lat <= 90.0) & (o.lon >= -180.0) & (o.lon <= 180.0) &
+           (o.speed >= 0.0) & (o.heading >= 0.0) & (o.heading < 360.0);
 }
 
 // The general restatement, kept out of line so the hot loop stays small in the I-cache.
@@ -445,14 +433,14 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
             }
         };
         // ---- 4. parse: one data line per thread, results staged in shared memory -----------------
-        auto parse_lines = [&](uint32_t n_pass, uint64_t slot0) {
-            for (uint32_t li = tid; li < n_pass; li += kDecodeThreads) {
+        // one data line starting at tile byte p_rel: staged results at index li, outputs at slot
+        auto parse_one = [&](uint32_t li, uint32_t p_rel, uint64_t slot) {
+            {
                 LineOut o;
                 o.ts = 0;
                 o.speed = 0.0;
                 o.id_rel = 0;
                 o.id_len = 0;
-                const uint32_t p_rel = S.starts[li];
                 uint32_t s;
                 uint32_t se_rel;  // shard end relative to the tile start (clamped to 32 bits)
                 int kind;
@@ -514,7 +502,6 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                 if (last == '\r') --len;
                 if (len == 0) {  // "\r\n" / "\r<shard end>": empty, not a data line (inert slot)
                     atomicAdd(&s_inert, 1u);  // rare: a shared counter, not a register
-                    const uint64_t slot = slot0 + li;
                     P.out.ts[slot] = 0;
                     P.out.speed[slot] = 0.0;
                     P.out.loff[slot] = tb + p_rel;
@@ -522,10 +509,10 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                     S.l_code[li] = kCodeRejected;
                     S.id_rel[li] = 0;
                     S.id_len[li] = 0;
-                    continue;
+                    return;
                 }
                 uint8_t why = kNeedGeneral;
-                if (in_smem && kind >= 0) why = fast_parse(bufb, S.cm, p_rel, p_rel + len, kind, fs, o);
+                if (in_smem && kind >= 0 && fast_parse(bufb, S.cm, p_rel, p_rel + len, kind, fs, o)) why = kAccepted;
                 if (why == kNeedGeneral) {  // (a separate out-struct: `o` itself never escapes to
                     LineOut og;              //  the out-of-line call, so it stays in registers)
                     og.ts = 0;
@@ -546,7 +533,6 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                 } else {
                     atomicAdd(&s_cnt[why - 1], 1u);  // rare
                 }
-                const uint64_t slot = slot0 + li;
                 P.out.ts[slot] = o.ts;
                 P.out.speed[slot] = o.speed;
                 P.out.loff[slot] = tb + p_rel;
@@ -559,6 +545,10 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                 S.id_rel[li] = o.id_rel;
                 S.id_len[li] = o.id_len | (why == kAccepted ? 0x80000000u : 0u);
             }
+        };
+        // overflow tiles: lines [pass_base, pass_base + n_pass) from the start list
+        auto parse_lines = [&](uint32_t n_pass, uint64_t slot0) {
+            for (uint32_t li = tid; li < n_pass; li += kDecodeThreads) parse_one(li, S.starts[li], slot0 + li);
         };
 
         // ---- 5. run heads: the journey id changes or the timestamp stops increasing --------------
@@ -576,37 +566,33 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                 if (k < n_pass) {
                     const uint32_t ln = S.id_len[k];
                     const uint32_t code = S.l_code[k];
-                    if (ln >> 31) {
-                        const uint32_t pl = k ? S.id_len[k - 1] : c_len;
-                        const long long pts = k ? S.l_ts[k - 1] : c_ts;
-                        const uint32_t idl = ln & 0x7FFFFFFFu;
-                        head = true;
-                        if ((pl >> 31) && (pl & 0x7FFFFFFFu) == idl && pts < S.l_ts[k]) {
-                            const uint32_t pid = k ? S.id_rel[k - 1] : c_id;
-                            const uint32_t mid = S.id_rel[k];
-                            bool same = true;
-                            if (pid + idl <= staged_len && mid + idl <= staged_len) {
-                                for (uint32_t i = 0; i < idl; i += 4) {
-                                    uint32_t x = word_at(ws, kPre + pid + i) ^ word_at(ws, kPre + mid + i);
-                                    if (idl - i < 4) x &= (1u << (8 * (idl - i))) - 1u;
-                                    if (x) {
-                                        same = false;
-                                        break;
-                                    }
+                    const uint32_t pl = k ? S.id_len[k - 1] : c_len;
+                    const long long pts = k ? S.l_ts[k - 1] : c_ts;
+                    const uint32_t idl = ln & 0x7FFFFFFFu;
+                    // a continuation needs: both accepted, equal id lengths, rising timestamps and
+                    // equal id bytes (compared straight from the staged tile for ids <= 8 bytes)
+                    bool cont = (ln >> 31) && pl == ln && pts < S.l_ts[k];
+                    if (cont) {
+                        const uint32_t pid = k ? S.id_rel[k - 1] : c_id;
+                        const uint32_t mid = S.id_rel[k];
+                        if (idl <= 8 && pid + 8 <= staged_len && mid + 8 <= staged_len) {
+                            const uint32_t m0 = ~bytes_from_rt(static_cast<int>(idl));
+                            const uint32_t m1 = ~bytes_from_rt(static_cast<int>(idl) - 4);
+                            const uint32_t x0 = word_at(ws, kPre + pid) ^ word_at(ws, kPre + mid);
+                            const uint32_t x1 = word_at(ws, kPre + pid + 4) ^ word_at(ws, kPre + mid + 4);
+                            cont = ((x0 & m0) | (x1 & m1)) == 0;
+                        } else {
+                            const uint8_t* pa = (pid + idl <= staged_len) ? tile_s + pid : P.csv + tb + pid;
+                            const uint8_t* pb = (mid + idl <= staged_len) ? tile_s + mid : P.csv + tb + mid;
+                            for (uint32_t i = 0; i < idl; ++i)
+                                if (pa[i] != pb[i]) {
+                                    cont = false;
+                                    break;
                                 }
-                            } else {
-                                const uint8_t* pa = (pid + idl <= staged_len) ? tile_s + pid : P.csv + tb + pid;
-                                const uint8_t* pb = (mid + idl <= staged_len) ? tile_s + mid : P.csv + tb + mid;
-                                for (uint32_t i = 0; i < idl; ++i)
-                                    if (pa[i] != pb[i]) {
-                                        same = false;
-                                        break;
-                                    }
-                            }
-                            head = !same;
                         }
-                        if (!head && (k ? S.l_code[k - 1] : c_code) != code) ++my_trans;
                     }
+                    head = (ln >> 31) && !cont;  // rejected lines are never heads
+                    if (cont && (k ? S.l_code[k - 1] : c_code) != code) ++my_trans;
                     P.out.code[slot0 + k] = head ? (code | kHeadBit) : code;
                 }
                 const uint32_t bal = __ballot_sync(0xFFFFFFFFu, head);
@@ -636,10 +622,18 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
             // ---- common case: the tile's own slot range [tile * kLineCap, + n_data) ----------------
             slot0 = static_cast<uint64_t>(tile) * kLineCap;
             head0 = slot0;
-            write_starts(0);
             if (tid == 0) c_len = 0;
-            __syncthreads();
-            parse_lines(n_data, slot0);
+            // every thread parses the data lines that start in its own 64 bytes (no start list)
+            {
+                uint64_t m = (static_cast<uint64_t>(smask[1]) << 32) | smask[0];
+                uint32_t li = my_off;
+                while (m) {
+                    const uint32_t bit = static_cast<uint32_t>(__ffsll(static_cast<long long>(m))) - 1u;
+                    m &= m - 1;
+                    parse_one(li, 64u * tid + bit, slot0 + li);
+                    ++li;
+                }
+            }
             __syncthreads();
             heads = mark_heads(n_data, slot0, [&](uint32_t idx, uint32_t k) {
                 P.out.hslot[head0 + idx] = static_cast<uint32_t>(slot0 + k);

@@ -194,6 +194,57 @@ CVLG_HD bool fast_number(const uint32_t* w, const uint8_t* buf, uint32_t b, uint
     return true;
 }
 
+// 4 validated ASCII digits (byte 0 = most significant) -> value, plus `acc`: two 16x8-bit dot
+// products on the device (IDP, the FMA pipe) instead of the ALU-pipe swar4 chain. The '0' bias
+// (48 * 1111) is folded into the accumulator.
+CVLG_HD uint32_t dig4_acc(uint32_t r, uint32_t acc) {
+#if defined(__CUDA_ARCH__)
+    return __dp2a_hi(0x0001000Au, r, __dp2a_lo(0x006403E8u, r, acc - 53328u));
+#else
+    return acc + swar4(r);
+#endif
+}
+
+// std::from_chars(double) on field [b, e) (buffer offsets) for the shape the previous line of
+// this column had: [-]digits.digits with the point at window index q (the 12-byte window is
+// right-aligned at e, so q = 11 - fraction digits) and at most 8 digits. Branch-free: the
+// caller combines the verdicts of all fields; false -> fast_number (which re-learns q) decides.
+// Bytes at window positions <= q move up one position (dropping the point), positions before
+// the first digit become '0', and the 8-digit string M is converted exactly; x = M / 10^(11-q)
+// correctly rounded (div_pow10: M < 10^8 is exact, Clinger's fast path).
+CVLG_HD bool fast_number_hit(const uint32_t* w, const uint8_t* buf, uint32_t b, uint32_t e, int q,
+                             double& v) {
+    const uint32_t n = e - b;
+    const uint32_t o = e - 12, i = o >> 2, sh = (o & 3) * 8;
+    const uint32_t x0 = w[i], x1 = w[i + 1], x2 = w[i + 2], x3 = w[i + 3];
+    const uint32_t a0 = fs_r(x0, x1, sh), a1 = fs_r(x1, x2, sh), a2 = fs_r(x2, x3, sh);
+    const uint32_t neg = buf[b] == '-' ? 1u : 0u;
+    const int D = static_cast<int>(n) - static_cast<int>(neg) - 1;  // digits (one point)
+    const int s = 12 - static_cast<int>(n) + static_cast<int>(neg);  // first byte after the sign
+    const uint32_t pt = fs_r(q < 8 ? a1 : a2, a2, static_cast<uint32_t>(8 * q)) & 0xFFu;
+    // drop the point: positions <= q take the byte below them
+    const uint32_t s1 = fs_l(a0, a1, 8), s2 = fs_l(a1, a2, 8);
+    const uint32_t k1 = bytes_from_rt(q - 3), k2 = bytes_from_rt(q - 7);
+    uint32_t r1 = (a1 & k1) | (s1 & ~k1);
+    uint32_t r2 = (a2 & k2) | (s2 & ~k2);
+    // digits occupy [12 - D, 12): everything before becomes '0'
+    const uint32_t d1 = bytes_from_rt(8 - D), d2 = bytes_from_rt(4 - D);
+    r1 = (r1 & d1) | (0x30303030u & ~d1);
+    r2 = (r2 & d2) | (0x30303030u & ~d2);
+    const bool ok = (n <= 12u) & (D >= 1) & (D <= 8) & (q >= 4) & (q >= s) & (pt == 0x2Eu) &
+                    digits3(r1, r2, 0x30303030u);
+    const uint32_t M = dig4_acc(r2, dig4_acc(r1, 0u) * 10000u);
+    const double x = div_pow10(static_cast<double>(M), (11 - q) & 7);
+    v = bits_dbl(dbl_bits(x) | (static_cast<uint64_t>(neg) << 63));
+    return ok;
+}
+
+// Trim byte of split_fields (ingest.cpp:31-39): ' ', '\t', '\r' (one range test + bit test)
+CVLG_HD bool trim_byte(uint32_t c) {
+    const uint32_t t = c - 9u;
+    return t < 24u && ((0x800011u >> t) & 1u);
+}
+
 // '\n' and ',' flags of 32 staged bytes (words x[0..7], little endian) -> two 32-bit masks, bit i
 // = byte i. Per byte class the exact zero-byte test costs 3 operations (the 0x7F mask of x is
 // shared; the class bytes have bit 7 clear). Flags of two words are merged into one word
@@ -254,29 +305,35 @@ CVLG_HD bool date_refill(uint32_t t0, uint32_t t1, uint32_t t2, DateCache& dc) {
 }
 
 // Timestamp::parse (datetime.cpp:65-75) of the 19 bytes at buffer offset off: epoch seconds and
-// minute of day (the time_bin input, grid.cpp:69-71).
-CVLG_HD bool fast_timestamp(const uint32_t* w, uint32_t off, DateCache& dc, int64_t& ts, uint32_t& mod) {
+// minute of day (the time_bin input, grid.cpp:69-71). `next` receives the byte after the 19
+// (the field separator the caller expects). Branch-free except for the date-cache refill.
+CVLG_HD bool fast_timestamp(const uint32_t* w, uint32_t off, DateCache& dc, int64_t& ts, uint32_t& mod,
+                            uint32_t& next) {
     const uint32_t i = off >> 2, sh = (off & 3) * 8;
     const uint32_t a0 = w[i], a1 = w[i + 1], a2 = w[i + 2], a3 = w[i + 3], a4 = w[i + 4], a5 = w[i + 5];
     const uint32_t t0 = fs_r(a0, a1, sh), t1 = fs_r(a1, a2, sh), t2 = fs_r(a2, a3, sh),
                    t3 = fs_r(a3, a4, sh), t4 = fs_r(a4, a5, sh);
+    next = t4 >> 24;
     if (t0 != dc.k0 || t1 != dc.k1 || (t2 & 0xFFFFu) != dc.k2)
         if (!date_refill(t0, t1, t2, dc)) return false;
-    // ' ' at 10, ':' at 13 and 16
-    if ((t2 & 0x00FF0000u) != 0x00200000u || (t3 & 0x0000FF00u) != 0x00003A00u ||
-        (t4 & 0xFFu) != 0x3Au)
-        return false;
     const uint32_t hm = bperm(t2, t3, 0x7643u);             // H H M M
     const uint32_t ss = bperm(t4, 0x30303030u, 0x4421u);    // S S 0 0
-    if (!digits3(hm, ss, 0x30303030u)) return false;
     const uint32_t dh = hm & 0x0F0F0F0Fu;
     const uint32_t p = dh * 10u + (dh >> 8);  // byte 0: HH, byte 2: MM
     const uint32_t h = p & 0xFFu, mi = (p >> 16) & 0xFFu;
     const uint32_t s = (ss & 0xFu) * 10u + ((ss >> 8) & 0xFu);
-    if (h > 23 || mi > 59 || s > 59) return false;
+    // ' ' at 10, ':' at 13 and 16, digits, 0..23:0..59:0..59
+    const bool ok = ((t2 & 0x00FF0000u) == 0x00200000u) & ((t3 & 0x0000FF00u) == 0x00003A00u) &
+                    ((t4 & 0xFFu) == 0x3Au) & digits3(hm, ss, 0x30303030u) & (h <= 23) & (mi <= 59) &
+                    (s <= 59);
     mod = h * 60u + mi;
     ts = day_sec(dc) + static_cast<int64_t>(mod * 60u + s);
-    return true;
+    return ok;
+}
+
+CVLG_HD bool fast_timestamp(const uint32_t* w, uint32_t off, DateCache& dc, int64_t& ts, uint32_t& mod) {
+    uint32_t next;
+    return fast_timestamp(w, off, dc, ts, mod, next);
 }
 
 }  // namespace cvlg

@@ -288,4 +288,59 @@ uint64_t hp_fuzz_fast_timestamp(uint64_t seed, uint64_t count, uint64_t* decided
     return bad;
 }
 
+
+// fast_number_hit (the cached-shape path of K1) against parse_double: same string shapes as
+// hp_fuzz_fast_number; the cached point index is the true one (right-aligned window) half of
+// the time, random otherwise. Returns disagreements (hit accepted, value or acceptance differs).
+uint64_t hp_fuzz_fast_number_hit(uint64_t seed, uint64_t count, uint64_t* decided, char* first_bad) {
+    uint64_t x = seed * 0x9E3779B97F4A7C15ull + 5;
+    auto rnd = [&]() {
+        x ^= x << 13;
+        x ^= x >> 7;
+        x ^= x << 17;
+        return x;
+    };
+    const char junk[] = "0123456789.-+ eE\tx,";
+    uint64_t bad = 0, dec = 0;
+    char s[32];
+    for (uint64_t i = 0; i < count; ++i) {
+        int n = 0;
+        const uint64_t r = rnd();
+        const int shape = r % 8;
+        if (shape < 5) {
+            if (rnd() % 3 == 0) s[n++] = '-';
+            const int I = rnd() % 5, F = rnd() % 10;
+            for (int k = 0; k < I; ++k) s[n++] = '0' + rnd() % 10;
+            if (shape != 4) s[n++] = '.';
+            for (int k = 0; k < F; ++k) s[n++] = '0' + rnd() % 10;
+        } else {
+            const int L = 1 + rnd() % 13;
+            for (int k = 0; k < L; ++k) s[n++] = junk[rnd() % (sizeof(junk) - 1)];
+        }
+        if (n == 0) continue;
+        s[n] = 0;
+        int q = static_cast<int>(rnd() % 14) - 1;
+        if (rnd() & 1) {
+            const char* d = static_cast<const char*>(std::memchr(s, '.', n));
+            q = d ? 12 - (n - static_cast<int>(d - s)) : -1;
+        }
+        alignas(16) uint8_t buf[128];
+        std::memset(buf, 'x', sizeof(buf));
+        const int at = 40 + static_cast<int>(rnd() % 4);
+        std::memcpy(buf + at - 5, "12.5,", 5);
+        std::memcpy(buf + at, s, n);
+        buf[at + n] = ',';
+        double vf = 0, vg = 0;
+        if (!cvlg::fast_number_hit(reinterpret_cast<const uint32_t*>(buf), buf, at, at + n, q, vf)) continue;
+        ++dec;
+        const bool g = cvlg::parse_double(reinterpret_cast<const uint8_t*>(s), n, vg);
+        if (!g || cvlg::dbl_bits(vf) != cvlg::dbl_bits(vg)) {
+            if (!bad) std::memcpy(first_bad, s, n + 1);
+            ++bad;
+        }
+    }
+    *decided = dec;
+    return bad;
+}
+
 }  // extern "C"

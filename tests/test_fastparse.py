@@ -18,6 +18,8 @@ def _setup(lib):
     u64p = ctypes.POINTER(ctypes.c_uint64)
     lib.hp_fuzz_fast_number.restype = ctypes.c_uint64
     lib.hp_fuzz_fast_number.argtypes = [ctypes.c_uint64, ctypes.c_uint64, u64p, ctypes.c_char_p]
+    lib.hp_fuzz_fast_number_hit.restype = ctypes.c_uint64
+    lib.hp_fuzz_fast_number_hit.argtypes = [ctypes.c_uint64, ctypes.c_uint64, u64p, ctypes.c_char_p]
     lib.hp_fuzz_fast_timestamp.restype = ctypes.c_uint64
     lib.hp_fuzz_fast_timestamp.argtypes = lib.hp_fuzz_fast_number.argtypes
     lib.hp_fast_number.argtypes = [ctypes.c_char_p, ctypes.c_int32, ctypes.c_int, ctypes.c_int,
@@ -109,3 +111,15 @@ def test_binning_fast_path(hp):
     steps = [0.1, 0.01, 0.013, 0.007, 0.25, 10.0, 90.0, 120.0, 45.0, 0.02, 1.0 / 3.0, 0.3]
     arr = (ctypes.c_double * len(steps))(*steps)
     assert hp.hp_fuzz_snapped_floor(1, 3_000_000, arr, len(steps)) == 0
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_fast_number_hit_fuzz(hp, seed):
+    """K1's cached-shape number path (fast_number_hit) never disagrees with from_chars, and it
+    decides a large share of the canonical shapes."""
+    lib = _setup(hp)
+    d = ctypes.c_uint64()
+    b = ctypes.create_string_buffer(64)
+    bad = lib.hp_fuzz_fast_number_hit(seed, 400_000, ctypes.byref(d), b)
+    assert bad == 0, b.value
+    assert d.value > 50_000
