@@ -13,7 +13,8 @@ done
 timeout 300 ncu --metrics $M --clock-control none -k regex:decode_kernel -c 2 python tools/profile_step.py --steps 2 > /tmp/ncu_main.txt 2>&1
 echo "== main" >> $out; grep -E "gpu__time|inst_executed|issue_active|warps_active|registers|occupancy" /tmp/ncu_main.txt | tail -6 >> $out
 cat $out
-if [ "$2" == "full" ]; then
+if [ "$2" == "none" ]; then echo "tests skipped";
+elif [ "$2" == "full" ]; then
   timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_$TAG.log
 else
   timeout 900 python -m pytest tests/test_decode_slots.py tests/test_gpu_parity.py -m gpu -x -q > gpurun_out/pytest_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_$TAG.log
