@@ -42,12 +42,13 @@ for g in a.grid.split(","):
     os.environ["CVLG_RING_MB"] = mb
     os.environ["CVLG_RING_SLOTS"] = slots
     for nt in threads:
-        cvlg.run_pipeline(paths, spec, n_threads=nt, ctx=ctx, out=(planes, raw))
+        os.environ["CVLG_RING_READERS"] = str(nt)
+        cvlg.run_pipeline(paths, spec, n_threads=T, ctx=ctx, out=(planes, raw))
         ts = []
         for _ in range(a.reps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            cvlg.run_pipeline(paths, spec, n_threads=nt, ctx=ctx, out=(planes, raw))
+            cvlg.run_pipeline(paths, spec, n_threads=T, ctx=ctx, out=(planes, raw))
             ts.append(time.perf_counter() - t0)
         best = min(ts)
         print(f"ring {mb:>3} MB x {slots:>3} slots, {nt:2d} readers: best {1000 * best:7.1f} ms "
