@@ -73,8 +73,9 @@ __global__ void tile_field_kernel(const uint4* tiles, uint64_t n, int field, uin
 // heads in tile order (= provenance order for regular tiles); a run ends at the next head of its
 // tile or at the tile's last line (runs never cross tiles: a tile's first line is always a head)
 __global__ void heads_compact_kernel(const uint4* tiles, uint64_t n, const uint32_t* hpos,
-                                     const uint32_t* hscr, const uint64_t* hid_scr, uint32_t* hslot,
-                                     uint32_t* hend, uint64_t* hid) {
+                                     const uint32_t* hscr, const uint64_t* hid_scr,
+                                     const ulonglong2* hkey_scr, uint32_t* hslot, uint32_t* hend,
+                                     uint64_t* hid, ulonglong2* hkey) {
     // one thread per tile (journey-ordered input: a head or two per tile); tiles with many heads
     // (shuffled rows) are copied by the whole warp afterwards
     const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -91,6 +92,7 @@ __global__ void heads_compact_kernel(const uint4* tiles, uint64_t n, const uint3
             hslot[base + i] = hscr[v.z + i];
             hend[base + i] = i + 1 < v.w ? hscr[v.z + i + 1] : v.x + v.y;
             hid[base + i] = hid_scr[v.z + i];
+            hkey[base + i] = hkey_scr[v.z + i];
         }
     }
     uint32_t big = __ballot_sync(0xFFFFFFFFu, !small);
@@ -104,6 +106,7 @@ __global__ void heads_compact_kernel(const uint4* tiles, uint64_t n, const uint3
             hslot[bb + i] = hscr[z + i];
             hend[bb + i] = i + 1 < w ? hscr[z + i + 1] : x + y;
             hid[bb + i] = hid_scr[z + i];
+            hkey[bb + i] = hkey_scr[z + i];
         }
     }
 }
@@ -166,7 +169,12 @@ __global__ void dict_insert_kernel(DictParams D) {
     const uint8_t* p = D.csv + off;
     uint64_t e0, e1, slot;
     const bool is_long = len > 15;
-    if (!is_long) {
+    const ulonglong2 hk = D.hkey[h];
+    if (hk.y != kNoKey) {  // K1 assembled the key from the staged tile (no CSV gather)
+        e0 = hk.x;
+        e1 = hk.y;
+        slot = mix64(e0 ^ mix64(e1)) & D.mask;
+    } else if (!is_long) {
         uint64_t k0 = 0, k1 = 0;
         if (off + 20 <= D.csv_len) {  // 5 aligned words cover bytes [off, off + 16)
             const uint32_t* w = reinterpret_cast<const uint32_t*>(D.csv + (off & ~3ull));
@@ -1084,10 +1092,11 @@ void launch_tile_field(const uint4* tiles, uint64_t n, int field, uint32_t* out,
 }
 
 void launch_heads_compact(const uint4* tiles, uint64_t n, const uint32_t* hpos, const uint32_t* hscr,
-                          const uint64_t* hid_scr, uint32_t* hslot, uint32_t* hend, uint64_t* hid,
-                          cudaStream_t s) {
+                          const uint64_t* hid_scr, const ulonglong2* hkey_scr, uint32_t* hslot,
+                          uint32_t* hend, uint64_t* hid, ulonglong2* hkey, cudaStream_t s) {
     if (!n) return;
-    heads_compact_kernel<<<grid_for(n, 256), 256, 0, s>>>(tiles, n, hpos, hscr, hid_scr, hslot, hend, hid);
+    heads_compact_kernel<<<grid_for(n, 256), 256, 0, s>>>(tiles, n, hpos, hscr, hid_scr, hkey_scr, hslot,
+                                                          hend, hid, hkey);
     count_launch();
 }
 
@@ -1188,8 +1197,10 @@ void launch_slot_jstart(const uint64_t* keys, int rank_shift, uint64_t n, uint32
     count_launch();
 }
 
-// enough lanes for every journey, capped at what is resident at once (journeys are handed out
-// dynamically, so CTAs beyond the resident set would find nothing left to do)
+// one warp per journey at least (the first journeys go lane-major to lane 0 of every warp of the
+// grid, so few long journeys spread over every SM instead of filling the lanes of a few warps),
+// capped at what is resident at once (journeys are handed out dynamically, so CTAs beyond the
+// resident set would find nothing left to do)
 unsigned fold_grid(uint64_t n_journeys, bool slow) {
     const int sms = per_device(kPdSms, [] {
         int dev = 0, n = 0;
@@ -1207,7 +1218,7 @@ unsigned fold_grid(uint64_t n_journeys, bool slow) {
         return n;
     });
     const uint64_t cap = static_cast<uint64_t>(sms) * std::max(1, per_sm);
-    return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n_journeys + kFoldWarps * 32 - 1) / (kFoldWarps * 32), cap)));
+    return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n_journeys + kFoldWarps - 1) / kFoldWarps, cap)));
 }
 
 // live pairs of the tail [n - dead, n) -> src list (any order)

@@ -164,6 +164,27 @@ __device__ __noinline__ uint8_t general_parse(const uint8_t* line, int32_t len, 
     return why;
 }
 
+// The dictionary key of a run head's journey id (dict_insert's format: bytes 0..7 big-endian,
+// then bytes 8..14 big-endian << 8 | length) from the staged tile, for ids of <= 15 bytes whose
+// bytes are staged; otherwise .y = kNoKey and dict_insert reads the id from the CSV itself.
+__device__ __forceinline__ ulonglong2 head_key(const uint32_t* ws, uint32_t rel, uint32_t len,
+                                               uint32_t staged_len) {
+    ulonglong2 k;
+    k.x = 0;
+    k.y = kNoKey;
+    if (len <= 15 && rel + len <= staged_len) {
+        uint32_t b[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            b[q] = word_at(ws, kPre + rel + 4 * q) & ~bytes_from_rt(static_cast<int>(len) - 4 * q);
+        auto bs = [](uint32_t x) { return __byte_perm(x, 0u, 0x0123u); };
+        k.x = (static_cast<uint64_t>(bs(b[0])) << 32) | bs(b[1]);
+        const uint64_t k1 = ((static_cast<uint64_t>(bs(b[2])) << 32) | bs(b[3])) >> 8;
+        k.y = (k1 << 8) | len;
+    }
+    return k;
+}
+
 // 1 / 0: canonical column map with / without a column between longitude and speed; -1: general
 __device__ __forceinline__ int canonical_kind(const ColumnMap& m) {
     if (m.journey_id != 0 || m.timestamp != 1 || m.latitude != 2 || m.longitude != 3) return -1;
@@ -637,7 +658,9 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
             __syncthreads();
             heads = mark_heads(n_data, slot0, [&](uint32_t idx, uint32_t k) {
                 P.out.hslot[head0 + idx] = static_cast<uint32_t>(slot0 + k);
-                P.out.hid[head0 + idx] = (tb + S.id_rel[k]) | (static_cast<uint64_t>(S.id_len[k] & 0x7FFFFFFFu) << 40);
+                const uint32_t rel = S.id_rel[k], len = S.id_len[k] & 0x7FFFFFFFu;
+                P.out.hid[head0 + idx] = (tb + rel) | (static_cast<uint64_t>(len) << 40);
+                P.out.hkey[head0 + idx] = head_key(reinterpret_cast<const uint32_t*>(bufb), rel, len, staged_len);
             });
         } else {
             // ---- more than kLineCap lines: slots and heads from the overflow regions --------------
@@ -662,8 +685,10 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
                     __syncthreads();
                     heads += mark_heads(n_pass, slot0 + pass_base, [&](uint32_t idx, uint32_t k) {
                         P.out.hslot[head0 + heads + idx] = static_cast<uint32_t>(slot0 + pass_base + k);
-                        P.out.hid[head0 + heads + idx] =
-                            (tb + S.id_rel[k]) | (static_cast<uint64_t>(S.id_len[k] & 0x7FFFFFFFu) << 40);
+                        const uint32_t rel = S.id_rel[k], len = S.id_len[k] & 0x7FFFFFFFu;
+                        P.out.hid[head0 + heads + idx] = (tb + rel) | (static_cast<uint64_t>(len) << 40);
+                        P.out.hkey[head0 + heads + idx] =
+                            head_key(reinterpret_cast<const uint32_t*>(bufb), rel, len, staged_len);
                     });
                     __syncthreads();
                     if (tid == 0) {  // carry the pass's last line

@@ -22,6 +22,7 @@ constexpr int kLineCap = 352 * kTile / 16384;  // data lines handled per pass ov
 // Slot word (one per data line): bits 0..30 = cell code (grid.cuh kCode*), bit 31 = run head.
 constexpr uint32_t kHeadBit = 0x80000000u;
 constexpr uint32_t kCodeMask = 0x7FFFFFFFu;
+constexpr unsigned long long kNoKey = ~0ull;  // hkey[].y of heads whose key dict_insert derives itself
 
 // Stats counters in device memory (u64 each).
 enum : int {
@@ -57,6 +58,8 @@ struct DecodeOut {
     double* lon;
     uint32_t* hslot;  // [head scratch] run-head slots; tile t's at tiles[t].z + (0 .. tiles[t].w)
     uint64_t* hid;    // [head scratch] journey id span of the head: byte offset | length << 40
+    ulonglong2* hkey;  // [head scratch] the dictionary key of ids <= 15 bytes (dict_insert's
+                       // format), .y = kNoKey when the id is longer or not staged
     uint4* tiles;     // [tile] (slot base, data lines, head base, heads)
     uint64_t reg_slots;                  // n_tiles * kLineCap
     unsigned long long* ovf_slots;       // overflow-region slot counter (zeroed)

@@ -275,6 +275,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         c->loff.ensure(S_all * 8);
         c->hscr.ensure(S_all * 4);
         c->hid_scr.ensure(S_all * 8);
+        c->hkey_scr.ensure(S_all * 16);
         P.out.ts = c->ts.as<int64_t>();
         P.out.speed = c->speed.as<double>();
         P.out.code = c->code.as<uint32_t>();
@@ -289,6 +290,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         }
         P.out.hslot = c->hscr.as<uint32_t>();
         P.out.hid = c->hid_scr.as<uint64_t>();
+        P.out.hkey = c->hkey_scr.as<ulonglong2>();
         P.out.tiles = c->tiles.as<uint4>();
         P.out.reg_slots = reg;
         P.out.ovf_slots = c->counter.as<unsigned long long>();
@@ -390,9 +392,11 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         exclusive_scan_u32(c->flags.as<uint32_t>(), c->thpos.as<uint32_t>(), n_tiles, nullptr,
                            c->scan_tmp.as<uint32_t>(), s);
         c->hid.ensure(H * 8 + 8);
+        c->hkey.ensure(H * 16 + 16);
         launch_heads_compact(c->tiles.as<uint4>(), n_tiles, c->thpos.as<uint32_t>(),
-                             c->hscr.as<uint32_t>(), c->hid_scr.as<uint64_t>(), c->hslot.as<uint32_t>(),
-                             c->hend.as<uint32_t>(), c->hid.as<uint64_t>(), s);
+                             c->hscr.as<uint32_t>(), c->hid_scr.as<uint64_t>(),
+                             c->hkey_scr.as<ulonglong2>(), c->hslot.as<uint32_t>(),
+                             c->hend.as<uint32_t>(), c->hid.as<uint64_t>(), c->hkey.as<ulonglong2>(), s);
 
         // ---- journey dictionary ----------------------------------------------------------------
         c->hdict.ensure(H * 4);
@@ -408,6 +412,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             DP.n_shards = n_shards;
             DP.csv_len = total;
             DP.hid = c->hid.as<uint64_t>();
+            DP.hkey = c->hkey.as<ulonglong2>();
             DP.n_heads = H;
             DP.table = c->dict.as<unsigned long long>();
             DP.mask = dcap - 1;
@@ -1377,7 +1382,7 @@ void cvlg_context_destroy(cvlg_context* c) {
     DevBuf* bufs[] = {&c->csv,    &c->shard_off, &c->cmap,     &c->good,     &c->counter,
                       &c->stats,  &c->ts,
                       &c->hscr,   &c->hend,      &c->tiles,    &c->thpos,    &c->ts2,
-                      &c->hid_scr, &c->hid,      &c->runs,     &c->lat,      &c->lon,
+                      &c->hid_scr, &c->hid, &c->hkey_scr, &c->hkey,      &c->runs,     &c->lat,      &c->lon,
                       &c->lat2,    &c->lon2,     &c->f_points, &c->f_tfirst, &c->f_tlast,
                       &c->f_len,   &c->f_step,   &c->f_vmax,   &c->f_acc,    &c->f_dwell,
                       &c->f_stops, &c->f_id,     &c->f_first,  &c->f_cmin,   &c->f_cmax,

@@ -17,6 +17,7 @@ ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--shuffle", action="store_true")
 ap.add_argument("--days", type=int, default=1)
 ap.add_argument("--fine", action="store_true")
+ap.add_argument("--mean-duration", type=float, default=500.0)
 a = ap.parse_args()
 if a.days > 1:  # c5 shape: day k uses seed 1 + k and date + k; its shards follow day k-1's
     import datetime
@@ -33,7 +34,7 @@ if a.days > 1:  # c5 shape: day k uses seed 1 + k and date + k; its shards follo
     blob = np.concatenate(blobs)
 else:
     blob, offs, rows = cvlg.synth_day(seed=1, journeys=a.journeys, shards=a.shards,
-                                      mean_duration=500.0)
+                                      mean_duration=a.mean_duration)
 if a.shuffle:  # adversarial variant: the full-sort path
     blob, offs = cvlg.cvlg.shuffle_rows(blob, offs, a.shards, seed=7)
 spec = cvlg.GridSpec(lat_step=0.01, lon_step=0.01, min_step=1) if a.fine else cvlg.GridSpec()
@@ -42,7 +43,13 @@ d_csv = torch.from_numpy(blob).cuda()
 d_planes = torch.empty((T, 8, R, C), dtype=torch.int32, device="cuda")
 d_raw = torch.empty((T, 4, R, C), dtype=torch.int32, device="cuda")
 ctx = cvlg.Context()
+times = []
 for _ in range(a.steps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
     cvlg.run_pipeline_device(d_csv.data_ptr(), offs, d_planes.data_ptr(), d_raw.data_ptr(), spec,
-                             ctx=ctx)
-print("rows", rows, "stage_ms", ctx.stage_ms())
+                             ctx=ctx, stream=torch.cuda.current_stream().cuda_stream)
+    e1.record()
+    torch.cuda.synchronize()
+    times.append(e0.elapsed_time(e1))
+print("rows", rows, "stage_ms", ctx.stage_ms(), "step_ms", ["%.2f" % t for t in times])
