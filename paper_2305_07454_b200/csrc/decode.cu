@@ -4,20 +4,24 @@
 // round-robin tiles: CTA c takes tiles c, c + G, ...). Per 16 KB tile a CTA:
 //   1. consumes the tile that one TMA bulk copy (cp.async.bulk + mbarrier) prefetched into one
 //      of two stage buffers while the previous tile was decoded, and issues the next one;
-//   2. builds '\n' and ',' bitmaps cooperatively (SIMD-within-a-register byte compares);
-//   3. lists the DATA lines that start in the tile (non-empty, not a header, good shard);
-//   4. parses one line per thread (fastparse.cuh SWAR fast path; anything unusual goes to the
-//      general restatement of parse_record_impl, parse.cuh), then filter + binning (grid.cuh);
+//   2. builds '\n' and ',' bitmaps cooperatively (SIMD-within-a-register byte compares; thread t
+//      owns tile bytes [64t, 64t + 64));
+//   3. finds the DATA lines that start in each thread's 64 bytes (non-empty, not a header, good
+//      shard) and numbers them with one block-wide scan;
+//   4. each thread parses the lines that start in its own bytes (fast path: field ends from the
+//      comma bitmap, fastparse.cuh's SWAR timestamp and cached-shape numbers, all checks combined
+//      without branches; anything unusual goes to the general restatement of parse_record_impl,
+//      parse.cuh), then filter + binning (grid.cuh);
 //   5. marks run heads (journey id changes, or the timestamp stops increasing, vs. the previous
-//      data line of the tile) and builds the tile's local head list from warp ballots;
-//   6. publishes (heads, lines) of the tile to a decoupled look-back, and only then resolves the
-//      slot/head base of the tile it decoded ONE ITERATION EARLIER and flushes that tile's
-//      staged outputs: by then every predecessor has published, so the look-back never spins.
-// Outputs, in provenance order (slot = data line; shards are concatenated in lexicographic path
-// order, so slot order equals the reference's (shard_rank, line) order, aggregate.cpp:287-289):
-// ts / speed / cell code (| head bit) / line offset per slot, and the run-head slot list.
-// Tiles with more than kLineCap data lines (pathological short lines) take a multi-pass path
-// that resolves its base first.
+//      data line of the tile) and writes the tile's head list from warp ballots, with each
+//      head's inline dictionary key.
+// Slot space is sparse per tile (tile t owns slots [t * kLineCap, t * kLineCap + lines)), so no
+// tile ever waits for another: no cross-tile scan or look-back. Outputs, in provenance order
+// (slot = data line; shards are concatenated in lexicographic path order, so slot order equals
+// the reference's (shard_rank, line) order, aggregate.cpp:287-289): ts / speed / cell code
+// (| head bit) / line offset per slot, the per-tile run-head lists and tiles[t]. Tiles with more
+// than kLineCap data lines (pathological short lines) take slots from an overflow region and a
+// multi-pass path over a start list.
 #include <algorithm>
 
 #include "fastparse.cuh"

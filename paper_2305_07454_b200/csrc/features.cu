@@ -6,7 +6,9 @@
 // Record set: exactly the records the lattice aggregates (aggregate.cpp:293-358): accepted by
 // parse_record_impl, first of each (journey, epoch) duplicate group in provenance order, passing
 // filter_reason. Order: each journey's records by timestamp (the canonical (rank, ts) order of
-// the fold). One thread per journey walks them sequentially (exact, deterministic):
+// the fold). One warp per journey walks them in 32-record chunks (coalesced loads; the link to the
+// previous kept record by ballot/shuffle; per-lane partial sums reduced in a fixed order at the
+// end, so the result is deterministic):
 //   points        number of records
 //   t_first/last  first / last epoch second
 //   length_m      sum of haversine step distances (mean Earth radius 6,371,008.8 m) in ts order
