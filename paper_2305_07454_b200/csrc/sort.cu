@@ -246,7 +246,12 @@ __global__ void radix_result_copy_kernel(uint64_t* keys, uint32_t* vals, const u
 // leave the tile as one contiguous run (coalesced stores instead of one sector per key)
 constexpr size_t kOsDynSmem = static_cast<size_t>(kRTile) * (8 + 4);
 
-__global__ void __launch_bounds__(kRThreads) radix_onesweep_kernel(
+#ifndef CVLG_OS_MINB
+#define CVLG_OS_MINB 3
+#endif
+// (3 CTAs per SM: 85 registers; unbounded, ptxas took 127 and only 2 CTAs fit, leaving the pass
+// latency-bound at 23% issue-active)
+__global__ void __launch_bounds__(kRThreads, CVLG_OS_MINB) radix_onesweep_kernel(
     uint64_t* keys_a, uint32_t* vals_a, uint64_t* keys_b, uint32_t* vals_b, uint64_t n, int shift,
     const uint32_t* digit_base, uint32_t* status, uint32_t* tile_counter, const uint32_t* plan) {
     const uint32_t pl = plan[shift / 8];
