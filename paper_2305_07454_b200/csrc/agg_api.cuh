@@ -39,6 +39,7 @@ struct FoldParams {
     const int64_t* ts;
     const double* speed;
     const uint32_t* code;
+    const ulonglong2* rec;  // slow path (nullable): (speed bits, code) per dense slot, one gather
     const uint64_t* loff;
     // slow path: the sorted (rank << span | ts - lo) keys, aligned with perm (nullable): equal keys
     // within a journey = equal timestamps, read in order instead of gathering ts per slot
@@ -124,6 +125,7 @@ struct DensifyParams {
     double* speed_out;
     uint32_t* code_out;
     uint64_t* loff_out;
+    ulonglong2* rec_out;  // nullable: (speed bits, code) interleaved for the slow fold's gathers
     uint32_t* hslot_out;
 };
 

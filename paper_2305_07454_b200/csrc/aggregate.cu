@@ -142,6 +142,12 @@ __global__ void densify_kernel(DensifyParams D) {
                 D.speed_out[dst + k] = sp[u];
                 D.code_out[dst + k] = cd[u];
                 D.loff_out[dst + k] = lo[u];
+                if (D.rec_out) {
+                    ulonglong2 r;
+                    r.x = static_cast<unsigned long long>(__double_as_longlong(sp[u]));
+                    r.y = cd[u];
+                    D.rec_out[dst + k] = r;
+                }
             }
         }
     }
@@ -746,8 +752,14 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
                 const int src = it * kPer + lane / kCh;
                 const uint32_t a = __shfl_sync(0xFFFFFFFFu, avail, src);
                 const bool in = static_cast<uint32_t>(k) < a;
-                cv[it] = in ? __ldg(&P.code[slv[it]]) : 0u;
-                sv[it] = in ? __ldg(&P.speed[slv[it]]) : 0.0;
+                if (P.rec) {  // (speed, code) of the slot in one 16-byte gather
+                    const ulonglong2 r = in ? __ldg(&P.rec[slv[it]]) : make_ulonglong2(0ull, 0ull);
+                    cv[it] = static_cast<uint32_t>(r.y);
+                    sv[it] = __longlong_as_double(static_cast<long long>(r.x));
+                } else {
+                    cv[it] = in ? __ldg(&P.code[slv[it]]) : 0u;
+                    sv[it] = in ? __ldg(&P.speed[slv[it]]) : 0.0;
+                }
                 tv[it] = !in ? 0 : P.skey ? static_cast<long long>(P.skey[p0s[it] + k]) : __ldg(&P.ts[slv[it]]);
             }
 #pragma unroll

@@ -548,6 +548,8 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             DZ.speed_out = c->speed2.as<double>();
             DZ.code_out = c->code2.as<uint32_t>();
             DZ.loff_out = c->loff2.as<uint64_t>();
+            c->rec.ensure(NS * 16 + 16);
+            DZ.rec_out = c->rec.as<ulonglong2>();
             DZ.hslot_out = c->hslot.as<uint32_t>();
             launch_densify(DZ, s);
             std::swap(c->ts, c->ts2);
@@ -627,6 +629,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         F.ts = c->ts.as<int64_t>();
         F.speed = c->speed.as<double>();
         F.code = c->code.as<uint32_t>();
+        F.rec = slow ? c->rec.as<ulonglong2>() : nullptr;
         F.loff = c->loff.as<uint64_t>();
         F.skey = (slow && c->slow_key_ts) ? c->keys.as<uint64_t>() : nullptr;
         F.pair_key = c->pair_key.as<uint64_t>();
@@ -1382,7 +1385,7 @@ void cvlg_context_destroy(cvlg_context* c) {
     DevBuf* bufs[] = {&c->csv,    &c->shard_off, &c->cmap,     &c->good,     &c->counter,
                       &c->stats,  &c->ts,
                       &c->hscr,   &c->hend,      &c->tiles,    &c->thpos,    &c->ts2,
-                      &c->hid_scr, &c->hid, &c->hkey_scr, &c->hkey,      &c->runs,     &c->lat,      &c->lon,
+                      &c->hid_scr, &c->hid, &c->hkey_scr, &c->hkey, &c->rec,      &c->runs,     &c->lat,      &c->lon,
                       &c->lat2,    &c->lon2,     &c->f_points, &c->f_tfirst, &c->f_tlast,
                       &c->f_len,   &c->f_step,   &c->f_vmax,   &c->f_acc,    &c->f_dwell,
                       &c->f_stops, &c->f_id,     &c->f_first,  &c->f_cmin,   &c->f_cmax,
