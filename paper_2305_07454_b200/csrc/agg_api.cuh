@@ -51,6 +51,10 @@ struct FoldParams {
     uint32_t* pair_count;
     uint64_t pair_cap;
     int rank_bits;
+    // bin-group mode (few long journeys): the fold's work items are (journey, time bin) groups of
+    // run pieces instead of journeys; jrank[g] is the journey rank of group g (nullable: off)
+    const uint32_t* jrank;
+    int runs_ready;             // runs[] already built (bin-group mode): skip run_list_kernel
     uint64_t* journey_counter;  // dynamic journey assignment (zeroed before the fold)
     // (cell, journey) table, key = cell << 32 | rank
     uint64_t* spill_key;
@@ -136,6 +140,19 @@ void launch_heads_compact(const uint4* tiles, uint64_t n, const uint32_t* hpos, 
 void launch_densify(const DensifyParams& d, cudaStream_t s);
 void launch_ts_range(const int64_t* ts, const uint32_t* code, uint64_t n, long long* mm, cudaStream_t s);
 void launch_dict_insert(const DictParams& d, cudaStream_t s);
+// bin-group mode: runs (perm order) -> pieces split at time-bin changes, keyed (journey, bin,
+// stream order); after sorting the keys, groups of equal (journey, bin)
+void launch_run_list(const uint32_t* perm, const uint32_t* hslot, const uint32_t* hend, uint64_t n,
+                     uint2* runs, cudaStream_t s);
+void launch_bin_pieces(const uint2* runs, uint64_t n_runs, const uint32_t* jstart, uint64_t J,
+                       uint32_t* run_j, const uint32_t* code, uint32_t drc, int bin_bits, int run_bits,
+                       uint64_t* keys, uint32_t* vals, uint2* pieces, uint32_t* counter,
+                       uint64_t cap, cudaStream_t s);
+void launch_bin_groups(const uint64_t* keys, const uint32_t* vals, const uint2* pieces, uint64_t n,
+                       int order_bits, int bin_bits, uint32_t* flags, uint2* runs_out, cudaStream_t s);
+void launch_bin_group_starts(const uint64_t* keys, const uint32_t* flags, const uint32_t* pos,
+                             uint64_t n, int order_bits, int bin_bits, uint32_t* gstart,
+                             uint32_t* gj, cudaStream_t s);
 void launch_dict_flags(const unsigned long long* table, uint64_t cap, uint32_t* flags,
                        cudaStream_t s);
 void launch_dict_compact(const uint32_t* flags, const uint32_t* pos, uint64_t cap, uint32_t* uslot,

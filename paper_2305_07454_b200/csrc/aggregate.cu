@@ -602,6 +602,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
     };
     // write the whole journey out: appended pairs, or the spill table once it has spilled
     auto flush_journey = [&]() {
+        const uint64_t jr = P.jrank ? P.jrank[j] : j;  // (bin-group mode: the group's journey)
         if (cur_g != kNone) {
             t_s[warp][cur][lane] = cur_sum;
             t_c[warp][cur][lane] = cur_cnt;
@@ -614,7 +615,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
                     ++c_ovf;
                     continue;
                 }
-                P.pair_key[at] = (static_cast<uint64_t>(t_g[warp][e][lane]) << P.rank_bits) | j;
+                P.pair_key[at] = (static_cast<uint64_t>(t_g[warp][e][lane]) << P.rank_bits) | jr;
                 P.pair_sum[at] = t_s[warp][e][lane];
                 P.pair_cnt[at] = t_c[warp][e][lane] & ~kBinSpilled;
             }
@@ -626,6 +627,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
     // closed-window entries [0, upto) -> pair list at `base` (one directory block per time bin,
     // entries of one bin are adjacent in the table), then the rest of the table moves down
     auto flush_closed = [&](uint32_t upto, uint32_t base) {
+        const uint64_t jr = j;  // (window mode is never combined with bin groups)
         uint32_t e = 0;
         while (e < upto) {
             const uint32_t tb = t_g[warp][e][lane] / P.drc;
@@ -637,7 +639,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
                 const uint32_t cn = t_c[warp][f][lane];
                 flag |= cn & kBinSpilled;
                 if (at < P.pair_cap) {
-                    P.pair_key[at] = (static_cast<uint64_t>(t_g[warp][f][lane]) << P.rank_bits) | j;
+                    P.pair_key[at] = (static_cast<uint64_t>(t_g[warp][f][lane]) << P.rank_bits) | jr;
                     P.pair_sum[at] = t_s[warp][f][lane];
                     P.pair_cnt[at] = cn & ~kBinSpilled;
                 } else {
@@ -963,6 +965,94 @@ __global__ void run_list_kernel(const uint32_t* perm, const uint32_t* hslot, con
     runs[i] = make_uint2(hslot[h], hend[h]);
 }
 
+// ---- bin-group mode (few long journeys) ----------------------------------------------------------
+// A (cell, journey) subtotal only ever collects records of the cell's time bin, so the records of
+// one (journey, bin) pair form an independent fold: runs are cut where the bin of the accepted
+// records changes, the pieces are sorted by (journey, bin, stream order), and every (journey, bin)
+// group becomes one lane's work item (its pieces in stream order = the journey's ts order).
+__global__ void run_journey_kernel(const uint32_t* jstart, uint64_t J, uint32_t* run_j) {
+    const uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (j >= J) return;
+    for (uint32_t r = jstart[j]; r < jstart[j + 1]; ++r) run_j[r] = static_cast<uint32_t>(j);
+}
+
+// one warp per run: pieces [start, end) with key (journey << (bin_bits + order_bits) | bin <<
+// order_bits | run << 9 | piece-in-run). Records before the run's first accepted record belong
+// to its first piece (they only count filter stats in the fold).
+__global__ void bin_pieces_kernel(const uint2* runs, uint64_t n_runs, const uint32_t* run_j,
+                                  const uint32_t* code, uint32_t drc, int bin_bits, int run_bits,
+                                  uint64_t* keys, uint32_t* vals, uint2* pieces, uint32_t* counter,
+                                  uint64_t cap) {
+    const uint64_t r = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (r >= n_runs) return;
+    const int lane = threadIdx.x & 31;
+    const uint2 run = runs[r];
+    const uint64_t jkey = static_cast<uint64_t>(run_j[r]) << (bin_bits + run_bits + 9);
+    const int order_bits = run_bits + 9;
+    constexpr uint32_t kNoBin = 0xFFFFFFFFu;
+    uint32_t cur_bin = kNoBin, start = run.x, n_piece = 0;
+    auto emit = [&](uint32_t end) {
+        if (lane == 0 && n_piece >= 512) atomicOr(counter + 1, 1u);  // order field overflow: host falls back
+        if (lane == 0) {
+            const uint32_t at = atomicAdd(counter, 1u);
+            if (at < cap) {
+                const uint64_t b = cur_bin == kNoBin ? 0u : cur_bin;
+                keys[at] = jkey | (b << order_bits) | (r << 9) | n_piece;
+                vals[at] = at;
+                pieces[at] = make_uint2(start, end);
+            }
+        }
+        ++n_piece;
+    };
+    for (uint32_t base = run.x; base < run.y; base += 32) {
+        const uint32_t i = base + lane;
+        const uint32_t c = i < run.y ? (code[i] & kCodeMask) : kCodeRejected;
+        const bool acc = c < kCodeFirstSpecial;
+        uint32_t x = acc ? c / drc : kNoBin;  // bin of the last accepted record at or before me
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o && x == kNoBin) x = t;
+        }
+        uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, x, 1);
+        if (lane == 0 || prev == kNoBin) prev = cur_bin;
+        const uint32_t my = acc ? c / drc : kNoBin;
+        uint32_t cut = __ballot_sync(0xFFFFFFFFu, acc && prev != kNoBin && my != prev);
+        const uint32_t last = __shfl_sync(0xFFFFFFFFu, x, 31);
+        if (cur_bin == kNoBin) {  // the open piece takes the bin of its first accepted record
+            const uint32_t first = __ballot_sync(0xFFFFFFFFu, acc);
+            if (first) cur_bin = __shfl_sync(0xFFFFFFFFu, my, __ffs(first) - 1);
+        }
+        while (cut) {
+            const int l = __ffs(cut) - 1;
+            cut &= cut - 1;
+            emit(base + l);
+            start = base + l;
+            cur_bin = __shfl_sync(0xFFFFFFFFu, my, l);
+        }
+        if (last != kNoBin) cur_bin = last;
+    }
+    emit(run.y);
+}
+
+// sorted pieces -> runs in group order, flags at group starts
+__global__ void bin_groups_kernel(const uint64_t* keys, const uint32_t* vals, const uint2* pieces,
+                                  uint64_t n, int order_bits, uint32_t* flags, uint2* runs_out) {
+    const uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (k >= n) return;
+    runs_out[k] = pieces[vals[k]];
+    flags[k] = (k == 0 || (keys[k] >> order_bits) != (keys[k - 1] >> order_bits)) ? 1u : 0u;
+}
+
+__global__ void bin_group_starts_kernel(const uint64_t* keys, const uint32_t* flags, const uint32_t* pos,
+                                        uint64_t n, int order_bits, int bin_bits, uint32_t* gstart,
+                                        uint32_t* gj) {
+    const uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (k >= n || !flags[k]) return;
+    gstart[pos[k]] = static_cast<uint32_t>(k);
+    gj[pos[k]] = static_cast<uint32_t>(keys[k] >> (order_bits + bin_bits));
+}
+
 // spilled journeys' subtotals -> pair list
 __global__ void spill_drain_kernel(FoldParams P) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -974,7 +1064,8 @@ __global__ void spill_drain_kernel(FoldParams P) {
         atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[kStOverflow]), 1ull);
         return;
     }
-    P.pair_key[pos] = ((k >> 32) << P.rank_bits) | (k & 0xFFFFFFFFull);
+    const uint64_t j = k & 0xFFFFFFFFull;
+    P.pair_key[pos] = ((k >> 32) << P.rank_bits) | (P.jrank ? P.jrank[j] : j);
     P.pair_sum[pos] = P.spill_sum[i];
     P.pair_cnt[pos] = P.spill_cnt[i];
 }
@@ -1268,7 +1359,7 @@ void launch_pair_compact(uint64_t* key, double* sum, uint32_t* cnt, uint64_t n, 
 }
 
 void launch_fold(const FoldParams& p, bool slow, cudaStream_t s) {
-    if (!slow && p.n_heads) {
+    if (!slow && p.n_heads && !p.runs_ready) {
         run_list_kernel<<<grid_for(p.n_heads, 256), 256, 0, s>>>(p.perm, p.hslot, p.hend, p.n_heads,
                                                                  const_cast<uint2*>(p.runs));
         count_launch();
@@ -1280,6 +1371,42 @@ void launch_fold(const FoldParams& p, bool slow, cudaStream_t s) {
         count_launch();
     }
     spill_drain_kernel<<<grid_for(p.spill_mask + 1, 256), 256, 0, s>>>(p);
+    count_launch();
+}
+
+void launch_run_list(const uint32_t* perm, const uint32_t* hslot, const uint32_t* hend, uint64_t n,
+                     uint2* runs, cudaStream_t s) {
+    if (!n) return;
+    run_list_kernel<<<grid_for(n, 256), 256, 0, s>>>(perm, hslot, hend, n, runs);
+    count_launch();
+}
+
+void launch_bin_pieces(const uint2* runs, uint64_t n_runs, const uint32_t* jstart, uint64_t J,
+                       uint32_t* run_j, const uint32_t* code, uint32_t drc, int bin_bits, int run_bits,
+                       uint64_t* keys, uint32_t* vals, uint2* pieces, uint32_t* counter,
+                       uint64_t cap, cudaStream_t s) {
+    if (!n_runs || !J) return;
+    run_journey_kernel<<<grid_for(J, 256), 256, 0, s>>>(jstart, J, run_j);
+    bin_pieces_kernel<<<grid_for(n_runs * 32, 256), 256, 0, s>>>(runs, n_runs, run_j, code, drc, bin_bits,
+                                                                   run_bits, keys, vals, pieces, counter, cap);
+    count_launch();
+    count_launch();
+}
+
+void launch_bin_groups(const uint64_t* keys, const uint32_t* vals, const uint2* pieces, uint64_t n,
+                       int order_bits, int bin_bits, uint32_t* flags, uint2* runs_out, cudaStream_t s) {
+    (void)bin_bits;
+    if (!n) return;
+    bin_groups_kernel<<<grid_for(n, 256), 256, 0, s>>>(keys, vals, pieces, n, order_bits, flags, runs_out);
+    count_launch();
+}
+
+void launch_bin_group_starts(const uint64_t* keys, const uint32_t* flags, const uint32_t* pos,
+                             uint64_t n, int order_bits, int bin_bits, uint32_t* gstart,
+                             uint32_t* gj, cudaStream_t s) {
+    if (!n) return;
+    bin_group_starts_kernel<<<grid_for(n, 256), 256, 0, s>>>(keys, flags, pos, n, order_bits, bin_bits,
+                                                             gstart, gj);
     count_launch();
 }
 

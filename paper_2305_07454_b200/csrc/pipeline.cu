@@ -670,6 +670,69 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         // shared memory (or a window holds); start small and re-run with the exact bound (and
         // without windows) if it ever fills.
         // (windows keep most subtotals out of the spill table unless they are long: few bins)
+        // ---- bin-group mode: few journeys for the lanes (each lane would fold one long journey
+        // alone): the work items become (journey, time bin) groups of run pieces ------------------
+        F.jrank = nullptr;
+        F.runs_ready = 0;
+        {
+            const char* genv = std::getenv("CVLG_FOLD_GROUPS");
+            const uint64_t lanes = static_cast<uint64_t>(fold_grid(~0ull >> 1, false)) * kFoldThreads;
+            const int jb = bits_for(J), bb = bits_for(dims.T), rb = bits_for(H);
+            const bool want = genv ? genv[0] == '1' : J * 8 <= lanes;
+            if (!slow && J && H && want && jb + bb + rb + 9 <= 64 && H < (1ull << 32)) {
+                const uint64_t cap = H + transitions + 16;
+                c->run_j.ensure(H * 4 + 4);
+                c->gkeys.ensure(cap * 8);
+                c->gkeys_alt.ensure(cap * 8);
+                c->gvals.ensure(cap * 4);
+                c->gvals_alt.ensure(cap * 4);
+                c->gpieces.ensure(cap * 8);
+                c->gruns.ensure(cap * 8);
+                c->flags.ensure(cap * 4 + 16);
+                c->pos.ensure(cap * 4 + 16);
+                c->scan_tmp.ensure(scan_temp_words(cap) * 4 + 64);
+                c->sort_tmp.ensure(radix_temp_bytes(cap));
+                launch_run_list(F.perm, F.hslot, F.hend, H, const_cast<uint2*>(F.runs), s);
+                uint32_t* d_cnt = c->scal.as<uint32_t>() + 30;
+                CK(cudaMemsetAsync(d_cnt, 0, 8, s));
+                launch_bin_pieces(F.runs, H, jstart, J, c->run_j.as<uint32_t>(), F.code, F.drc, bb, rb,
+                                  c->gkeys.as<uint64_t>(), c->gvals.as<uint32_t>(),
+                                  c->gpieces.as<uint2>(), d_cnt, cap, s);
+                CK(cudaMemcpyAsync(hs, d_cnt, 8, cudaMemcpyDeviceToHost, s));
+                sync(c);
+                const uint64_t n_pieces = static_cast<uint32_t*>(static_cast<void*>(hs))[0];
+                const bool order_ovf = static_cast<uint32_t*>(static_cast<void*>(hs))[1] != 0;
+                if (n_pieces > cap) fail(CVLG_E_INTERNAL, "bin pieces exceed their bound");
+                if (!order_ovf) {
+                radix_sort_pairs(c->gkeys.as<uint64_t>(), c->gvals.as<uint32_t>(),
+                                 c->gkeys_alt.as<uint64_t>(), c->gvals_alt.as<uint32_t>(), n_pieces, 0,
+                                 jb + bb + rb + 9, c->sort_tmp.p, s, d_orand, h_orand);
+                launch_bin_groups(c->gkeys.as<uint64_t>(), c->gvals.as<uint32_t>(), c->gpieces.as<uint2>(),
+                                  n_pieces, rb + 9, bb, c->flags.as<uint32_t>(), c->gruns.as<uint2>(), s);
+                exclusive_scan_u32(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), n_pieces, d_cnt,
+                                   c->scan_tmp.as<uint32_t>(), s);
+                CK(cudaMemcpyAsync(hs, d_cnt, 4, cudaMemcpyDeviceToHost, s));
+                sync(c);
+                const uint64_t G = static_cast<uint32_t*>(static_cast<void*>(hs))[0];
+                c->gstart.ensure(G * 4 + 8);
+                c->gj.ensure(G * 4 + 4);
+                launch_bin_group_starts(c->gkeys.as<uint64_t>(), c->flags.as<uint32_t>(),
+                                        c->pos.as<uint32_t>(), n_pieces, rb + 9, bb,
+                                        c->gstart.as<uint32_t>(), c->gj.as<uint32_t>(), s);
+                set_u32_kernel<<<1, 1, 0, s>>>(c->gstart.as<uint32_t>() + G, static_cast<uint32_t>(n_pieces));
+                count_launch();
+                F.n_journeys = G;
+                F.jstart = c->gstart.as<uint32_t>();
+                F.runs = c->gruns.as<uint2>();
+                F.runs_ready = 1;
+                F.jrank = c->gj.as<uint32_t>();
+                F.win = 0;  // one bin per group: nothing to window
+                TRACE("fold: bin groups");
+                } else {  // a run with > 511 pieces: fold whole journeys (runs are already built)
+                    F.runs_ready = 1;
+                }
+            }
+        }
         uint64_t scap = pow2_at_least(std::max<uint64_t>(F.win ? 1u << 20 : 1u << 18,
                                                          pair_bound / (F.win && dims.T > 48 ? 16 : 2)));
         F.pair_cap = F.win ? pair_room : pair_bound;
@@ -1385,7 +1448,7 @@ void cvlg_context_destroy(cvlg_context* c) {
     DevBuf* bufs[] = {&c->csv,    &c->shard_off, &c->cmap,     &c->good,     &c->counter,
                       &c->stats,  &c->ts,
                       &c->hscr,   &c->hend,      &c->tiles,    &c->thpos,    &c->ts2,
-                      &c->hid_scr, &c->hid, &c->hkey_scr, &c->hkey, &c->rec,      &c->runs,     &c->lat,      &c->lon,
+                      &c->hid_scr, &c->hid, &c->hkey_scr, &c->hkey, &c->rec, &c->run_j, &c->gkeys, &c->gkeys_alt, &c->gvals, &c->gvals_alt, &c->gpieces, &c->gruns, &c->gstart, &c->gj,      &c->runs,     &c->lat,      &c->lon,
                       &c->lat2,    &c->lon2,     &c->f_points, &c->f_tfirst, &c->f_tlast,
                       &c->f_len,   &c->f_step,   &c->f_vmax,   &c->f_acc,    &c->f_dwell,
                       &c->f_stops, &c->f_id,     &c->f_first,  &c->f_cmin,   &c->f_cmax,

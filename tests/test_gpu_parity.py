@@ -337,12 +337,14 @@ def test_shuffled_10m_rows_bitexact(ref, tmp_path):
     assert est["rows_read"] == rows
 
 
-@pytest.mark.parametrize("windows", ["1", "0"])
-def test_fine_grid_reopened_bins(ref, tmp_path, monkeypatch, windows):
+@pytest.mark.parametrize("mode", ["windows", "no-windows", "bin-groups"])
+def test_fine_grid_reopened_bins(ref, tmp_path, monkeypatch, mode):
     """c5's fine lattice (1-minute bins, 0.01-degree cells) over days that revisit the same time
-    bins: reloads of flushed window blocks, spilled windows, and the same with the window path off."""
+    bins: reloads of flushed window blocks, spilled windows, the same with the window path off,
+    and the (journey, bin) group fold (groups spanning several days)."""
     import paper_2305_07454_b200 as cvlg
-    monkeypatch.setenv("CVLG_FOLD_WINDOWS", windows)
+    monkeypatch.setenv("CVLG_FOLD_WINDOWS", "0" if mode == "no-windows" else "1")
+    monkeypatch.setenv("CVLG_FOLD_GROUPS", "1" if mode == "bin-groups" else "0")
     fine = cvlg.GridSpec(lat_step=0.01, lon_step=0.01, min_step=1)
     for cells, days in ((6, 4), (16, 3)):
         paths = write_shards(tmp_path / f"c{cells}", commuter_days(300, days, cells, seed=cells))
@@ -430,3 +432,15 @@ def test_daily_bins_fine_cells_spill_retry(ref, tmp_path):
     d = diff_lattice(ep, er, lat.planes, lat.raw)
     assert d == "", d
     assert stats_dict(st) == est
+
+
+@pytest.mark.parametrize("groups", ["1", "0"])
+def test_few_long_journeys_bin_groups(ref, tmp_path, monkeypatch, groups):
+    """Few, long journeys (the fold's lanes would each carry one journey): the (journey, time bin)
+    group fold against the reference, default and fine grids, and the journey fold it replaces."""
+    import paper_2305_07454_b200 as cvlg
+    monkeypatch.setenv("CVLG_FOLD_GROUPS", groups)
+    blob, offs, _ = cvlg.synth_day(seed=9, journeys=150, shards=3, mean_duration=9000.0)
+    paths = write_shards(tmp_path, [blob[offs[i]:offs[i + 1]].tobytes() for i in range(3)])
+    assert_parity(ref, paths, cvlg.GridSpec())
+    assert_parity(ref, paths, cvlg.GridSpec(lat_step=0.01, lon_step=0.01, min_step=1))
