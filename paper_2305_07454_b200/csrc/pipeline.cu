@@ -1120,10 +1120,11 @@ struct RingIngest::Impl {
     const char* const* paths;
     std::vector<FileRange> ranges;
     uint8_t* d_dst;
-    // 16 x 4 MB: small enough that the reader threads' stores are still in the host LLC when
+    // 16 x 6 MB: small enough that the reader threads' stores are still in the host LLC when
     // the copy engine reads them (measured on the B200 host: 4 MB x 16 slots 48.6 GB/s vs
-    // 32 MB x 16 slots 38.3 GB/s on c2; c3 e2e 657 vs 736 ms, tools/ring_sweep.py)
-    uint64_t chunk = 4ull << 20;
+    // 32 MB x 16 slots 38.3 GB/s on c2; c3 e2e 645 (6 MB) / 656 (4 MB) vs 736 ms (32 MB),
+    // profiles/r02_ingest_ring_c3.log)
+    uint64_t chunk = 6ull << 20;
     int slots = 16;
     struct Chunk {
         size_t range;
