@@ -464,11 +464,12 @@ def run_ours(args):
     achieved = dec_bytes / (dec_ms / 1000.0) / 1e9
     traffic = None
     tfile = ROOT / "profiles" / "decode_traffic.json"
-    if tfile.exists():
+    if tfile.exists() and world == 1:  # (the device-resident run is one K1 launch over the input)
         try:
             tj = json.loads(tfile.read_text())
-            if tj.get("csv_bytes") == local_bytes:
-                traffic = tj.get("dram_bytes_per_launch")
+            for e in (tj if isinstance(tj, list) else [tj]):
+                if e.get("csv_bytes") == local_bytes:
+                    traffic = e.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     stage_avg = [sum(s[i] for s in stage) / len(stage) for i in range(4)]

@@ -131,6 +131,32 @@ int cvlg_run_pipeline_device(cvlg_context* ctx, const uint8_t* d_csv, const uint
                              const cvlg_filter_rules* rules, uint32_t* d_planes,
                              uint32_t* d_raw_count, cvlg_stats* stats, void* stream);
 
+/* One parsed record with its provenance: cvl::CvRecord + cvl::RecordProvenance
+ * (records.hpp:13-32). Strings are borrowed (pointer + length, need not be NUL-terminated). */
+typedef struct cvlg_record {
+    const char* journey_id;
+    uint32_t journey_len;
+    uint32_t postal_len;
+    const char* postal_code;
+    const char* shard_path;
+    uint32_t shard_path_len;
+    uint32_t reserved;
+    int64_t line_number; /* 1-based, header excluded */
+    int64_t epoch_sec;
+    double latitude, longitude, speed, heading;
+} cvlg_record;
+
+/* Replaces cvl::run_pipeline_from_records (aggregate.hpp:130-133, aggregate.cpp:454-491): the
+ * same pipeline over records that are already parsed (no parse step and no parse checks: values
+ * are taken as they are). Provenance rank = rank of shard_path among the sorted unique paths;
+ * the dedup survivor is the record with the minimum (rank, (uint32) line_number); rows_read =
+ * parsed = n. Conflicting duplicates compare the full record (id, time, lat, lon, postal code,
+ * speed, heading with ==), each non-survivor against the survivor. */
+int cvlg_run_pipeline_records(cvlg_context* ctx, const cvlg_record* records, size_t n,
+                              const cvlg_grid_spec* spec, const cvlg_filter_rules* rules,
+                              uint32_t n_partitions, uint32_t n_threads, uint32_t* planes,
+                              uint32_t* raw_count, cvlg_stats* stats);
+
 /* ---- multi-GPU building blocks (one process per GPU; journeys sharded by FNV-1a id hash,
  * ingest.cpp:287-301, so every journey lives on exactly one GPU) ---------------------------
  * cvlg_partial_device runs the device-resident pipeline up to the per-(cell, journey) subtotals

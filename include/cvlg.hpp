@@ -118,6 +118,46 @@ std::vector<Frame> run_pipeline_impl(const Manifest& manifest, const Spec& spec,
     return to_frames<Frame>(planes, raw, T, R, C);
 }
 
+// cvl::run_pipeline_from_records over any record type with the reference's field names
+// (CvRecord: journey_id, timestamp.epoch_sec, latitude, longitude, postal_code, speed, heading;
+// RecordProvenance: shard_path, line_number, records.hpp:13-32)
+template <class Frame, class Records, class Spec, class Rules, class Stats, class Raise>
+std::vector<Frame> run_records_impl(const Records& records, const Spec& spec, const Rules& rules,
+                                    uint32_t n_partitions, uint32_t n_threads, Stats* stats,
+                                    Raise raise) {
+    const cvlg_grid_spec g = to_c(spec);
+    const cvlg_filter_rules f = to_c_rules(rules);
+    uint32_t T = 0, D = 0, R = 0, C = 0;
+    if (int rc = cvlg_grid_dims(&g, &T, &D, &R, &C)) raise(rc, last_error());
+    std::vector<cvlg_record> recs(records.size());
+    for (size_t i = 0; i < records.size(); ++i) {
+        const auto& rec = records[i].first;
+        const auto& prov = records[i].second;
+        cvlg_record& r = recs[i];
+        r.journey_id = rec.journey_id.data();
+        r.journey_len = static_cast<uint32_t>(rec.journey_id.size());
+        r.postal_code = rec.postal_code.data();
+        r.postal_len = static_cast<uint32_t>(rec.postal_code.size());
+        r.shard_path = prov.shard_path.data();
+        r.shard_path_len = static_cast<uint32_t>(prov.shard_path.size());
+        r.reserved = 0;
+        r.line_number = prov.line_number;
+        r.epoch_sec = rec.timestamp.epoch_sec;
+        r.latitude = rec.latitude;
+        r.longitude = rec.longitude;
+        r.speed = rec.speed;
+        r.heading = rec.heading;
+    }
+    std::vector<uint32_t> planes(static_cast<size_t>(T) * 8 * R * C);
+    std::vector<uint32_t> raw(static_cast<size_t>(T) * 4 * R * C);
+    cvlg_stats st;
+    if (int rc = cvlg_run_pipeline_records(nullptr, recs.data(), recs.size(), &g, &f, n_partitions,
+                                           n_threads, planes.data(), raw.data(), &st))
+        raise(rc, last_error());
+    fill_stats(st, stats);
+    return to_frames<Frame>(planes, raw, T, R, C);
+}
+
 }  // namespace cvlg_detail
 
 #if defined(__has_include)
@@ -138,6 +178,19 @@ inline std::vector<BatchFrame> run_pipeline(const SourceManifest& manifest, cons
                                             uint32_t n_threads = 0, PipelineStats* stats = nullptr) {
     return cvlg_detail::run_pipeline_impl<BatchFrame>(
         manifest, spec, rules, n_partitions, n_threads, stats,
+        [](int rc, const std::string& msg) {
+            if (rc >= 1 && rc <= 17) throw CvlError(static_cast<Err>(rc - 1), msg);
+            throw std::runtime_error("cvlg: " + msg);
+        });
+}
+
+// Same contract as cvl::run_pipeline_from_records (aggregate.hpp:130-133).
+inline std::vector<BatchFrame> run_pipeline_from_records(
+    const std::vector<std::pair<CvRecord, RecordProvenance>>& records, const GridSpec& spec,
+    const FilterRules& rules, uint32_t n_partitions, uint32_t n_threads = 0,
+    PipelineStats* stats = nullptr) {
+    return cvlg_detail::run_records_impl<BatchFrame>(
+        records, spec, rules, n_partitions, n_threads, stats,
         [](int rc, const std::string& msg) {
             if (rc >= 1 && rc <= 17) throw CvlError(static_cast<Err>(rc - 1), msg);
             throw std::runtime_error("cvlg: " + msg);

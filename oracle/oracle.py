@@ -52,6 +52,25 @@ class CStats(ctypes.Structure):
         }
 
 
+class CRecordProv(ctypes.Structure):  # ref_record_prov (= cvlg_record in include/cvlg.h)
+    _fields_ = [("journey_id", ctypes.c_char_p), ("journey_len", ctypes.c_uint32),
+                ("postal_len", ctypes.c_uint32), ("postal_code", ctypes.c_char_p),
+                ("shard_path", ctypes.c_char_p), ("shard_path_len", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32), ("line_number", ctypes.c_int64),
+                ("epoch_sec", ctypes.c_int64), ("latitude", ctypes.c_double),
+                ("longitude", ctypes.c_double), ("speed", ctypes.c_double),
+                ("heading", ctypes.c_double)]
+
+
+def record_array(records):
+    """records: (journey_id, epoch_sec, lat, lon, postal, speed, heading, shard_path, line)
+    with bytes strings -> ctypes array (the bytes objects stay referenced by the tuples)."""
+    arr = (CRecordProv * max(len(records), 1))()
+    for i, (jid, ts, la, lo, pc, sp, hd, path, line) in enumerate(records):
+        arr[i] = CRecordProv(jid, len(jid), len(pc), pc, path, len(path), 0, line, ts, la, lo, sp, hd)
+    return arr
+
+
 class CRecord(ctypes.Structure):
     _fields_ = [("epoch_sec", ctypes.c_int64), ("latitude", ctypes.c_double),
                 ("longitude", ctypes.c_double), ("speed", ctypes.c_double),
@@ -104,6 +123,11 @@ class Ref:
                                              ctypes.c_uint32, ctypes.c_uint32, vp, vp,
                                              ctypes.POINTER(CStats), ctypes.c_char_p,
                                              ctypes.c_size_t]
+            lib.ref_run_pipeline_from_records.argtypes = [vp, ctypes.c_size_t,
+                                                          ctypes.POINTER(CGrid), ctypes.POINTER(CRules),
+                                                          ctypes.c_uint32, ctypes.c_uint32, vp, vp,
+                                                          ctypes.POINTER(CStats), ctypes.c_char_p,
+                                                          ctypes.c_size_t]
             lib.ref_oracle_pipeline.argtypes = [ctypes.POINTER(ctypes.c_char_p), ctypes.c_size_t,
                                                 ctypes.POINTER(CGrid), ctypes.POINTER(CRules),
                                                 vp, vp, ctypes.c_char_p, ctypes.c_size_t]
@@ -160,6 +184,24 @@ class Ref:
         if rc:
             raise RefError(rc, err.value.decode())
         return planes, rawa, st.as_dict(), list(st.stage_seconds)
+
+    def run_pipeline_from_records(self, records, spec, rules=None, n_partitions=1, n_threads=1):
+        """cvl::run_pipeline_from_records over record tuples (see record_array)"""
+        t, _, r, c = dims(spec)
+        planes = np.zeros((t, 8, r, c), dtype=np.uint32)
+        rawa = np.zeros((t, 4, r, c), dtype=np.uint32)
+        arr = record_array(records)
+        st = CStats()
+        err = ctypes.create_string_buffer(512)
+        rc = self.lib.ref_run_pipeline_from_records(ctypes.addressof(arr), len(records),
+                                                    ctypes.byref(grid_struct(spec)),
+                                                    ctypes.byref(rules_struct(rules)), n_partitions,
+                                                    n_threads, planes.ctypes.data_as(ctypes.c_void_p),
+                                                    rawa.ctypes.data_as(ctypes.c_void_p),
+                                                    ctypes.byref(st), err, 512)
+        if rc:
+            raise RefError(rc, err.value.decode())
+        return planes, rawa, st.as_dict()
 
     def oracle_pipeline(self, paths, spec, rules=None):
         t, _, r, c = dims(spec)

@@ -188,6 +188,56 @@ int ref_run_pipeline(const char* const* paths, size_t n_paths, const ref_grid* g
     }
 }
 
+// one parsed record with provenance (layout = cvlg_record in include/cvlg.h)
+struct ref_record_prov {
+    const char* journey_id;
+    uint32_t journey_len;
+    uint32_t postal_len;
+    const char* postal_code;
+    const char* shard_path;
+    uint32_t shard_path_len;
+    uint32_t reserved;
+    int64_t line_number;
+    int64_t epoch_sec;
+    double latitude, longitude, speed, heading;
+};
+
+// -> cvl::run_pipeline_from_records (aggregate.hpp:130-133)
+int ref_run_pipeline_from_records(const ref_record_prov* recs, size_t n, const ref_grid* grid,
+                                  const ref_rules* rules, uint32_t n_partitions, uint32_t n_threads,
+                                  uint32_t* planes, uint32_t* raw, ref_stats* stats, char* err,
+                                  size_t errlen) {
+    try {
+        std::vector<std::pair<CvRecord, RecordProvenance>> records;
+        records.reserve(n);
+        for (size_t i = 0; i < n; ++i) {
+            const ref_record_prov& r = recs[i];
+            CvRecord rec;
+            rec.journey_id.assign(r.journey_id ? r.journey_id : "", r.journey_len);
+            rec.timestamp.epoch_sec = r.epoch_sec;
+            rec.latitude = r.latitude;
+            rec.longitude = r.longitude;
+            rec.postal_code.assign(r.postal_code ? r.postal_code : "", r.postal_len);
+            rec.speed = r.speed;
+            rec.heading = r.heading;
+            RecordProvenance prov;
+            prov.shard_path.assign(r.shard_path ? r.shard_path : "", r.shard_path_len);
+            prov.line_number = r.line_number;
+            records.emplace_back(std::move(rec), std::move(prov));
+        }
+        PipelineStats st;
+        const auto frames = run_pipeline_from_records(records, to_spec(grid), to_rules(rules),
+                                                      n_partitions, n_threads, &st);
+        frames_to_planes(frames, planes, raw);
+        fill_stats(st, stats);
+        return 0;
+    } catch (const CvlError& e) {
+        return fail_code(e, err, errlen);
+    } catch (const std::exception& e) {
+        return fail_other(e, err, errlen);
+    }
+}
+
 int ref_oracle_pipeline(const char* const* paths, size_t n_paths, const ref_grid* grid,
                         const ref_rules* rules, uint32_t* planes, uint32_t* raw, char* err,
                         size_t errlen) {

@@ -6,5 +6,5 @@ is the Python host mirror of the reference pipeline API on top of it (see cvlg.p
 from .cvlg import (  # noqa: F401
     BatchFrame, Context, CvlError, FilterRules, GridSpec, Lattice, MultiGPU, PipelineStats,
     journey_features_device, journey_features_host, journey_ids, launch_count, pin_host, run_pipeline, run_pipeline_device,
-    run_pipeline_host, synth_day, unpin_host, write_container,
+    run_pipeline_host, run_pipeline_from_records, synth_day, unpin_host, write_container,
 )

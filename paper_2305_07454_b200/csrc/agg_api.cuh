@@ -73,6 +73,14 @@ struct FoldParams {
     uint32_t* dead_count;
     uint32_t* abort_flag;     // set by a failed spill insert: every warp stops (the host re-runs)
     uint32_t flush_slack;     // chunk-end flush of closed windows once n_cells + slack >= table size
+    // records entry point (nullable): payload columns by record index (loff = record index), so
+    // the conflict test compares records instead of re-parsing lines
+    const double* r_lat;
+    const double* r_lon;
+    const double* r_speed;
+    const double* r_heading;
+    const uint64_t* r_postal;
+    const uint8_t* r_postal_arena;
     // conflict re-parse
     const uint8_t* csv;
     const uint64_t* shard_off;

@@ -441,6 +441,17 @@ __device__ bool payload_equal(const FoldParams& P, uint64_t la, uint64_t lb) {
     return bytes_equal(pa + a.postal_begin, pb + b.postal_begin, static_cast<uint32_t>(a.postal_len));
 }
 
+// records entry point: CvRecord::operator== minus the dedup key (id and time are equal)
+__device__ bool payload_equal_rec(const FoldParams& P, uint64_t a, uint64_t b) {
+    if (!(P.r_lat[a] == P.r_lat[b] && P.r_lon[a] == P.r_lon[b] && P.r_speed[a] == P.r_speed[b] &&
+          P.r_heading[a] == P.r_heading[b]))
+        return false;
+    const uint64_t pa = P.r_postal[a], pb = P.r_postal[b];
+    if ((pa >> 40) != (pb >> 40)) return false;
+    return bytes_equal(P.r_postal_arena + (pa & ((1ull << 40) - 1)),
+                       P.r_postal_arena + (pb & ((1ull << 40) - 1)), static_cast<uint32_t>(pa >> 40));
+}
+
 // ---- F: per-journey fold -----------------------------------------------------------------------
 // One LANE per journey (dynamic assignment), so the inherently sequential per-(cell, journey)
 // left fold (aggregate.cpp:349-356) runs with every lane busy. Each window the warp stages the
@@ -786,7 +797,9 @@ __global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_ker
                     const int64_t t = s_ts[warp][lane][kSlow ? k : 0];
                     if (have_prev && t == prev_ts) {  // duplicate key: dropped before filtering
                         ++c_dup;
-                        if (!payload_equal(P, P.loff[slot], P.loff[surv])) ++c_conf;
+                        const bool same = P.r_lat ? payload_equal_rec(P, P.loff[slot], P.loff[surv])
+                                                  : payload_equal(P, P.loff[slot], P.loff[surv]);
+                        if (!same) ++c_conf;
                         continue;
                     }
                     have_prev = true;

@@ -746,4 +746,93 @@ void launch_decode(const DecodeParams& p, uint32_t tile_begin, uint32_t n_tiles,
     decode_kernel<<<ctas, kDecodeThreads, sizeof(DecodeSmem), s>>>(p, tile_begin);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Records entry point: one CTA per tile of kLineCap records (provenance order). Codes come from
+// filter_reason (aggregate.cpp:48-56: MissingField for an empty id when drop_missing, then the
+// grid filters) and the binning of grid.cpp; run heads are decided exactly as K1 decides them
+// (id change or non-increasing timestamp vs. the previous record; the tile's first record is a
+// head); thread 0 writes the tile's head list in order.
+constexpr int kRecThreads = 128;
+
+__device__ __forceinline__ bool arena_equal(const uint8_t* a, uint64_t ia, uint64_t ib) {
+    const uint32_t la = static_cast<uint32_t>(ia >> 40), lb = static_cast<uint32_t>(ib >> 40);
+    if (la != lb) return false;
+    const uint8_t* pa = a + (ia & ((1ull << 40) - 1));
+    const uint8_t* pb = a + (ib & ((1ull << 40) - 1));
+    for (uint32_t i = 0; i < la; ++i)
+        if (pa[i] != pb[i]) return false;
+    return true;
+}
+
+__global__ void __launch_bounds__(kRecThreads) records_decode_kernel(RecordsDecodeParams P) {
+    __shared__ uint32_t s_code[kLineCap];
+    __shared__ long long s_ts[kLineCap];
+    __shared__ unsigned long long s_id[kLineCap];
+    __shared__ uint8_t s_head[kLineCap];
+    __shared__ uint32_t s_trans;
+    const uint32_t t = blockIdx.x;
+    const uint64_t base = static_cast<uint64_t>(t) * kLineCap;
+    const uint32_t cnt = static_cast<uint32_t>(P.n - base < kLineCap ? P.n - base : kLineCap);
+    if (threadIdx.x == 0) s_trans = 0;
+    for (uint32_t k = threadIdx.x; k < cnt; k += kRecThreads) {
+        const uint32_t r = P.perm[base + k];
+        const int64_t ts = P.ts[r];
+        const uint64_t id = P.id[r];
+        uint32_t code;
+        if (P.grid.drop_missing && (id >> 40) == 0) code = kCodeMissingField;
+        else code = cell_code(ts, P.lat[r], P.lon[r], P.speed[r], P.heading[r], P.grid);
+        P.out.ts[base + k] = ts;
+        P.out.speed[base + k] = P.speed[r];
+        P.out.loff[base + k] = r;
+        s_code[k] = code;
+        s_ts[k] = ts;
+        s_id[k] = id;
+    }
+    __syncthreads();
+    uint32_t trans = 0;
+    for (uint32_t k = threadIdx.x; k < cnt; k += kRecThreads) {
+        bool head = true;
+        if (k > 0 && s_ts[k - 1] < s_ts[k] && arena_equal(P.arena, s_id[k - 1], s_id[k])) head = false;
+        if (!head && s_code[k - 1] != s_code[k]) ++trans;
+        s_head[k] = head ? 1 : 0;
+        P.out.code[base + k] = head ? (s_code[k] | kHeadBit) : s_code[k];
+    }
+    if (trans) atomicAdd(&s_trans, trans);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t h = 0;
+        for (uint32_t k = 0; k < cnt; ++k) {
+            if (!s_head[k]) continue;
+            const uint64_t id = s_id[k];
+            const uint32_t len = static_cast<uint32_t>(id >> 40);
+            P.out.hslot[base + h] = static_cast<uint32_t>(base + k);
+            P.out.hid[base + h] = id;
+            ulonglong2 key;
+            key.x = 0;
+            key.y = kNoKey;
+            if (len <= 15) {  // dict_insert's inline key: bytes 0..7 BE, bytes 8..14 BE << 8 | len
+                const uint8_t* q = P.arena + (id & ((1ull << 40) - 1));
+                uint64_t k0 = 0, k1 = 0;
+                for (uint32_t i = 0; i < 8; ++i) k0 = (k0 << 8) | (i < len ? q[i] : 0u);
+                for (uint32_t i = 8; i < 15; ++i) k1 = (k1 << 8) | (i < len ? q[i] : 0u);
+                key.x = k0;
+                key.y = (k1 << 8) | len;
+            }
+            P.out.hkey[base + h] = key;
+            ++h;
+        }
+        P.out.tiles[t] = make_uint4(static_cast<uint32_t>(base), cnt, static_cast<uint32_t>(base), h);
+        unsigned long long* st = reinterpret_cast<unsigned long long*>(P.stats);
+        atomicAdd(&st[kStRowsRead], static_cast<unsigned long long>(cnt));
+        atomicAdd(&st[kStParsed], static_cast<unsigned long long>(cnt));
+        atomicAdd(&st[kStHeads], static_cast<unsigned long long>(h));
+        if (s_trans) atomicAdd(&st[kStGTransitions], static_cast<unsigned long long>(s_trans));
+    }
+}
+
+void launch_records_decode(const RecordsDecodeParams& p, cudaStream_t s) {
+    if (p.n_tiles == 0) return;
+    records_decode_kernel<<<p.n_tiles, kRecThreads, 0, s>>>(p);
+}
+
 }  // namespace cvlg

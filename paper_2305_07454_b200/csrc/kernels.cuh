@@ -86,4 +86,27 @@ void launch_parse_headers(const uint8_t* csv, const uint64_t* shard_off, uint32_
                           ColumnMap* cmap, uint8_t* good, uint64_t* stats, cudaStream_t s);
 void launch_decode(const DecodeParams& p, uint32_t tile_begin, uint32_t n_tiles, cudaStream_t s);
 
+// Records entry point (cvlg_run_pipeline_records): already-parsed records, in provenance order
+// through perm, fill the same per-slot columns, run heads and tiles as K1 (tiles of kLineCap
+// records, dense). Columns are indexed by record; loff[slot] = the record index.
+struct RecordsDecodeParams {
+    const uint32_t* perm;  // slot order -> record index
+    uint64_t n;
+    const int64_t* ts;
+    const double* lat;
+    const double* lon;
+    const double* speed;
+    const double* heading;
+    const uint64_t* id;    // arena offset | length << 40
+    const uint8_t* arena;  // journey id bytes
+    uint64_t arena_len;
+    const uint64_t* postal;       // postal code spans in postal_arena (the fold's conflict test)
+    const uint8_t* postal_arena;
+    uint32_t n_tiles;
+    GridParams grid;
+    DecodeOut out;
+    uint64_t* stats;
+};
+void launch_records_decode(const RecordsDecodeParams& p, cudaStream_t s);
+
 }  // namespace cvlg

@@ -11,6 +11,8 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <string_view>
+#include <unordered_map>
 #include <atomic>
 #include <chrono>
 #include <climits>
@@ -219,15 +221,17 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
               const ColumnMap* h_cmap, const uint8_t* h_good, uint64_t bad_headers,
               const cvlg_grid_spec* spec, const cvlg_filter_rules* rules, uint32_t* d_planes,
               uint32_t* d_raw, cvlg_stats* out_stats, const MarkSource& next_mark,
-              bool partial, const double* feat_stop_speed) {
+              bool partial, const double* feat_stop_speed, const RecordsDecodeParams* records) {
     const bool feat = feat_stop_speed != nullptr;
+    if (records && feat) fail(CVLG_E_INVALID_ARG, "features are not available for records input");
     const Dims dims = validate_grid(spec);
     c->csv_in = d_csv;
     const GridParams gp = make_params(spec, rules, dims);
     cudaStream_t s = c->stream;
     const uint32_t n_shards = static_cast<uint32_t>(shard_off.size() - 1);
-    const uint64_t total = shard_off.back();
-    const uint64_t n_tiles = (total + kTile - 1) / kTile;
+    const uint64_t total = records ? records->arena_len : shard_off.back();
+    // (records input: tiles of kLineCap parsed records, dense)
+    const uint64_t n_tiles = records ? (records->n + kLineCap - 1) / kLineCap : (total + kTile - 1) / kTile;
     if (n_tiles >= (1ull << 32)) fail(CVLG_E_UNSUPPORTED, "input larger than 64 TiB");
 
     c->h_small.ensure(4096);
@@ -299,40 +303,52 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         P.out.ovf_head_cap = ovf_cap;
         init_run_kernel<<<1, 32, 0, s>>>(d_stats);
         count_launch();
-        if (h_cmap) {
-            if (bad_headers) {
-                hs[0] = bad_headers;
-                CK(cudaMemcpyAsync(d_stats + kStBadHeader, hs, 8, cudaMemcpyHostToDevice, s));
-            }
+        if (records) {  // already-parsed records: fill K1's outputs directly
+            RecordsDecodeParams RP = *records;
+            RP.n_tiles = static_cast<uint32_t>(n_tiles);
+            RP.grid = gp;
+            RP.out = P.out;
+            RP.stats = d_stats;
+            CK(cudaMemsetAsync(c->counter.p, 0, 16, s));
+            CK(cudaEventRecord(c->ev_dec0, s));
+            launch_records_decode(RP, s);
+            count_launch();
         } else {
-            launch_parse_headers(d_csv, P.shard_off, n_shards, c->cmap.as<ColumnMap>(),
-                                 c->good.as<uint8_t>(), d_stats, s);
-            count_launch();
-        }
-        CK(cudaMemsetAsync(c->counter.p, 0, 16, s));
-        CK(cudaEventRecord(c->ev_dec0, s));
-        uint64_t tiles_done = 0;
-        if (attempt == 0) {
-            ChunkMark m;
-            while (next_mark(m)) {
-                const bool last = m.avail_end >= total;
-                const uint64_t t_hi =
-                    last ? n_tiles : std::min<uint64_t>(m.safe_end / kTile, n_tiles);
-                if (m.ready) CK(cudaStreamWaitEvent(s, m.ready, 0));
-                if (t_hi > tiles_done) {
-                    P.avail_end = m.avail_end;
-                    P.tile_end = static_cast<uint32_t>(t_hi);
-                    launch_decode(P, static_cast<uint32_t>(tiles_done), static_cast<uint32_t>(t_hi - tiles_done), s);
-                    count_launch();
-                    tiles_done = t_hi;
+            if (h_cmap) {
+                if (bad_headers) {
+                    hs[0] = bad_headers;
+                    CK(cudaMemcpyAsync(d_stats + kStBadHeader, hs, 8, cudaMemcpyHostToDevice, s));
                 }
+            } else {
+                launch_parse_headers(d_csv, P.shard_off, n_shards, c->cmap.as<ColumnMap>(),
+                                     c->good.as<uint8_t>(), d_stats, s);
+                count_launch();
             }
-            if (tiles_done < n_tiles) fail(CVLG_E_INTERNAL, "input stream ended early");
-        } else if (n_tiles) {
-            P.avail_end = total;
-            P.tile_end = static_cast<uint32_t>(n_tiles);
-            launch_decode(P, 0, static_cast<uint32_t>(n_tiles), s);
-            count_launch();
+            CK(cudaMemsetAsync(c->counter.p, 0, 16, s));
+            CK(cudaEventRecord(c->ev_dec0, s));
+            uint64_t tiles_done = 0;
+            if (attempt == 0) {
+                ChunkMark m;
+                while (next_mark(m)) {
+                    const bool last = m.avail_end >= total;
+                    const uint64_t t_hi =
+                        last ? n_tiles : std::min<uint64_t>(m.safe_end / kTile, n_tiles);
+                    if (m.ready) CK(cudaStreamWaitEvent(s, m.ready, 0));
+                    if (t_hi > tiles_done) {
+                        P.avail_end = m.avail_end;
+                        P.tile_end = static_cast<uint32_t>(t_hi);
+                        launch_decode(P, static_cast<uint32_t>(tiles_done), static_cast<uint32_t>(t_hi - tiles_done), s);
+                        count_launch();
+                        tiles_done = t_hi;
+                    }
+                }
+                if (tiles_done < n_tiles) fail(CVLG_E_INTERNAL, "input stream ended early");
+            } else if (n_tiles) {
+                P.avail_end = total;
+                P.tile_end = static_cast<uint32_t>(n_tiles);
+                launch_decode(P, 0, static_cast<uint32_t>(n_tiles), s);
+                count_launch();
+            }
         }
         CK(cudaEventRecord(c->ev_dec1, s));
         CK(cudaGetLastError());
@@ -638,6 +654,12 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         F.pair_count = d_pairs;
         F.rank_bits = rbits;
         F.journey_counter = c->scal.as<uint64_t>() + 7;
+        F.r_lat = records ? records->lat : nullptr;
+        F.r_lon = records ? records->lon : nullptr;
+        F.r_speed = records ? records->speed : nullptr;
+        F.r_heading = records ? records->heading : nullptr;
+        F.r_postal = records ? records->postal : nullptr;
+        F.r_postal_arena = records ? records->postal_arena : nullptr;
         F.csv = d_csv;
         F.shard_off = P.shard_off;
         F.cmap = P.cmap;
@@ -996,6 +1018,109 @@ void run_host(cvlg_context* c, const uint8_t* const* bufs, const uint64_t* lens,
     if (planes)
         CK(cudaMemcpyAsync(planes, d_planes, lattice_words * 4, cudaMemcpyDeviceToHost, c->stream));
     if (raw) CK(cudaMemcpyAsync(raw, d_raw, raw_words * 4, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+}
+
+// Parsed records (run_pipeline_from_records, aggregate.cpp:454-491): provenance ranks from the
+// sorted unique shard paths (:464-468), columns and id / postal arenas uploaded by record index,
+// a stable device sort by (rank, (uint32) line) gives the slot order, and the pipeline runs from
+// its post-parse stages on (records_decode_kernel fills K1's outputs).
+void run_records(cvlg_context* c, const cvlg_record* recs, size_t n, const cvlg_grid_spec* spec,
+                 const cvlg_filter_rules* rules, uint32_t* planes, uint32_t* raw, cvlg_stats* stats) {
+    const Dims dims = validate_grid(spec);
+    if (n >= (1ull << 32) - 1) fail(CVLG_E_UNSUPPORTED, ">= 2^32-1 records on one device");
+    cudaStream_t s = c->stream;
+    // provenance ranks: lexicographic order of the distinct paths
+    std::unordered_map<std::string_view, uint32_t> path_ix;
+    std::vector<std::string_view> uniq;
+    for (size_t i = 0; i < n; ++i) {
+        const std::string_view v(recs[i].shard_path ? recs[i].shard_path : "", recs[i].shard_path_len);
+        if (path_ix.emplace(v, 0u).second) uniq.push_back(v);
+    }
+    std::sort(uniq.begin(), uniq.end());
+    for (size_t r = 0; r < uniq.size(); ++r) path_ix[uniq[r]] = static_cast<uint32_t>(r);
+    std::vector<uint64_t> key(n), id(n), postal(n);
+    std::vector<int64_t> ts(n);
+    std::vector<double> lat(n), lon(n), speed(n), heading(n);
+    uint64_t id_bytes = 0, postal_bytes = 0;
+    for (size_t i = 0; i < n; ++i) {
+        id_bytes += recs[i].journey_len;
+        postal_bytes += recs[i].postal_len;
+    }
+    if (id_bytes >= (1ull << 40) || postal_bytes >= (1ull << 40)) fail(CVLG_E_UNSUPPORTED, "string arenas too large");
+    std::vector<uint8_t> arena(id_bytes + 16), parena(postal_bytes + 16);
+    uint64_t ia = 0, pa = 0;
+    for (size_t i = 0; i < n; ++i) {
+        const cvlg_record& r = recs[i];
+        const std::string_view v(r.shard_path ? r.shard_path : "", r.shard_path_len);
+        key[i] = (static_cast<uint64_t>(path_ix[v]) << 32) | static_cast<uint32_t>(r.line_number);
+        ts[i] = r.epoch_sec;
+        lat[i] = r.latitude;
+        lon[i] = r.longitude;
+        speed[i] = r.speed;
+        heading[i] = r.heading;
+        if (r.journey_len) std::memcpy(arena.data() + ia, r.journey_id, r.journey_len);
+        id[i] = ia | (static_cast<uint64_t>(r.journey_len) << 40);
+        ia += r.journey_len;
+        if (r.postal_len) std::memcpy(parena.data() + pa, r.postal_code, r.postal_len);
+        postal[i] = pa | (static_cast<uint64_t>(r.postal_len) << 40);
+        pa += r.postal_len;
+    }
+    auto up = [&](DevBuf& b, const void* h, size_t bytes) {
+        b.ensure(bytes + 16);
+        if (bytes) CK(cudaMemcpyAsync(b.p, h, bytes, cudaMemcpyHostToDevice, s));
+    };
+    up(c->r_keys, key.data(), n * 8);
+    up(c->r_ts, ts.data(), n * 8);
+    up(c->r_lat, lat.data(), n * 8);
+    up(c->r_lon, lon.data(), n * 8);
+    up(c->r_speed, speed.data(), n * 8);
+    up(c->r_heading, heading.data(), n * 8);
+    up(c->r_id, id.data(), n * 8);
+    up(c->r_arena, arena.data(), arena.size());
+    up(c->r_postal, postal.data(), n * 8);
+    up(c->r_parena, parena.data(), parena.size());
+    c->r_keys_alt.ensure(n * 8 + 16);
+    c->r_perm.ensure(n * 4 + 16);
+    c->r_perm_alt.ensure(n * 4 + 16);
+    if (n) {
+        iota_kernel<<<blocks_for(n, 256), 256, 0, s>>>(c->r_perm.as<uint32_t>(), n);
+        count_launch();
+        c->scal.ensure(128);
+        c->h_small.ensure(4096);
+        c->sort_tmp.ensure(radix_temp_bytes(n));
+        radix_sort_pairs(c->r_keys.as<uint64_t>(), c->r_perm.as<uint32_t>(), c->r_keys_alt.as<uint64_t>(),
+                         c->r_perm_alt.as<uint32_t>(), n, 0, 64, c->sort_tmp.p, s,
+                         c->scal.as<unsigned long long>() + 4,
+                         reinterpret_cast<unsigned long long*>(h_small64(c) + 40));
+    }
+    RecordsDecodeParams RP{};
+    RP.perm = c->r_perm.as<uint32_t>();
+    RP.n = n;
+    RP.ts = c->r_ts.as<int64_t>();
+    RP.lat = c->r_lat.as<double>();
+    RP.lon = c->r_lon.as<double>();
+    RP.speed = c->r_speed.as<double>();
+    RP.heading = c->r_heading.as<double>();
+    RP.id = c->r_id.as<uint64_t>();
+    RP.arena = c->r_arena.as<uint8_t>();
+    RP.arena_len = id_bytes;
+    RP.postal = c->r_postal.as<uint64_t>();
+    RP.postal_arena = c->r_parena.as<uint8_t>();
+    const uint64_t lattice_words = static_cast<uint64_t>(dims.T) * 8 * dims.RC;
+    const uint64_t raw_words = static_cast<uint64_t>(dims.T) * 4 * dims.RC;
+    c->planes.ensure(lattice_words * 4);
+    uint32_t* d_planes = c->planes.as<uint32_t>();
+    uint32_t* d_raw = nullptr;
+    if (raw) {
+        c->raw.ensure(raw_words * 4);
+        d_raw = c->raw.as<uint32_t>();
+    }
+    std::vector<uint64_t> off{0, id_bytes};
+    run_core(c, RP.arena, off, nullptr, nullptr, 0, spec, rules, d_planes, d_raw, stats,
+             marks_of({ChunkMark{id_bytes, id_bytes, nullptr}}), false, nullptr, &RP);
+    if (planes) CK(cudaMemcpyAsync(planes, d_planes, lattice_words * 4, cudaMemcpyDeviceToHost, s));
+    if (raw) CK(cudaMemcpyAsync(raw, d_raw, raw_words * 4, cudaMemcpyDeviceToHost, s));
     sync(c);
 }
 
@@ -1449,7 +1574,7 @@ void cvlg_context_destroy(cvlg_context* c) {
     DevBuf* bufs[] = {&c->csv,    &c->shard_off, &c->cmap,     &c->good,     &c->counter,
                       &c->stats,  &c->ts,
                       &c->hscr,   &c->hend,      &c->tiles,    &c->thpos,    &c->ts2,
-                      &c->hid_scr, &c->hid, &c->hkey_scr, &c->hkey, &c->rec, &c->run_j, &c->gkeys, &c->gkeys_alt, &c->gvals, &c->gvals_alt, &c->gpieces, &c->gruns, &c->gstart, &c->gj,      &c->runs,     &c->lat,      &c->lon,
+                      &c->hid_scr, &c->hid, &c->hkey_scr, &c->hkey, &c->rec, &c->r_keys, &c->r_keys_alt, &c->r_perm, &c->r_perm_alt, &c->r_ts, &c->r_lat, &c->r_lon, &c->r_speed, &c->r_heading, &c->r_id, &c->r_arena, &c->r_postal, &c->r_parena, &c->run_j, &c->gkeys, &c->gkeys_alt, &c->gvals, &c->gvals_alt, &c->gpieces, &c->gruns, &c->gstart, &c->gj,      &c->runs,     &c->lat,      &c->lon,
                       &c->lat2,    &c->lon2,     &c->f_points, &c->f_tfirst, &c->f_tlast,
                       &c->f_len,   &c->f_step,   &c->f_vmax,   &c->f_acc,    &c->f_dwell,
                       &c->f_stops, &c->f_id,     &c->f_first,  &c->f_cmin,   &c->f_cmax,
@@ -1515,6 +1640,22 @@ int cvlg_run_pipeline_host(cvlg_context* ctx, const uint8_t* const* shard_bufs,
         if (!c) fail(CVLG_E_CUDA, "no CUDA context");
         CK(cudaSetDevice(c->device));
         run_host(c, shard_bufs, shard_lens, n_shards, spec, rules, planes, raw_count, stats);
+    });
+}
+
+int cvlg_run_pipeline_records(cvlg_context* ctx, const cvlg_record* records, size_t n,
+                              const cvlg_grid_spec* spec, const cvlg_filter_rules* rules,
+                              uint32_t n_partitions, uint32_t n_threads, uint32_t* planes,
+                              uint32_t* raw_count, cvlg_stats* stats) {
+    (void)n_threads;
+    return guard([&] {
+        validate_grid(spec);
+        if (n_partitions == 0) fail(CVLG_E_ZERO_PARTITIONS, "ZeroPartitions: n_partitions must be >= 1");
+        if (n && !records) fail(CVLG_E_INVALID_ARG, "NULL records");
+        cvlg_context* c = ctx ? ctx : default_context();
+        if (!c) fail(CVLG_E_CUDA, "no CUDA context");
+        CK(cudaSetDevice(c->device));
+        run_records(c, records, n, spec, rules, planes, raw_count, stats);
     });
 }
 

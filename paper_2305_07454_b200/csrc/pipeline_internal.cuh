@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "../../include/cvlg.h"
+#include "kernels.cuh"
 #include "parse.cuh"
 
 namespace cvlg {
@@ -91,6 +92,9 @@ struct cvlg_context {
     uint32_t fold_epoch = 0;
     bool slow_key_ts = false;
     cvlg::DevBuf planes, raw, rank_slot, x_keys, x_sum, x_cnt;
+    // records entry point (cvlg_run_pipeline_records): columns by record index, provenance sort
+    cvlg::DevBuf r_keys, r_keys_alt, r_perm, r_perm_alt, r_ts, r_lat, r_lon, r_speed, r_heading, r_id,
+        r_arena, r_postal, r_parena;
     // multi-GPU data plane (multi.cu): this GPU's slice of the input, routing state, tuples
     cvlg::DevBuf slice, r_tbytes, r_tbase, r_pobase, r_total, r_lines, r_idcol, r_poff, r_tfirst,
         r_hdr, r_hoff, r_dst, r_err, r_send, tuples, tuples_in, tuples_send, t_counts, t_dst;
@@ -129,7 +133,8 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
               const ColumnMap* h_cmap, const uint8_t* h_good, uint64_t bad_headers,
               const cvlg_grid_spec* spec, const cvlg_filter_rules* rules, uint32_t* d_planes,
               uint32_t* d_raw, cvlg_stats* out_stats, const MarkSource& next_mark,
-              bool partial = false, const double* feat_stop_speed = nullptr);
+              bool partial = false, const double* feat_stop_speed = nullptr,
+              const RecordsDecodeParams* records = nullptr);
 
 // Per-(cell, journey) subtotals of the last partial run -> (cell, key0, key1, sum, count) with
 // exact global journey keys (stride in u64 words between consecutive tuples' fields).

@@ -98,6 +98,9 @@ def _load() -> ctypes.CDLL:
     lib.cvlg_run_pipeline_host.argtypes = [vp, ctypes.POINTER(vp), u64p, ctypes.c_size_t,
                                            ctypes.POINTER(_Grid), ctypes.POINTER(_Rules),
                                            ctypes.c_uint32, vp, vp, ctypes.POINTER(_Stats)]
+    lib.cvlg_run_pipeline_records.argtypes = [vp, vp, ctypes.c_size_t, ctypes.POINTER(_Grid),
+                                              ctypes.POINTER(_Rules), ctypes.c_uint32,
+                                              ctypes.c_uint32, vp, vp, ctypes.POINTER(_Stats)]
     lib.cvlg_run_pipeline_device.argtypes = [vp, vp, u64p, ctypes.c_size_t,
                                              ctypes.POINTER(_Grid), ctypes.POINTER(_Rules), vp,
                                              vp, ctypes.POINTER(_Stats), vp]
@@ -495,6 +498,40 @@ def run_pipeline_host(buffers: Iterable, spec: GridSpec | None = None,
     _check(_lib.cvlg_run_pipeline_host(ctx.handle, parr, larr, n, ctypes.byref(spec._c()),
                                        ctypes.byref(rules._c()), n_partitions, _ptr(planes),
                                        _ptr(rawa), ctypes.byref(st)))
+    if stats is not None:
+        stats._fill(st)
+    return Lattice(planes, rawa)
+
+
+class _Record(ctypes.Structure):  # cvlg_record (include/cvlg.h)
+    _fields_ = [("journey_id", ctypes.c_char_p), ("journey_len", ctypes.c_uint32),
+                ("postal_len", ctypes.c_uint32), ("postal_code", ctypes.c_char_p),
+                ("shard_path", ctypes.c_char_p), ("shard_path_len", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32), ("line_number", ctypes.c_int64),
+                ("epoch_sec", ctypes.c_int64), ("latitude", ctypes.c_double),
+                ("longitude", ctypes.c_double), ("speed", ctypes.c_double),
+                ("heading", ctypes.c_double)]
+
+
+def run_pipeline_from_records(records: Sequence, spec: GridSpec | None = None,
+                              rules: FilterRules | None = None, n_partitions: int = 1,
+                              n_threads: int = 0, stats: PipelineStats | None = None,
+                              ctx: Context | None = None, raw: bool = True) -> Lattice:
+    """cvl::run_pipeline_from_records (aggregate.hpp:130-133): already-parsed records with
+    provenance -> lattice. Each record is (journey_id, epoch_sec, latitude, longitude,
+    postal_code, speed, heading, shard_path, line_number); strings as bytes."""
+    spec = spec or GridSpec()
+    rules = rules or FilterRules()
+    ctx = ctx or default_context()
+    arr = (_Record * max(len(records), 1))()
+    for i, (jid, ts, la, lo, pc, sp, hd, path, line) in enumerate(records):
+        arr[i] = _Record(jid, len(jid), len(pc), pc, path, len(path), 0, line, ts, la, lo, sp, hd)
+    planes, rawa = _alloc(spec, raw)
+    st = _Stats()
+    _check(_lib.cvlg_run_pipeline_records(ctx.handle, ctypes.addressof(arr), len(records),
+                                          ctypes.byref(spec._c()), ctypes.byref(rules._c()),
+                                          n_partitions, n_threads, _ptr(planes), _ptr(rawa),
+                                          ctypes.byref(st)))
     if stats is not None:
         stats._fill(st)
     return Lattice(planes, rawa)

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "cvl/aggregate.hpp"
+#include "cvl/ingest.hpp"
 #include "cvl/lattice_store.hpp"
 #include "cvlg.hpp"
 
@@ -56,6 +57,23 @@ int main(int argc, char** argv) {
     } catch (const cvl::CvlError& e) {
         if (e.code() != cvl::Err::BadGrid) return 16;
     }
+    // the secondary boundary: cvl::run_pipeline_from_records over the same shards' records
+    std::vector<std::pair<cvl::CvRecord, cvl::RecordProvenance>> recs;
+    for (const auto& path : m.shard_paths) {
+        cvl::ShardData sd = cvl::read_shard(path);
+        for (size_t k = 0; k < sd.records.size(); ++k)
+            recs.emplace_back(std::move(sd.records[k]), cvl::RecordProvenance{path, sd.line_numbers[k]});
+    }
+    cvl::PipelineStats ra, rb;
+    const auto rref = cvl::run_pipeline_from_records(recs, spec, rules, 3, 1, &ra);
+    const auto rgpu = cvl::gpu::run_pipeline_from_records(recs, spec, rules, 3, 1, &rb);
+    if (rref.size() != rgpu.size()) return 17;
+    for (size_t t = 0; t < rref.size(); ++t) {
+        if (!rref[t].bitwise_equal(rgpu[t])) return 18;
+        for (int d = 0; d < 4; ++d)
+            if (rref[t].raw_count[d] != rgpu[t].raw_count[d]) return 19;
+    }
+    if (ra.rows_read != rb.rows_read || ra.accepted != rb.accepted || ra.filtered != rb.filtered) return 20;
     std::printf("drop-in identical: %zu frames, %llu records\n", gpu.size(),
                 static_cast<unsigned long long>(b.accepted));
     return 0;

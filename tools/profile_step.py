@@ -18,6 +18,7 @@ ap.add_argument("--shuffle", action="store_true")
 ap.add_argument("--days", type=int, default=1)
 ap.add_argument("--fine", action="store_true")
 ap.add_argument("--mean-duration", type=float, default=500.0)
+ap.add_argument("--print-csv-bytes", action="store_true")
 a = ap.parse_args()
 if a.days > 1:  # c5 shape: day k uses seed 1 + k and date + k; its shards follow day k-1's
     import datetime
@@ -37,6 +38,8 @@ else:
                                       mean_duration=a.mean_duration)
 if a.shuffle:  # adversarial variant: the full-sort path
     blob, offs = cvlg.cvlg.shuffle_rows(blob, offs, a.shards, seed=7)
+if a.print_csv_bytes:
+    print("csv_bytes", int(offs[-1]), flush=True)
 spec = cvlg.GridSpec(lat_step=0.01, lon_step=0.01, min_step=1) if a.fine else cvlg.GridSpec()
 T, _, R, C = spec.dims()
 d_csv = torch.from_numpy(blob).cuda()
