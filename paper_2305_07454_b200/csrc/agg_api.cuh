@@ -138,6 +138,7 @@ struct DensifyParams {
     uint32_t* code_out;
     uint64_t* loff_out;
     ulonglong2* rec_out;  // nullable: (speed bits, code) interleaved for the slow fold's gathers
+    long long* ts_mm;     // nullable: min / max epoch over non-rejected slots (init LLONG_MAX / MIN)
     uint32_t* hslot_out;
 };
 
@@ -179,7 +180,8 @@ void launch_gather_rank_keys(const uint32_t* rank_src, const uint32_t* vals, uin
 void launch_head_order_check(const uint32_t* perm, const uint32_t* hrank, const uint32_t* hslot,
                              const uint32_t* hend, const int64_t* ts, const uint32_t* code,
                              uint64_t n_heads, uint32_t* jstart, uint32_t* invalid, cudaStream_t s);
-void launch_slot_keys(const uint32_t* hslot, const uint32_t* hrank, uint64_t n_heads,
+void launch_slot_keys(const uint32_t* hslot, const uint32_t* hrank, const uint32_t* hdict,
+                      const uint32_t* rank_of_slot, uint64_t n_heads,
                       const int64_t* ts, const uint32_t* code, uint64_t n_slots, int64_t ts_min,
                       int tsbits, int mode, uint32_t reject_rank, uint64_t* keys, uint32_t* vals,
                       uint32_t* srank, cudaStream_t s);

@@ -118,6 +118,7 @@ __global__ void densify_kernel(DensifyParams D) {
     const int lane = threadIdx.x & 31;
     const uint4 v = D.tiles[t];
     const uint32_t dst = D.lpos[t];
+    long long t_lo = LLONG_MAX, t_hi = LLONG_MIN;  // kept epochs (the slow sort's key range)
     // four rounds of loads in flight before their stores (memory-level parallelism)
     for (uint32_t k0 = lane; k0 < v.y; k0 += 128) {
         int64_t ts[4];
@@ -142,6 +143,10 @@ __global__ void densify_kernel(DensifyParams D) {
                 D.speed_out[dst + k] = sp[u];
                 D.code_out[dst + k] = cd[u];
                 D.loff_out[dst + k] = lo[u];
+                if ((cd[u] & kCodeMask) != kCodeRejected) {
+                    t_lo = ts[u] < t_lo ? ts[u] : t_lo;
+                    t_hi = ts[u] > t_hi ? ts[u] : t_hi;
+                }
                 if (D.rec_out) {
                     ulonglong2 r;
                     r.x = static_cast<unsigned long long>(__double_as_longlong(sp[u]));
@@ -149,6 +154,18 @@ __global__ void densify_kernel(DensifyParams D) {
                     D.rec_out[dst + k] = r;
                 }
             }
+        }
+    }
+    if (D.ts_mm) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const long long a = __shfl_xor_sync(0xFFFFFFFFu, t_lo, o), b = __shfl_xor_sync(0xFFFFFFFFu, t_hi, o);
+            t_lo = a < t_lo ? a : t_lo;
+            t_hi = b > t_hi ? b : t_hi;
+        }
+        if (lane == 0 && t_lo <= t_hi) {
+            atomicMin(&D.ts_mm[0], t_lo);
+            atomicMax(&D.ts_mm[1], t_hi);
         }
     }
     if (D.lat) {
@@ -210,7 +227,11 @@ __global__ void dict_insert_kernel(DictParams D) {
         slot = mix64(fnv) & D.mask;
     }
     const uint32_t wmax = __reduce_max_sync(__activemask(), len);
-    if (len == wmax) {  // one atomic per warp (ties: all equal lanes, harmless)
+    // one atomic per warp, and only while the warp's longest id is longer than what is already
+    // recorded: every head of a journey inserts the same id, so the shared maximum is settled by
+    // the first warps and later warps only read it (row-shuffled input has a head per line:
+    // 1.6M same-address atomics otherwise)
+    if (len == wmax && wmax > ld_relaxed_u64(reinterpret_cast<const uint64_t*>(D.max_len))) {
         const uint32_t lanes = __match_any_sync(__activemask(), len);
         if ((threadIdx.x & 31) == __ffs(lanes) - 1) atomicMax(D.max_len, static_cast<unsigned long long>(len));
     }
@@ -390,7 +411,8 @@ __global__ void ts_range_init_kernel(long long* mm) {
 
 // Same keys without a search: one thread per run head writes its run's slots (dense layout: a
 // run ends at the next head), thread 0 also the slots before the first head (rejected lines).
-__global__ void run_keys_kernel(const uint32_t* hslot, const uint32_t* hrank, uint64_t n_heads,
+__global__ void run_keys_kernel(const uint32_t* hslot, const uint32_t* hrank, const uint32_t* hdict,
+                                const uint32_t* rank_of_slot, uint64_t n_heads,
                                 const int64_t* ts, const uint32_t* code, uint64_t n_slots,
                                 int64_t ts_min, int tsbits, int mode, uint32_t reject_rank,
                                 uint64_t* keys, uint32_t* vals, uint32_t* srank) {
@@ -407,7 +429,7 @@ __global__ void run_keys_kernel(const uint32_t* hslot, const uint32_t* hrank, ui
     if (h == 0)
         for (uint64_t i = 0; i < hslot[0]; ++i) put(i, reject_rank);
     const uint64_t end = h + 1 < n_heads ? hslot[h + 1] : n_slots;
-    const uint32_t r = hrank[h];
+    const uint32_t r = hrank ? hrank[h] : rank_of_slot[hdict[h]];
     for (uint64_t i = hslot[h]; i < end; ++i) put(i, r);
 }
 
@@ -1290,7 +1312,8 @@ void launch_head_order_check(const uint32_t* perm, const uint32_t* hrank, const 
     count_launch();
 }
 
-void launch_slot_keys(const uint32_t* hslot, const uint32_t* hrank, uint64_t n_heads,
+void launch_slot_keys(const uint32_t* hslot, const uint32_t* hrank, const uint32_t* hdict,
+                      const uint32_t* rank_of_slot, uint64_t n_heads,
                       const int64_t* ts, const uint32_t* code, uint64_t n_slots, int64_t ts_min,
                       int tsbits, int mode, uint32_t reject_rank, uint64_t* keys, uint32_t* vals,
                       uint32_t* srank, cudaStream_t s) {
@@ -1299,7 +1322,7 @@ void launch_slot_keys(const uint32_t* hslot, const uint32_t* hrank, uint64_t n_h
                                                                 n_slots, ts_min, tsbits, mode,
                                                                 reject_rank, keys, vals, srank);
     } else {
-        run_keys_kernel<<<grid_for(n_heads, 256), 256, 0, s>>>(hslot, hrank, n_heads, ts, code,
+        run_keys_kernel<<<grid_for(n_heads, 256), 256, 0, s>>>(hslot, hrank, hdict, rank_of_slot, n_heads, ts, code,
                                                                n_slots, ts_min, tsbits, mode,
                                                                reject_rank, keys, vals, srank);
     }

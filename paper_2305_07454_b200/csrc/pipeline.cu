@@ -484,7 +484,12 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         launch_rank_slot(c->uslot.as<uint32_t>(), c->vals.as<uint32_t>(), J,
                          c->rank_slot.as<uint32_t>(), s);
         c->hrank.ensure(H * 4);
-        launch_head_rank(c->hdict.as<uint32_t>(), c->rank_of_slot.as<uint32_t>(), H,
+        // runs averaging < 4 records (row-shuffled input) go straight to the full sort, whose keys
+        // take the rank from (hdict, rank_of_slot) directly: the head rank list is then only
+        // needed by the feature table
+        const bool pre_slow = H * 4 > n_parsed;
+        if (!pre_slow || feat)
+            launch_head_rank(c->hdict.as<uint32_t>(), c->rank_of_slot.as<uint32_t>(), H,
                          c->hrank.as<uint32_t>(), s);
         TRACE("dict sorted");
 
@@ -496,7 +501,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         uint32_t* jstart = c->jstart.as<uint32_t>();
         // runs averaging < 4 records (row-shuffled input): the run merge cannot pay, go straight
         // to the full sort (the head sort + order check would cost as much as the sort itself)
-        slow = H * 4 > n_parsed;
+        slow = pre_slow;
         if (!slow) {
             const int rbits = bits_for(J - 1);
             const int mode = 1;  // sort by ts, then (stably) by rank
@@ -566,6 +571,13 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             DZ.loff_out = c->loff2.as<uint64_t>();
             c->rec.ensure(NS * 16 + 16);
             DZ.rec_out = c->rec.as<ulonglong2>();
+            long long* d_mm = reinterpret_cast<long long*>(c->scal.as<uint32_t>() + 18);
+            {
+                const long long init[2] = {LLONG_MAX, LLONG_MIN};
+                std::memcpy(hs + 48, init, 16);
+                CK(cudaMemcpyAsync(d_mm, hs + 48, 16, cudaMemcpyHostToDevice, s));
+            }
+            DZ.ts_mm = d_mm;
             DZ.hslot_out = c->hslot.as<uint32_t>();
             launch_densify(DZ, s);
             std::swap(c->ts, c->ts2);
@@ -584,9 +596,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             int key_tsbits = tsbits;
             int mode = 1;
             {
-                long long* d_mm = reinterpret_cast<long long*>(c->scal.as<uint32_t>() + 18);
-                launch_ts_range(c->ts.as<int64_t>(), c->code.as<uint32_t>(), NS, d_mm, s);
-                CK(cudaMemcpyAsync(hs + 48, d_mm, 16, cudaMemcpyDeviceToHost, s));
+                CK(cudaMemcpyAsync(hs + 48, d_mm, 16, cudaMemcpyDeviceToHost, s));  // (from densify)
                 sync(c);
                 const int64_t lo = static_cast<int64_t>(hs[48]), hi = static_cast<int64_t>(hs[49]);
                 if (lo <= hi) {
@@ -599,14 +609,20 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
                     }
                 }
             }
-            launch_slot_keys(c->hslot.as<uint32_t>(), c->hrank.as<uint32_t>(), H,
+            launch_slot_keys(c->hslot.as<uint32_t>(), (!pre_slow || feat) ? c->hrank.as<uint32_t>() : nullptr,
+                             c->hdict.as<uint32_t>(), c->rank_of_slot.as<uint32_t>(), H,
                              c->ts.as<int64_t>(), c->code.as<uint32_t>(), NS, key_ts_min, key_tsbits, mode,
                              static_cast<uint32_t>(J), c->keys.as<uint64_t>(),
                              c->vals.as<uint32_t>(), c->srank.as<uint32_t>(), s);
+            bool in_alt = false;  // (a result in the alternate buffers is swapped in, not copied)
             radix_sort_pairs(c->keys.as<uint64_t>(), c->vals.as<uint32_t>(),
                              c->keys_alt.as<uint64_t>(), c->vals_alt.as<uint32_t>(), NS, 0,
                              mode == 0 ? key_tsbits + rbits : key_tsbits, c->sort_tmp.p, s, d_orand,
-                             h_orand);
+                             h_orand, &in_alt);
+            if (in_alt) {
+                std::swap(c->keys, c->keys_alt);
+                std::swap(c->vals, c->vals_alt);
+            }
             if (mode == 1) {
                 launch_gather_rank_keys(c->srank.as<uint32_t>(), c->vals.as<uint32_t>(), NS,
                                         c->keys.as<uint64_t>(), s);

@@ -400,7 +400,8 @@ uint64_t radix_temp_bytes(uint64_t n) {
 
 void radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,
                       uint64_t n, int begin_bit, int end_bit, void* d_tmp, cudaStream_t s,
-                      unsigned long long* d_orand, unsigned long long* h_orand) {
+                      unsigned long long* d_orand, unsigned long long* h_orand, bool* in_alt) {
+    if (in_alt) *in_alt = false;
     if (n <= 1 || end_bit <= begin_bit) return;
     if (n < (1ull << 30) && d_orand && h_orand) {  // one-sweep passes, planned on the device
         const uint32_t n_tiles = static_cast<uint32_t>((n + kRTile - 1) / kRTile);
@@ -428,6 +429,12 @@ void radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32
                 keys, vals, keys_alt, vals_alt, n, 8 * d, dbase + d * 256,
                 status + static_cast<uint64_t>(d) * n_tiles * 256, counters + d, plan);
             count_launch();
+        }
+        if (in_alt && h_orand) {  // the caller swaps buffers instead of a copy pass
+            cudaMemcpyAsync(h_orand, plan + 8, 4, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            *in_alt = *reinterpret_cast<const uint32_t*>(h_orand) != 0;
+            return;
         }
         radix_result_copy_kernel<<<static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 148 * 8)), 256, 0, s>>>(
             keys, vals, keys_alt, vals_alt, n, plan);

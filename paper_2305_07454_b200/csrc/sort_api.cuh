@@ -19,8 +19,11 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t*
 uint64_t radix_temp_bytes(uint64_t n);
 // Stable LSD sort of (keys, vals) on key bits [begin_bit, end_bit). Result in (keys, vals).
 // d_orand (2 x u64 device) + h_orand (2 x u64 pinned host) enable constant-digit skipping.
+// With `in_alt` (host flag out), the one-sweep path does not copy a result that ended in the
+// alternate buffers back: it waits for the pass plan and sets *in_alt instead (the caller swaps).
 void radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,
                       uint64_t n, int begin_bit, int end_bit, void* d_tmp, cudaStream_t s,
-                      unsigned long long* d_orand, unsigned long long* h_orand);
+                      unsigned long long* d_orand, unsigned long long* h_orand,
+                      bool* in_alt = nullptr);
 
 }  // namespace cvlg
