@@ -525,7 +525,11 @@ template <bool kSlow>
 #ifndef CVLG_FOLD_MINB
 #define CVLG_FOLD_MINB 1
 #endif
-__global__ void __launch_bounds__(kFoldWarps * 32, CVLG_FOLD_MINB) fold_lane_kernel(FoldParams P) {
+#ifndef CVLG_FOLD_MINB_SLOW
+#define CVLG_FOLD_MINB_SLOW 4  // the slow path waits on gathers: 4 CTAs per SM (128 registers)
+#endif
+__global__ void __launch_bounds__(kFoldWarps * 32, kSlow ? CVLG_FOLD_MINB_SLOW : CVLG_FOLD_MINB)
+    fold_lane_kernel(FoldParams P) {
     constexpr int kLaneCells = kSlow ? kLaneCellsSlow : kLaneCellsFast;
     constexpr int kCh = kSlow ? kChunk : kChunkFast;
     __shared__ uint32_t s_code[kFoldWarps][32][kCh + 1];
