@@ -145,7 +145,8 @@ struct DensifyParams {
 void launch_tile_field(const uint4* tiles, uint64_t n, int field, uint32_t* out, cudaStream_t s);
 void launch_heads_compact(const uint4* tiles, uint64_t n, const uint32_t* hpos, const uint32_t* hscr,
                           const uint64_t* hid_scr, const ulonglong2* hkey_scr, uint32_t* hslot,
-                          uint32_t* hend, uint64_t* hid, ulonglong2* hkey, cudaStream_t s);
+                          uint32_t* hend, uint64_t* hid, ulonglong2* hkey, cudaStream_t s,
+                          const DictParams* dict = nullptr);
 void launch_densify(const DensifyParams& d, cudaStream_t s);
 void launch_ts_range(const int64_t* ts, const uint32_t* code, uint64_t n, long long* mm, cudaStream_t s);
 void launch_dict_insert(const DictParams& d, cudaStream_t s);

@@ -70,12 +70,16 @@ __global__ void tile_field_kernel(const uint4* tiles, uint64_t n, int field, uin
     out[t] = field == 0 ? v.x : field == 1 ? v.y : field == 2 ? v.z : v.w;
 }
 
+__device__ uint32_t dict_insert_one(const DictParams& D, uint64_t id, ulonglong2 hk);
+
 // heads in tile order (= provenance order for regular tiles); a run ends at the next head of its
 // tile or at the tile's last line (runs never cross tiles: a tile's first line is always a head)
+// With D.table set, each head's journey id is also inserted into the dictionary on the way
+// (hdict at its dense index), so the dense key list is never written or read back.
 __global__ void heads_compact_kernel(const uint4* tiles, uint64_t n, const uint32_t* hpos,
                                      const uint32_t* hscr, const uint64_t* hid_scr,
                                      const ulonglong2* hkey_scr, uint32_t* hslot, uint32_t* hend,
-                                     uint64_t* hid, ulonglong2* hkey) {
+                                     uint64_t* hid, ulonglong2* hkey, DictParams D) {
     // one thread per tile (journey-ordered input: a head or two per tile); tiles with many heads
     // (shuffled rows) are copied by the whole warp afterwards
     const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -92,7 +96,8 @@ __global__ void heads_compact_kernel(const uint4* tiles, uint64_t n, const uint3
             hslot[base + i] = hscr[v.z + i];
             hend[base + i] = i + 1 < v.w ? hscr[v.z + i + 1] : v.x + v.y;
             hid[base + i] = hid_scr[v.z + i];
-            hkey[base + i] = hkey_scr[v.z + i];
+            if (D.table) D.hdict[base + i] = dict_insert_one(D, hid_scr[v.z + i], hkey_scr[v.z + i]);
+            else hkey[base + i] = hkey_scr[v.z + i];
         }
     }
     uint32_t big = __ballot_sync(0xFFFFFFFFu, !small);
@@ -106,7 +111,8 @@ __global__ void heads_compact_kernel(const uint4* tiles, uint64_t n, const uint3
             hslot[bb + i] = hscr[z + i];
             hend[bb + i] = i + 1 < w ? hscr[z + i + 1] : x + y;
             hid[bb + i] = hid_scr[z + i];
-            hkey[bb + i] = hkey_scr[z + i];
+            if (D.table) D.hdict[bb + i] = dict_insert_one(D, hid_scr[z + i], hkey_scr[z + i]);
+            else hkey[bb + i] = hkey_scr[z + i];
         }
     }
 }
@@ -183,16 +189,12 @@ __global__ void densify_kernel(DensifyParams D) {
 // longer ids by (FNV-1a high 40 bits | len, offset << 8 | 0xFF) with a byte comparison.
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0u, 0x0123u); }
 
-__global__ void dict_insert_kernel(DictParams D) {
-    const uint64_t h = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    if (h >= D.n_heads) return;
-    const uint64_t id = D.hid[h];
+__device__ uint32_t dict_insert_one(const DictParams& D, uint64_t id, ulonglong2 hk) {
     const uint64_t off = id & ((1ull << 40) - 1);
     const uint32_t len = static_cast<uint32_t>(id >> 40);
     const uint8_t* p = D.csv + off;
     uint64_t e0, e1, slot;
     const bool is_long = len > 15;
-    const ulonglong2 hk = D.hkey[h];
     if (hk.y != kNoKey) {  // K1 assembled the key from the staged tile (no CSV gather)
         e0 = hk.x;
         e1 = hk.y;
@@ -258,7 +260,13 @@ __global__ void dict_insert_kernel(DictParams D) {
         }
         slot = (slot + 1) & D.mask;
     }
-    D.hdict[h] = static_cast<uint32_t>(slot);
+    return static_cast<uint32_t>(slot);
+}
+
+__global__ void dict_insert_kernel(DictParams D) {
+    const uint64_t h = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (h >= D.n_heads) return;
+    D.hdict[h] = dict_insert_one(D, D.hid[h], D.hkey[h]);
 }
 
 // ---- D2: occupied slots -> flags for compaction ---------------------------------------------
@@ -1235,10 +1243,13 @@ void launch_tile_field(const uint4* tiles, uint64_t n, int field, uint32_t* out,
 
 void launch_heads_compact(const uint4* tiles, uint64_t n, const uint32_t* hpos, const uint32_t* hscr,
                           const uint64_t* hid_scr, const ulonglong2* hkey_scr, uint32_t* hslot,
-                          uint32_t* hend, uint64_t* hid, ulonglong2* hkey, cudaStream_t s) {
+                          uint32_t* hend, uint64_t* hid, ulonglong2* hkey, cudaStream_t s,
+                          const DictParams* dict) {
     if (!n) return;
+    DictParams D{};
+    if (dict) D = *dict;
     heads_compact_kernel<<<grid_for(n, 256), 256, 0, s>>>(tiles, n, hpos, hscr, hid_scr, hkey_scr, hslot,
-                                                          hend, hid, hkey);
+                                                          hend, hid, hkey, D);
     count_launch();
 }
 

@@ -408,11 +408,6 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         exclusive_scan_u32(c->flags.as<uint32_t>(), c->thpos.as<uint32_t>(), n_tiles, nullptr,
                            c->scan_tmp.as<uint32_t>(), s);
         c->hid.ensure(H * 8 + 8);
-        c->hkey.ensure(H * 16 + 16);
-        launch_heads_compact(c->tiles.as<uint4>(), n_tiles, c->thpos.as<uint32_t>(),
-                             c->hscr.as<uint32_t>(), c->hid_scr.as<uint64_t>(),
-                             c->hkey_scr.as<ulonglong2>(), c->hslot.as<uint32_t>(),
-                             c->hend.as<uint32_t>(), c->hid.as<uint64_t>(), c->hkey.as<ulonglong2>(), s);
 
         // ---- journey dictionary ----------------------------------------------------------------
         c->hdict.ensure(H * 4);
@@ -428,14 +423,18 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
             DP.n_shards = n_shards;
             DP.csv_len = total;
             DP.hid = c->hid.as<uint64_t>();
-            DP.hkey = c->hkey.as<ulonglong2>();
+            DP.hkey = nullptr;  // (inserted by heads_compact from K1's per-tile keys)
             DP.n_heads = H;
             DP.table = c->dict.as<unsigned long long>();
             DP.mask = dcap - 1;
             DP.hdict = c->hdict.as<uint32_t>();
             DP.max_len = d_maxlen;
             DP.full = d_dict_full;
-            launch_dict_insert(DP, s);
+            // dense run-head list in tile order + run ends, each head's id inserted on the way
+            launch_heads_compact(c->tiles.as<uint4>(), n_tiles, c->thpos.as<uint32_t>(),
+                                 c->hscr.as<uint32_t>(), c->hid_scr.as<uint64_t>(),
+                                 c->hkey_scr.as<ulonglong2>(), c->hslot.as<uint32_t>(),
+                                 c->hend.as<uint32_t>(), c->hid.as<uint64_t>(), nullptr, s, &DP);
             TRACE("dict inserted");
             launch_dict_flags(c->dict.as<unsigned long long>(), dcap, c->flags.as<uint32_t>(), s);
             exclusive_scan_u32(c->flags.as<uint32_t>(), c->pos.as<uint32_t>(), dcap, d_total,
