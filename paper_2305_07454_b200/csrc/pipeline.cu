@@ -10,6 +10,8 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <string_view>
 #include <unordered_map>
@@ -213,6 +215,22 @@ struct Tracer {
     }
 };
 
+// NVTX ranges over the host-side phases of a run (named like the reference's stage_seconds,
+// aggregate.cpp:370-449): one open range at a time, closed on every exit path.
+struct NvtxStages {
+    bool open = false;
+    void next(const char* name) {
+        if (open) nvtxRangePop();
+        nvtxRangePushA(name);
+        open = true;
+    }
+    void end() {
+        if (open) nvtxRangePop();
+        open = false;
+    }
+    ~NvtxStages() { end(); }
+};
+
 }  // namespace
 
 // The pipeline proper over CSV bytes in HBM. `marks` drive incremental decode while the bytes
@@ -240,6 +258,8 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
     const Tracer TRACE;
 
     CK(cudaEventRecord(c->ev[0], s));
+    NvtxStages nvtx;
+    nvtx.next("cvlg: parse");
     // ---- setup -----------------------------------------------------------------------------
     c->stats.ensure(kStCount * 8);
     d_stats = c->stats.as<uint64_t>();
@@ -361,6 +381,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         ovf_cap = need;  // exact demand of the overflow tiles
     }
     CK(cudaEventRecord(c->ev[1], s));
+    nvtx.next("cvlg: dedup+filter+accumulate");
         TRACE("decode done");
     if (hs[kStOverflow]) fail(CVLG_E_INTERNAL, "decode capacity invariant violated");
     const uint64_t n_parsed = hs[kStParsed];
@@ -818,6 +839,7 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
                                 F.dead_list + pair_room, c->scal.as<uint32_t>() + 26, s);
         }
         CK(cudaEventRecord(c->ev[3], s));
+        nvtx.next("cvlg: merge+finalize");
         const uint64_t n_pairs = n_written - n_dead;
 
         if (feat) {  // per-journey features over the fold's record order (features.cu)
@@ -900,9 +922,11 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
         c->part_long_ids = false;
         CK(cudaEventRecord(c->ev[2], s));
         CK(cudaEventRecord(c->ev[3], s));
+        nvtx.next("cvlg: merge+finalize");
         CK(cudaEventRecord(c->ev[4], s));
     }
     CK(cudaEventRecord(c->ev[5], s));
+    nvtx.end();
     CK(cudaMemcpyAsync(hs, d_stats, kStCount * 8, cudaMemcpyDeviceToHost, s));
     sync(c);
     CK(cudaGetLastError());
@@ -1145,6 +1169,10 @@ void run_records(cvlg_context* c, const cvlg_record* recs, size_t n, const cvlg_
 void run_files(cvlg_context* c, const char* const* paths, size_t n, const cvlg_grid_spec* spec,
                const cvlg_filter_rules* rules, uint32_t n_threads, uint32_t* planes, uint32_t* raw,
                cvlg_stats* stats) {
+    struct Range {  // NVTX: the whole file-to-lattice call (ingest overlaps the parse stage)
+        Range() { nvtxRangePushA("cvlg: run_pipeline(files)"); }
+        ~Range() { nvtxRangePop(); }
+    } range;
     const Dims dims = validate_grid(spec);
     // sizes and header lines (parse_header, ingest.cpp:204-221) before anything streams
     const std::vector<ShardHead> heads = read_shard_heads(paths, n);
