@@ -293,12 +293,13 @@ __global__ void __launch_bounds__(kRThreads, CVLG_OS_MINB) radix_onesweep_kernel
         const bool valid = idx < n;
         const uint32_t d = valid ? (static_cast<uint32_t>(k[i] >> shift) & 0xFFu) : 256u;
         const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
-        uint32_t r = 0;
-        if (valid) r = wc[warp][d] + __popc(peers & lt);
-        __syncwarp();
-        if (valid && (peers & lt) == 0) wc[warp][d] += __popc(peers);
-        __syncwarp();
-        rank[i] = r;
+        // the peer group's leader reserves its ranks with one shared-memory atomic; the returned
+        // count is not needed before the next item's reservation, so the items of a thread do
+        // not form a read-modify-write chain through the counters
+        const int leader = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if (valid && lane == leader) old = atomicAdd(&wc[warp][d], static_cast<uint32_t>(__popc(peers)));
+        rank[i] = __shfl_sync(0xFFFFFFFFu, old, leader) + __popc(peers & lt);
     }
     __syncthreads();
     {
