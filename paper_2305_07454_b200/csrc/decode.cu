@@ -586,6 +586,10 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
             uint32_t my_trans = 0;
 #pragma unroll
             for (int r = 0; r < kRounds; ++r) {
+                if (r > 0 && r * kDecodeThreads >= n_pass) {  // (uniform: no line in this round)
+                    if (lane == 0) S.hbits[r * kNW + warp] = 0u;
+                    continue;
+                }
                 const uint32_t k = r * kDecodeThreads + tid;
                 bool head = false;
                 if (k < n_pass) {
@@ -631,6 +635,7 @@ __global__ void __launch_bounds__(kDecodeThreads, kDecodeCtasPerSm) decode_kerne
             const uint32_t nh = __shfl_sync(0xFFFFFFFFu, incw, kHeadWords - 1);
 #pragma unroll
             for (int r = 0; r < kRounds; ++r) {
+                if (r > 0 && r * kDecodeThreads >= n_pass) break;
                 const uint32_t k = r * kDecodeThreads + tid;
                 const int wd = r * kNW + warp;
                 const uint32_t bits = S.hbits[wd];
