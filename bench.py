@@ -345,10 +345,18 @@ def run_ours(args):
     import torch.distributed as dist
 
     world, rank, local = dist_env()
+    # (CVLG_BENCH_DEVICE / CVLG_BENCH_BACKEND: exercise the N-rank path on fewer GPUs, e.g. two
+    # ranks sharing cuda:0 over gloo; never used for a reported number)
+    if os.environ.get("CVLG_BENCH_DEVICE"):
+        local = int(os.environ["CVLG_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("CVLG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import paper_2305_07454_b200 as cvlg
 
     threads = args.threads or os.cpu_count() or 1
@@ -387,7 +395,8 @@ def run_ours(args):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        on_dev = dist.get_backend() == "nccl"
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}" if on_dev else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
