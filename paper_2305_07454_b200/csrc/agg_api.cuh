@@ -54,6 +54,7 @@ struct FoldParams {
     // bin-group mode (few long journeys): the fold's work items are (journey, time bin) groups of
     // run pieces instead of journeys; jrank[g] is the journey rank of group g (nullable: off)
     const uint32_t* jrank;
+    const uint32_t* jorder;     // nullable: work items in this order (longest first)
     int runs_ready;             // runs[] already built (bin-group mode): skip run_list_kernel
     uint64_t* journey_counter;  // dynamic journey assignment (zeroed before the fold)
     // (cell, journey) table, key = cell << 32 | rank
@@ -150,6 +151,8 @@ void launch_heads_compact(const uint4* tiles, uint64_t n, const uint32_t* hpos, 
 void launch_densify(const DensifyParams& d, cudaStream_t s);
 void launch_ts_range(const int64_t* ts, const uint32_t* code, uint64_t n, long long* mm, cudaStream_t s);
 void launch_dict_insert(const DictParams& d, cudaStream_t s);
+void launch_journey_len_keys(const uint32_t* jstart, uint64_t n, const uint2* runs, int runs_mode,
+                             uint64_t* keys, uint32_t* vals, cudaStream_t s);
 // bin-group mode: runs (perm order) -> pieces split at time-bin changes, keyed (journey, bin,
 // stream order); after sorting the keys, groups of equal (journey, bin)
 void launch_run_list(const uint32_t* perm, const uint32_t* hslot, const uint32_t* hend, uint64_t n,

@@ -555,10 +555,14 @@ __global__ void __launch_bounds__(kFoldWarps * 32, kSlow ? CVLG_FOLD_MINB_SLOW :
     // first journey: spread over every CTA and warp (lane-major), so a run with fewer journeys
     // than lanes still occupies all SMs; later ones come from the shared counter
     const uint64_t n_lanes = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    // work items are handed out longest first when P.jorder is set (a journey index sorted by
+    // record count): the last items any warp picks up are short, so warps do not idle behind one
+    // long straggler once the counter runs out
+    auto order = [&](uint64_t i) -> uint64_t { return P.jorder && i < P.n_journeys ? P.jorder[i] : i; };
     auto next_journey = [&]() {
-        return n_lanes + atomicAdd(reinterpret_cast<unsigned long long*>(P.journey_counter), 1ull);
+        return order(n_lanes + atomicAdd(reinterpret_cast<unsigned long long*>(P.journey_counter), 1ull));
     };
-    uint64_t j = static_cast<uint64_t>(lane * kFoldWarps + warp) * gridDim.x + blockIdx.x;
+    uint64_t j = order(static_cast<uint64_t>(lane * kFoldWarps + warp) * gridDim.x + blockIdx.x);
     bool active = j < P.n_journeys;
     uint32_t ri = 0, re = 0;    // fast path: remaining runs of the journey, [ri, re) in perm
     // fast path prefetch: the next run of this journey (runs[ri]) and the next journey (its run
@@ -1100,6 +1104,21 @@ __global__ void bin_group_starts_kernel(const uint64_t* keys, const uint32_t* fl
     gj[pos[k]] = static_cast<uint32_t>(keys[k] >> (order_bits + bin_bits));
 }
 
+// longest-first work order: key = ~(records of item j) (ascending = longest first), value = j
+__global__ void journey_len_keys_kernel(const uint32_t* jstart, uint64_t n, const uint2* runs,
+                                        int runs_mode, uint64_t* keys, uint32_t* vals) {
+    const uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (j >= n) return;
+    uint64_t len = 0;
+    if (runs_mode) {  // fast path: sum of the item's run lengths
+        for (uint32_t r = jstart[j]; r < jstart[j + 1]; ++r) len += runs[r].y - runs[r].x;
+    } else {
+        len = jstart[j + 1] - jstart[j];
+    }
+    keys[j] = 0xFFFFFFFFull - (len > 0xFFFFFFFFull ? 0xFFFFFFFFull : len);
+    vals[j] = static_cast<uint32_t>(j);
+}
+
 // spilled journeys' subtotals -> pair list
 __global__ void spill_drain_kernel(FoldParams P) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -1458,6 +1477,13 @@ void launch_bin_group_starts(const uint64_t* keys, const uint32_t* flags, const 
     if (!n) return;
     bin_group_starts_kernel<<<grid_for(n, 256), 256, 0, s>>>(keys, flags, pos, n, order_bits, bin_bits,
                                                              gstart, gj);
+    count_launch();
+}
+
+void launch_journey_len_keys(const uint32_t* jstart, uint64_t n, const uint2* runs, int runs_mode,
+                             uint64_t* keys, uint32_t* vals, cudaStream_t s) {
+    if (!n) return;
+    journey_len_keys_kernel<<<grid_for(n, 256), 256, 0, s>>>(jstart, n, runs, runs_mode, keys, vals);
     count_launch();
 }
 

@@ -791,6 +791,29 @@ void run_core(cvlg_context* c, const uint8_t* d_csv, const std::vector<uint64_t>
                 }
             }
         }
+        // ---- longest-first work order (journey mode): sort the work items by record count -------
+        F.jorder = nullptr;
+        {
+            const char* oenv = std::getenv("CVLG_FOLD_ORDER");
+            const uint64_t nj = F.n_journeys;
+            if (!F.jrank && nj > 1 && !(oenv && oenv[0] == '0')) {
+                if (!slow && !F.runs_ready) {
+                    launch_run_list(F.perm, F.hslot, F.hend, H, const_cast<uint2*>(F.runs), s);
+                    F.runs_ready = 1;
+                }
+                c->jo_keys.ensure(nj * 8);
+                c->jo_keys_alt.ensure(nj * 8);
+                c->jo_vals.ensure(nj * 4);
+                c->jo_vals_alt.ensure(nj * 4);
+                c->sort_tmp.ensure(radix_temp_bytes(nj));
+                launch_journey_len_keys(F.jstart, nj, F.runs, slow ? 0 : 1, c->jo_keys.as<uint64_t>(),
+                                        c->jo_vals.as<uint32_t>(), s);
+                radix_sort_pairs(c->jo_keys.as<uint64_t>(), c->jo_vals.as<uint32_t>(),
+                                 c->jo_keys_alt.as<uint64_t>(), c->jo_vals_alt.as<uint32_t>(), nj, 0, 32,
+                                 c->sort_tmp.p, s, d_orand, h_orand);
+                F.jorder = c->jo_vals.as<uint32_t>();
+            }
+        }
         uint64_t scap = pow2_at_least(std::max<uint64_t>(F.win ? 1u << 20 : 1u << 18,
                                                          pair_bound / (F.win && dims.T > 48 ? 16 : 2)));
         F.pair_cap = F.win ? pair_room : pair_bound;
@@ -1617,7 +1640,7 @@ void cvlg_context_destroy(cvlg_context* c) {
     DevBuf* bufs[] = {&c->csv,    &c->shard_off, &c->cmap,     &c->good,     &c->counter,
                       &c->stats,  &c->ts,
                       &c->hscr,   &c->hend,      &c->tiles,    &c->thpos,    &c->ts2,
-                      &c->hid_scr, &c->hid, &c->hkey_scr, &c->hkey, &c->rec, &c->r_keys, &c->r_keys_alt, &c->r_perm, &c->r_perm_alt, &c->r_ts, &c->r_lat, &c->r_lon, &c->r_speed, &c->r_heading, &c->r_id, &c->r_arena, &c->r_postal, &c->r_parena, &c->run_j, &c->gkeys, &c->gkeys_alt, &c->gvals, &c->gvals_alt, &c->gpieces, &c->gruns, &c->gstart, &c->gj,      &c->runs,     &c->lat,      &c->lon,
+                      &c->hid_scr, &c->hid, &c->hkey_scr, &c->hkey, &c->rec, &c->r_keys, &c->r_keys_alt, &c->r_perm, &c->r_perm_alt, &c->r_ts, &c->r_lat, &c->r_lon, &c->r_speed, &c->r_heading, &c->r_id, &c->r_arena, &c->r_postal, &c->r_parena, &c->run_j, &c->jo_keys, &c->jo_keys_alt, &c->jo_vals, &c->jo_vals_alt, &c->gkeys, &c->gkeys_alt, &c->gvals, &c->gvals_alt, &c->gpieces, &c->gruns, &c->gstart, &c->gj,      &c->runs,     &c->lat,      &c->lon,
                       &c->lat2,    &c->lon2,     &c->f_points, &c->f_tfirst, &c->f_tlast,
                       &c->f_len,   &c->f_step,   &c->f_vmax,   &c->f_acc,    &c->f_dwell,
                       &c->f_stops, &c->f_id,     &c->f_first,  &c->f_cmin,   &c->f_cmax,

@@ -81,6 +81,7 @@ struct cvlg_context {
     cvlg::DevBuf csv, shard_off, cmap, good, counter, stats;
     cvlg::DevBuf ts, speed, code, loff, hslot, hscr, hend, tiles, thpos, hid_scr, hid, hkey_scr, hkey, rec, runs;
     cvlg::DevBuf run_j, gkeys, gkeys_alt, gvals, gvals_alt, gpieces, gruns, gstart, gj;  // fold bin groups
+    cvlg::DevBuf jo_keys, jo_keys_alt, jo_vals, jo_vals_alt;  // fold work order (longest first)
     cvlg::DevBuf ts2, speed2, code2, loff2;  // dense copies for the slow (full-sort) path
     // per-journey features (cvlg_journey_features_*): lat/lon per slot, outputs per journey / cell
     cvlg::DevBuf lat, lon, lat2, lon2, f_points, f_tfirst, f_tlast, f_len, f_step, f_vmax, f_acc,
